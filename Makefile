@@ -11,7 +11,7 @@ NCCL_DIR  := $(shell $(PY) -c "import nvidia.nccl, os; print(list(nvidia.nccl.__
 PKG       := paper_1403_5805_b200
 
 LIB_SRCS  := $(PKG)/csrc/sweep.cu $(PKG)/csrc/plan.cu $(PKG)/csrc/dist.cu
-LIB_HDRS  := include/jacobi.h $(PKG)/csrc/internal.h $(PKG)/csrc/sweep_kernels.cuh
+LIB_HDRS  := include/jacobi.h $(PKG)/csrc/internal.h
 
 all: oracle gen lib probe
 

@@ -1,0 +1,344 @@
+#!/usr/bin/env python
+"""Benchmark of the dense Jacobi sweep (BASELINE.json metric: Jacobi iterations/s and effective HBM
+GB/s, % of peak) on the headline workload c4: n = 65536 dense fp64 (34.4 GB), fixed 100 sweeps.
+
+One STEP = one jacobi_plan_solve of the workload (100 sweeps, tol = 0, the whole hot path:
+sweep + fused update + max|dx| + device stop test; + allgather/allreduce when N > 1).
+  value : iterations/s with A, b, x0 resident in HBM (device-pointer solve), CUDA events on the
+          plan's stream, max over ranks.  A (34 GB) >> L2 (126 MB): every sweep streams A from HBM,
+          so no L2 flush is needed between steps.
+  e2e   : the same metric through the C-ABI one-shot call jacobi_solve() with HOST (pinned) buffers:
+          the H2D copy of A, b, x0, plan setup, 100 sweeps and the D2H copy of x are inside the
+          timed region every step (N = 1; under torchrun the distributed plan is created per step
+          from host rows).
+  --impl reference : the CPU oracle (oracle/), as it stands, on the box's host cores, on a bounded
+          row sample of the same workload per step; it/s extrapolated to whole sweeps.
+
+Launch: python bench.py [--gpus N --steps K --warmup W]; N > 1 under torchrun (one rank per GPU).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (gen config key, sweeps per step, tol, description)
+    "c4": ("c4", 100, 0.0, "c4: n=65536 dense fp64 (34.4 GB), off-diag U[-1,1], diag=rowabs+U[1,2], "
+                           "b=A x*, x0=0, fixed 100 iterations, row-block sharded"),
+    "c2": ("c2", 500, 0.0, "c2: n=4096 dense fp64 (134 MB), fixed 500 iterations"),
+    "c5": ("c5", 100, 0.0, "c5 companion: n=131072, A fp32 (68.7 GB), fp64 accumulate, fixed 100 iterations"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["cuda", "reference"], default="cuda")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c4")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU oracle sample budget per run")
+    ap.add_argument("--out", default=None, help="also append the JSON line to this file")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks sampling
+class Clocks:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=5)
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        loaded = [s for s in sm if s > 0.5 * mx] if mx else sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(name):
+    """dram bytes per sweep launch from the committed ncu --set full summary (profiles/)."""
+    p = os.path.join(ROOT, "profiles", "ncu_sweep_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(name, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+# ----------------------------------------------------------------------------- CPU oracle timing
+def cpu_oracle_rate(wname, seconds, steps=None):
+    """Oracle (oracle.sweep_rows) on a bounded row sample of the workload, on all host
+    cores (rows split over threads; ctypes releases the GIL).  Returns (it/s, cores, sample)."""
+    import jacobi_gen as g
+    import oracle
+    cfg = g.CONFIGS[WORKLOADS[wname][0]]
+    n = cfg.n
+    cores = len(os.sched_getaffinity(0))
+    rows = min(n, max(cores * 64, 4096 if n >= 65536 else n))
+    A, b = g.host_rows(cfg, 0, rows)
+    x = g.host_xstar(cfg) * 0.5  # any x^(k-1); the work per row is data independent
+    chunks = np.array_split(np.arange(rows), cores)
+
+    def one_pass():
+        out = [None] * len(chunks)
+
+        def run(t):
+            idx = chunks[t]
+            if len(idx):
+                out[t] = oracle.sweep_rows(A[idx[0]: idx[-1] + 1], int(idx[0]), b[idx[0]: idx[-1] + 1], x)
+
+        th = [threading.Thread(target=run, args=(t,)) for t in range(len(chunks))]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+
+    one_pass()  # warm
+    t0 = time.perf_counter()
+    passes = 0
+    while True:
+        one_pass()
+        passes += 1
+        el = time.perf_counter() - t0
+        if (steps is not None and passes >= steps) or (steps is None and el >= seconds):
+            break
+    rate = passes * rows / n / el
+    sample = f"oracle.sweep_rows over rows [0,{rows}) of {n} x {passes} passes in {el:.2f}s; it/s = passes*rows/n/t"
+    return rate, cores, sample, el
+
+
+# ----------------------------------------------------------------------------- main (GPU arm)
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    gname, sweeps, tol, desc = WORKLOADS[args.workload]
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        per_step = []
+        rate, cores, sample, el = cpu_oracle_rate(args.workload, None, steps=1)  # warm-up + sizing
+        for _ in range(args.warmup):
+            cpu_oracle_rate(args.workload, None, steps=1)
+        t0 = time.perf_counter()
+        rate, cores, sample, el = cpu_oracle_rate(args.workload, None, steps=args.steps)
+        line = {"impl": "reference", "metric": "Jacobi iterations/s", "value": rate, "unit": "it/s",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": desc, "n": 65536 if gname == "c4" else None, "sweeps_per_step": sweeps},
+                "cpu_baseline": {"value": rate, "unit": "it/s", "cores": cores, "kind": "oracle", "sample": sample},
+                "e2e": {"value": rate, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import torch
+    import torch.distributed as dist
+
+    import jacobi_gen as g
+    import paper_1403_5805_b200 as jb
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = g.CONFIGS[gname]
+    n = cfg.n
+    dt = torch.float32 if cfg.a_dtype == g.F32 else torch.float64
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+    row0, m = jb.partition(n, world, rank)
+
+    # ---- resident inputs (device twin of the generator; identical bits to the host generator)
+    dA = torch.empty((m, n), dtype=dt, device="cuda")
+    db = torch.empty(m, dtype=torch.float64, device="cuda")
+    g.device_rows(cfg, row0, row0 + m, dA.data_ptr(), n, db.data_ptr(), sh)
+    dx0 = torch.zeros(n, dtype=torch.float64, device="cuda")
+    dxo = torch.empty(n, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    if world > 1:
+        uid = [jb.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        plan = jb.Plan(dA, n=n, stream=sh, dist=(uid[0], rank, world))
+    else:
+        plan = jb.Plan(dA, n=n, stream=sh)
+    K = 20 if sweeps % 20 == 0 else 4
+    plan.set_batch(K)  # 100 sweeps = 5 graph batches exactly: no no-op overshoot launches
+
+    def step():
+        return plan.solve_device(db, dx0, dxo, sweeps, tol)
+
+    for _ in range(max(3, args.warmup)):
+        r = step()
+    assert r.iters == sweeps and r.status == jb.MAX_ITER
+    info = plan.info
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        launches = 0
+        for _ in range(args.steps):
+            step()
+            li = plan.info
+            launches += li.sweeps_launched + li.sweeps_launched // K + 2  # sweeps + k_advance + 2 scans
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    its = args.steps * sweeps / (ms * 1e-3)
+    sweep_ms = ms / (args.steps * sweeps)  # average sweep (kernel + exchange) duration on the stream
+    bytes_sweep = info.bytes_per_sweep  # per GPU
+    achieved = bytes_sweep / (sweep_ms * 1e-3) / 1e9
+    peak, peak_src = measured_peak_hbm()
+
+    # per-kernel timing (untimed cross-check: events around each sweep kernel alone)
+    kms = plan.time_sweeps(db, dx0, min(sweeps, 20))
+    kernel_ms = float(np.median(kms[1:])) if len(kms) > 1 else float(kms[0])
+
+    ceiling = None
+    if rank == 0:
+        try:
+            ceiling = jb.bwprobe(min(32 << 30, int(bytes_sweep)), 5)
+        except Exception:
+            ceiling = None
+
+    plan.close()
+    del dA, db
+    torch.cuda.empty_cache()
+
+    # ---- e2e through the public C-ABI with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e and world == 1 and args.e2e_steps > 0:
+        hA = torch.empty((n, n), dtype=dt, pin_memory=True)
+        g.host_rows(cfg, 0, n, out=hA.numpy())
+        hb = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        hb.numpy()[:] = g.host_diag_b(cfg, 0, n)[1]
+        hx0 = torch.zeros(n, dtype=torch.float64, pin_memory=True)
+        hx = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        solve_fn = jb._lib.jacobi_solve_f32a if cfg.a_dtype == g.F32 else jb._lib.jacobi_solve
+        import ctypes
+        it = ctypes.c_int64()
+
+        def e2e_step():
+            st = solve_fn(n, hA.data_ptr(), hb.data_ptr(), hx0.data_ptr(), sweeps, tol, hx.data_ptr(), ctypes.byref(it))
+            assert st == jb.MAX_ITER and it.value == sweeps, (st, jb.last_error())
+
+        e2e_step()  # warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        e2e = {"value": args.e2e_steps * sweeps / el, "unit": "it/s",
+               "h2d_bytes_per_step": int(hA.numel() * hA.element_size() + 2 * 8 * n),
+               "d2h_bytes_per_step": int(8 * n + 48), "steps": args.e2e_steps,
+               "api": "jacobi_solve (C-ABI, host pinned buffers; plan setup + H2D + sweeps + D2H per step)"}
+        del hA
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, cores, sample, _ = cpu_oracle_rate(args.workload, args.cpu_seconds)
+        cpu = {"value": rate, "unit": "it/s", "cores": cores, "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": "Jacobi iterations/s", "value": its, "unit": "it/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded counter-based generator, BASELINE.json recipe; device twin)",
+            "config": {"workload": desc, "n": n, "sweeps_per_step": sweeps, "tol": tol,
+                       "parallelism": f"row-block x{world}" + (" + NCCL allgather/allreduce" if world > 1 else ""),
+                       "l2": "A per GPU >> 126 MB L2; each sweep streams A from HBM (no flush needed)",
+                       "graph_batch": K, "chunk_cols": info.chunk_cols, "rows_per_warp": info.rows_per_warp,
+                       "grid": f"{info.grid_ctas}x{info.threads_per_cta}"},
+            "effective_gbs_per_gpu": achieved, "effective_gbs_aggregate": achieved * world,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(args.workload),
+                         "peak_source": peak_src, "kernel": "k_sweep<double,4,2>" if dt == torch.float64 else "k_sweep<float,4,1>",
+                         "bytes_per_launch": bytes_sweep, "avg_launch_ms": sweep_ms,
+                         "kernel_only_ms": kernel_ms, "kernel_only_gbs": bytes_sweep / (kernel_ms * 1e-3) / 1e9,
+                         "read_ceiling_gbs": ceiling,
+                         "frac_of_read_ceiling": (achieved / ceiling) if ceiling else None,
+                         "frac_of_8tbs": achieved / 8000.0},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+        }
+        s = json.dumps(line)
+        print(s, flush=True)
+        if args.out:
+            with open(args.out, "a") as f:
+                f.write(s + "\n")
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

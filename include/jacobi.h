@@ -1,0 +1,138 @@
+/* jacobi.h — C-ABI of the B200-native dense Jacobi sweep.
+ *
+ * Method: Margaris, Souravlas & Roumeliotis, "Parallel implementations of the Jacobi linear
+ * algebraic systems solver" (arXiv:1403.5805); citations are lines of /root/reference/PAPER.md.
+ *
+ *   Sweep (§2 component equation; matrix form X^(k) = T X^(k-1) + C):
+ *       x_i^(k) = ( b_i - sum_{j != i} a_ij x_j^(k-1) ) / a_ii        (one IEEE division)
+ *   Distance (stop test):  d_k = max_i |x_i^(k) - x_i^(k-1)|   (max norm: BASELINE.json north_star;
+ *       PAPER.md:51/94 use the Euclidean norm — DESIGN.md reading R1).  NaN-sticky.
+ *   Loop (§2 pseudocode): k = 1..max_iter; stop after sweep k when d_k < tol
+ *       (strict) -> JACOBI_CONVERGED, iters = k; else after max_iter sweeps -> JACOBI_MAX_ITER,
+ *       iters = max_iter, x = X^(max_iter).  max_iter = 0 returns x0 (MAX_ITER, iters 0).
+ *       tol = 0 is the fixed-iteration mode (never converges).
+ *   Precondition a_ii != 0: violated -> JACOBI_EZERODIAG (lowest such i).
+ *   Row-block distribution (§3 / §3.1): rank r of P owns rows [r*n/P, (r+1)*n/P);
+ *       P must divide n.  Every sweep ends with an allgather of x (the MPI_Allgather variant of
+ *       §3.1, done with NCCL over NVLink) and a one-scalar max allreduce of d_k.
+ *
+ * Conventions (all functions):
+ *   - Sizes are int64_t.  A is row-major: a_ij = A[i*lda + j], lda >= n (elements).  b, x0, x_out
+ *     are fp64 of length n (b: length m = rows owned, for the distributed plan).
+ *   - A is fp64 (JACOBI_F64) or fp32 (JACOBI_F32: values are widened exactly; all arithmetic fp64).
+ *   - Ownership: the caller owns every buffer it passes.  A, b, x0 are read-only and are consumed
+ *     before x_out is written, so x_out may alias x0.  A device-resident A passed to a plan
+ *     (a_on_device = 1) is BORROWED: it must stay valid and unmodified until jacobi_plan_destroy
+ *     (it is copied only when its pointer is not 32-byte aligned or lda is not a multiple of 8).
+ *     The library owns its own device allocations and frees them in jacobi_plan_destroy (or before
+ *     jacobi_solve returns).
+ *   - Outputs (x_out, iters_out, dist_hist) are written only when the status is >= 0.
+ *   - Validation order: JACOBI_EINVAL (n < 1, NULL pointer, lda < n, max_iter < 0, tol < 0 or NaN,
+ *     bad dtype) before any CUDA call; then JACOBI_EINDIVISIBLE (distributed, P does not divide n);
+ *     then JACOBI_EZERODIAG (lowest i, across ranks); then JACOBI_ENONFINITE (any non-finite value
+ *     in A, b or x0).
+ *   - Errors: every negative status sets a thread-local message readable with jacobi_last_error().
+ *     There is no CPU fallback: without a usable CUDA device the status is JACOBI_ECUDA.
+ *   - Determinism: results are bitwise reproducible run to run and bitwise independent of the
+ *     number of ranks / row blocks (the per-row summation order depends only on column indices).
+ *   - Threading: a plan is used by one host thread at a time; distinct plans are independent.
+ *   - Streams: cuda_stream (a cudaStream_t, may be NULL) is the stream every kernel, copy and NCCL
+ *     call of the plan is issued on; NULL makes the plan create its own non-blocking stream.
+ *     Functions return after the work they enqueue has completed (they synchronize that stream).
+ */
+#ifndef JACOBI_H
+#define JACOBI_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  JACOBI_CONVERGED = 0,     /* some k <= max_iter had d_k < tol; iters_out = k            */
+  JACOBI_MAX_ITER = 1,      /* max_iter sweeps done without d_k < tol (not an error)      */
+  JACOBI_EINVAL = -1,       /* bad argument                                               */
+  JACOBI_EZERODIAG = -2,    /* a_ii == 0 for some i (message names the lowest i)          */
+  JACOBI_ENONFINITE = -3,   /* NaN or Inf in A, b or x0                                   */
+  JACOBI_ENOMEM = -4,       /* device or pinned host allocation failed                    */
+  JACOBI_ECUDA = -5,        /* CUDA runtime error (message has the CUDA error string)     */
+  JACOBI_ENCCL = -6,        /* NCCL error                                                 */
+  JACOBI_EINDIVISIBLE = -7  /* distributed: nranks does not divide n                      */
+};
+
+enum { JACOBI_F64 = 0, JACOBI_F32 = 1 };
+
+typedef struct jacobi_plan jacobi_plan;
+
+/* One-shot solve on the current CUDA device with HOST pointers (A: n x n, lda = n).
+ * Copies A, b, x0 to the device, runs the sweeps, copies x back. */
+int jacobi_solve(int64_t n, const double* A, const double* b, const double* x0, int64_t max_iter,
+                 double tol, double* x_out, int64_t* iters_out);
+/* Same with A stored as fp32 (values widened exactly; fp64 accumulation, fp64 x and b). */
+int jacobi_solve_f32a(int64_t n, const float* A, const double* b, const double* x0, int64_t max_iter,
+                      double tol, double* x_out, int64_t* iters_out);
+
+/* Plan API: uploads (or borrows) A once, validates it (EZERODIAG, ENONFINITE) and keeps the
+ * device state, so repeated solves (and timing) exclude the upload.
+ *   dtype: JACOBI_F64 / JACOBI_F32;  A: n rows of lda elements, host (a_on_device = 0) or device. */
+int jacobi_plan_create(jacobi_plan** out, int64_t n, int dtype, const void* A, int64_t lda,
+                       int a_on_device, void* cuda_stream);
+/* Solve with HOST pointers: b (n, or m for a distributed plan), x0 (n), x_out (n),
+ * dist_hist (nullable; receives d_1..d_iters, needs max_iter entries). */
+int jacobi_plan_solve(jacobi_plan* plan, const double* b, const double* x0, int64_t max_iter, double tol,
+                      double* x_out, int64_t* iters_out, double* dist_hist);
+/* Same contract with DEVICE pointers (b, x0, x_out, dist_hist on the plan's device); only the
+ * 48-byte stop state crosses PCIe.  x_out may alias x0. */
+int jacobi_plan_solve_device(jacobi_plan* plan, const double* d_b, const double* d_x0, int64_t max_iter,
+                             double tol, double* d_x_out, int64_t* iters_out, double* d_dist_hist);
+void jacobi_plan_destroy(jacobi_plan* plan);
+
+/* Test hook for SURVEY.md pin P12(a): run each sweep of a single-GPU plan as `nblocks` row-block
+ * launches (nblocks must divide the plan's rows).  Results must be bitwise identical to 1. */
+int jacobi_plan_set_row_blocks(jacobi_plan* plan, int nblocks);
+/* Sweeps per captured CUDA graph batch (multiple of 4, 4..1024; default 32).  The stop state is
+ * polled on the host once per batch; sweeps after the stop decision are no-op launches. */
+int jacobi_plan_set_batch(jacobi_plan* plan, int sweeps_per_batch);
+
+typedef struct {
+  int64_t n, lda, rows, row0;   /* global size, A leading dimension, owned rows, first owned row */
+  int dtype, rank, nranks;
+  int chunk_cols;               /* column chunk width of the sweep kernel (depends on n only)   */
+  int rows_per_warp;            /* rows a warp streams together (x reuse factor)               */
+  int grid_ctas, threads_per_cta;
+  int a_borrowed;               /* 1 if the caller's device A is used in place                 */
+  int64_t sweeps_launched;      /* sweep kernels launched by the last solve (incl. no-ops)     */
+  double bytes_per_sweep;       /* algorithmic HBM bytes per sweep: rows*n*s_A + 8n + 16*rows  */
+} jacobi_plan_info_t;
+int jacobi_plan_info(const jacobi_plan* plan, jacobi_plan_info_t* info);
+
+/* Per-sweep kernel timing (CUDA events around each sweep kernel, launched without a graph on the
+ * plan's stream): runs `sweeps` fixed sweeps from the given DEVICE b / x0 and writes each kernel's
+ * duration in ms.  For roofline measurements; the solve path itself uses CUDA graphs. */
+int jacobi_plan_time_sweeps(jacobi_plan* plan, const double* d_b, const double* d_x0, int sweeps,
+                            float* ms_out);
+
+/* ------------------------------------------------------------------ distributed (NCCL) */
+/* Row-block partition of PAPER.md:72: rows [rank*m, (rank+1)*m), m = n/nranks. */
+int jacobi_partition(int64_t n, int nranks, int rank, int64_t* row0, int64_t* rows);
+/* 128-byte NCCL unique id (rank 0 creates it; the caller broadcasts it, e.g. via torch.distributed). */
+int jacobi_nccl_unique_id(void* out128);
+/* One process per GPU: rank passes its own row block A_rows (rows x lda, rows = n/nranks).
+ * Collective over the nranks processes (all must call it).  Solve then takes b of length rows,
+ * x0 and x_out of length n (every rank receives the full solution). */
+int jacobi_dist_plan_create(jacobi_plan** out, const void* uid128, int rank, int nranks, int64_t n,
+                            int dtype, const void* A_rows, int64_t lda, int a_on_device,
+                            void* cuda_stream);
+
+/* ------------------------------------------------------------------ measurement */
+/* Read-only HBM ceiling: streams `nbytes` of device memory with the sweep kernel's load flavour
+ * (256-bit, L1::no_allocate) and returns the best GB/s of `reps` timed passes. */
+int jacobi_bwprobe(int64_t nbytes, int reps, double* best_gbs);
+
+const char* jacobi_last_error(void);
+int jacobi_version(void); /* 100 * major + minor */
+
+#ifdef __cplusplus
+}
+#endif
+#endif

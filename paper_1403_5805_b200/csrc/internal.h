@@ -1,0 +1,112 @@
+// internal.h — plan layout, device stop state and kernel launchers shared by the C-ABI sources.
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+#include <string>
+#include "jacobi.h"
+
+namespace jacobi {
+
+// Device-resident stop state of one solve.  Written by the host at solve start,
+// then only by the first CTA of a sweep kernel's prologue and by k_advance.
+struct State {
+  int64_t kbase;      // sweeps of earlier graph batches; sweep k = kbase + j + 1
+  int64_t max_iter;   // L of PAPER.md:59
+  double tol;         // tol of PAPER.md:59 (strict "<", max norm)
+  double* hist;       // d_k history (device, nullable), hist[k-1] = d_k
+  int32_t done;       // stop decided
+  int32_t status;     // JACOBI_CONVERGED / JACOBI_MAX_ITER once done
+  int64_t iters;      // sweeps performed once done
+};
+
+// Everything a sweep kernel needs; fixed for the life of a plan (captured into CUDA graphs).
+struct SweepArgs {
+  const void* A;            // owned rows, row-major, lda elements per row (fp64 or fp32)
+  int64_t lda;
+  int64_t n;                // global columns
+  int64_t m;                // rows handled by this launch
+  int64_t row0;             // global index of the launch's first row (diagonal position)
+  const double* diag;       // a_ii of the launch's rows (fp64)
+  const double* b;          // b of the launch's rows
+  double* x0buf;            // full-length x ping-pong buffers: sweep k reads x[(k-1)&1], writes x[k&1]
+  double* x1buf;
+  double* part;             // partial row sums, part[c * m + r]
+  unsigned* cnt;            // per row-tile arrival counters (reset by the finalizing warp)
+  unsigned long long* dslot;// 4-slot ring of max|dx| bit patterns; sweep k uses slot k & 3
+  State* st;
+  int chunk;                // columns per work item (multiple of 512, depends on n only)
+  int nchunks;              // ceil(n / chunk)
+  int tiles;                // ceil(m / R)
+};
+
+enum { kThreads = 512 };    // threads per CTA of the sweep kernel
+
+// Launchers (sweep.cu).  Return cudaGetLastError() of the launch.
+cudaError_t launch_sweep(int dtype, const SweepArgs& a, int j, int grid, cudaStream_t s);
+cudaError_t launch_advance(State* st, unsigned long long* dslot, int K, cudaStream_t s);
+cudaError_t launch_setup_diag(int dtype, const void* A, int64_t lda, int64_t m, int64_t row0,
+                              double* diag, unsigned long long* zero_min, cudaStream_t s);
+cudaError_t launch_scan_nonfinite_A(int dtype, const void* A, int64_t lda, int64_t m, int64_t n,
+                                    int* flag, cudaStream_t s);
+cudaError_t launch_scan_nonfinite_vec(const double* v, int64_t len, int* flag, cudaStream_t s);
+cudaError_t launch_copy_pitched(int dtype, const void* src, int64_t src_ld, void* dst, int64_t dst_ld,
+                                int64_t rows, int64_t n, cudaStream_t s);
+int sweep_rows_per_warp(int dtype);
+int sweep_grid(int dtype, int num_sms);
+int chunk_for(int64_t n);
+double bwprobe(int64_t nbytes, int reps);
+
+}  // namespace jacobi
+
+// The opaque plan of jacobi.h.
+struct jacobi_plan {
+  int64_t n = 0, lda = 0, m = 0, row0 = 0;
+  int dtype = JACOBI_F64, rank = 0, nranks = 1;
+  int device = 0, num_sms = 0, grid = 0;
+  int nblocks = 1;               // P12(a) row-block emulation
+  int batch = 32;                // sweeps per graph batch
+  bool own_stream = false, a_borrowed = false;
+  cudaStream_t stream = nullptr;
+  const void* dA = nullptr;      // device A (owned or borrowed)
+  void* dA_owned = nullptr;
+  double* diag = nullptr;
+  double* b = nullptr;           // owned copy of b (rows)
+  double* x[2] = {nullptr, nullptr};   // full-length ping-pong (x_len doubles each)
+  int64_t x_len = 0;
+  double* part = nullptr;
+  unsigned* cnt = nullptr;
+  unsigned long long* dslot = nullptr;
+  jacobi::State* st = nullptr;   // device
+  jacobi::State* st_host = nullptr;   // pinned mirror
+  double* hist_dev = nullptr;    // device history buffer for host-pointer solves
+  int64_t hist_cap = 0;
+  int* flag_dev = nullptr;       // scratch: non-finite flag / zero-diag min index
+  unsigned long long* zmin_dev = nullptr;
+  ncclComm_t comm = nullptr;     // distributed plans only
+  cudaGraphExec_t graph = nullptr;
+  int graph_batch = 0, graph_nblocks = 0;
+  int64_t sweeps_launched = 0;
+  int chunk = 0;
+};
+
+// Error helpers (plan.cu)
+int jacobi_set_error(int code, const std::string& msg);
+#define JCUDA(call)                                                                             \
+  do {                                                                                          \
+    cudaError_t _e = (call);                                                                    \
+    if (_e != cudaSuccess)                                                                      \
+      return jacobi_set_error(_e == cudaErrorMemoryAllocation ? JACOBI_ENOMEM : JACOBI_ECUDA,   \
+                              std::string(#call) + ": " + cudaGetErrorString(_e));              \
+  } while (0)
+#define JNCCL(call)                                                                             \
+  do {                                                                                          \
+    ncclResult_t _r = (call);                                                                   \
+    if (_r != ncclSuccess)                                                                      \
+      return jacobi_set_error(JACOBI_ENCCL, std::string(#call) + ": " + ncclGetErrorString(_r));\
+  } while (0)
+
+// Shared by plan.cu / dist.cu
+int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dtype, const void* A,
+                     int64_t lda, int a_on_device, void* stream);
+int plan_validate_A(jacobi_plan* p, unsigned long long* zero_row, int* nonfinite);

@@ -1,0 +1,451 @@
+// plan.cu — the C-ABI of include/jacobi.h: plans, validation, CUDA-graph sweep batches, stop polling.
+//
+// Solve loop (PAPER.md:59-66 on the device).  A solve captures, once per plan, a CUDA graph of K
+// sweep kernels (+ the exchange collectives for distributed plans) followed by k_advance.  The host
+// launches batches with a look-ahead of two and polls the 48-byte device stop state (copied to
+// pinned memory behind each batch); sweeps after the device's stop decision exit in their prologue.
+// No batch is issued beyond ceil(max_iter / K), so tol = 0 runs never wait on a poll.
+#include "internal.h"
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+namespace {
+thread_local std::string g_err;
+constexpr int kLookahead = 2;
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+}  // namespace
+
+int jacobi_set_error(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+extern "C" const char* jacobi_last_error(void) { return g_err.c_str(); }
+extern "C" int jacobi_version(void) { return 100; }
+
+static int plan_free(jacobi_plan* p) {
+  if (!p) return 0;
+  if (p->graph) cudaGraphExecDestroy(p->graph);
+  if (p->comm) ncclCommDestroy(p->comm);
+  cudaFree(p->dA_owned);
+  cudaFree(p->diag);
+  cudaFree(p->b);
+  cudaFree(p->x[0]);
+  cudaFree(p->x[1]);
+  cudaFree(p->part);
+  cudaFree(p->cnt);
+  cudaFree(p->dslot);
+  cudaFree(p->st);
+  cudaFree(p->hist_dev);
+  cudaFree(p->flag_dev);
+  cudaFree(p->zmin_dev);
+  if (p->st_host) cudaFreeHost(p->st_host);
+  if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
+  delete p;
+  return 0;
+}
+
+int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dtype, const void* A, int64_t lda,
+                     int a_on_device, void* stream) {
+  p->n = n;
+  p->m = m;
+  p->row0 = row0;
+  p->dtype = dtype;
+  JCUDA(cudaGetDevice(&p->device));
+  JCUDA(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, p->device));
+  int major = 0;
+  JCUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, p->device));
+  if (major != 10) return jacobi_set_error(JACOBI_ECUDA, "device is not sm_100 (B200); this build targets sm_100a only");
+  if (stream) {
+    p->stream = (cudaStream_t)stream;
+  } else {
+    JCUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    p->own_stream = true;
+  }
+  const int64_t elt = dtype == JACOBI_F32 ? 4 : 8;
+  const int64_t lda_dev = round_up(n, 8);
+  if (a_on_device && ((uintptr_t)A % 32 == 0) && lda % 8 == 0) {
+    p->dA = A;
+    p->lda = lda;
+    p->a_borrowed = true;
+  } else {
+    JCUDA(cudaMalloc(&p->dA_owned, (size_t)(m * lda_dev * elt)));
+    p->lda = lda_dev;
+    p->dA = p->dA_owned;
+    if (a_on_device) {
+      JCUDA(jacobi::launch_copy_pitched(dtype, A, lda, p->dA_owned, lda_dev, m, n, p->stream));
+    } else if (lda == lda_dev) {
+      JCUDA(cudaMemcpyAsync(p->dA_owned, A, (size_t)(m * lda * elt), cudaMemcpyHostToDevice, p->stream));
+    } else {
+      JCUDA(cudaMemsetAsync(p->dA_owned, 0, (size_t)(m * lda_dev * elt), p->stream));
+      JCUDA(cudaMemcpy2DAsync(p->dA_owned, (size_t)(lda_dev * elt), A, (size_t)(lda * elt), (size_t)(n * elt),
+                              (size_t)m, cudaMemcpyHostToDevice, p->stream));
+    }
+  }
+  p->chunk = jacobi::chunk_for(n);
+  p->grid = jacobi::sweep_grid(dtype, p->num_sms);
+  p->x_len = round_up(n, 256) + 256;
+  const int64_t nchunks = (n + p->chunk - 1) / p->chunk;
+  JCUDA(cudaMalloc(&p->diag, (size_t)m * 8));
+  JCUDA(cudaMalloc(&p->b, (size_t)m * 8));
+  JCUDA(cudaMalloc(&p->x[0], (size_t)p->x_len * 8));
+  JCUDA(cudaMalloc(&p->x[1], (size_t)p->x_len * 8));
+  JCUDA(cudaMalloc(&p->part, (size_t)(nchunks * m) * 8));
+  JCUDA(cudaMalloc(&p->cnt, (size_t)m * 4));
+  JCUDA(cudaMalloc(&p->dslot, 4 * 8));
+  JCUDA(cudaMalloc(&p->st, sizeof(jacobi::State)));
+  JCUDA(cudaMalloc(&p->flag_dev, 16));
+  JCUDA(cudaMalloc(&p->zmin_dev, 8));
+  JCUDA(cudaMallocHost(&p->st_host, kLookahead * sizeof(jacobi::State)));
+  JCUDA(cudaMemsetAsync(p->x[0], 0, (size_t)p->x_len * 8, p->stream));
+  JCUDA(cudaMemsetAsync(p->x[1], 0, (size_t)p->x_len * 8, p->stream));
+  JCUDA(cudaMemsetAsync(p->cnt, 0, (size_t)m * 4, p->stream));
+  return 0;
+}
+
+// Setup kernels: diag gather + lowest zero-diagonal row + non-finite scan of A.
+int plan_validate_A(jacobi_plan* p, unsigned long long* zero_row, int* nonfinite) {
+  JCUDA(cudaMemsetAsync(p->zmin_dev, 0xff, 8, p->stream));
+  JCUDA(cudaMemsetAsync(p->flag_dev, 0, 4, p->stream));
+  JCUDA(jacobi::launch_setup_diag(p->dtype, p->dA, p->lda, p->m, p->row0, p->diag, p->zmin_dev, p->stream));
+  JCUDA(jacobi::launch_scan_nonfinite_A(p->dtype, p->dA, p->lda, p->m, p->n, p->flag_dev, p->stream));
+  if (p->comm) {
+    JNCCL(ncclAllReduce(p->zmin_dev, p->zmin_dev, 1, ncclUint64, ncclMin, p->comm, p->stream));
+    JNCCL(ncclAllReduce(p->flag_dev, p->flag_dev, 1, ncclInt32, ncclMax, p->comm, p->stream));
+  }
+  JCUDA(cudaMemcpyAsync(zero_row, p->zmin_dev, 8, cudaMemcpyDeviceToHost, p->stream));
+  JCUDA(cudaMemcpyAsync(nonfinite, p->flag_dev, 4, cudaMemcpyDeviceToHost, p->stream));
+  JCUDA(cudaStreamSynchronize(p->stream));
+  return 0;
+}
+
+static int validate_result(unsigned long long zero_row, int nonfinite) {
+  if (zero_row != ~0ull)
+    return jacobi_set_error(JACOBI_EZERODIAG, "a_ii == 0 at i = " + std::to_string(zero_row) +
+                                                  " (PAPER.md:53: the method needs a_ii != 0)");
+  if (nonfinite) return jacobi_set_error(JACOBI_ENONFINITE, "A contains NaN or Inf");
+  return 0;
+}
+
+extern "C" int jacobi_plan_create(jacobi_plan** out, int64_t n, int dtype, const void* A, int64_t lda,
+                                  int a_on_device, void* cuda_stream) {
+  if (!out || !A || n < 1 || lda < n || (dtype != JACOBI_F64 && dtype != JACOBI_F32))
+    return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_create: bad argument (out/A NULL, n < 1, lda < n or dtype)");
+  jacobi_plan* p = new jacobi_plan();
+  int rc = plan_init_common(p, n, n, 0, dtype, A, lda, a_on_device, cuda_stream);
+  unsigned long long zr = 0;
+  int nf = 0;
+  if (rc == 0) rc = plan_validate_A(p, &zr, &nf);
+  if (rc == 0) rc = validate_result(zr, nf);
+  if (rc != 0) {
+    std::string keep = g_err;
+    plan_free(p);
+    g_err = keep;
+    return rc;
+  }
+  *out = p;
+  return 0;
+}
+
+extern "C" void jacobi_plan_destroy(jacobi_plan* p) {
+  if (p && p->stream) cudaStreamSynchronize(p->stream);
+  plan_free(p);
+}
+
+extern "C" int jacobi_plan_set_row_blocks(jacobi_plan* p, int nblocks) {
+  if (!p || nblocks < 1 || p->m % nblocks != 0 || p->comm)
+    return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_set_row_blocks: nblocks must divide the rows of a 1-GPU plan");
+  p->nblocks = nblocks;
+  return 0;
+}
+
+extern "C" int jacobi_plan_set_batch(jacobi_plan* p, int K) {
+  if (!p || K < 4 || K > 1024 || K % 4 != 0)
+    return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_set_batch: K must be a multiple of 4 in [4, 1024]");
+  p->batch = K;
+  return 0;
+}
+
+extern "C" int jacobi_plan_info(const jacobi_plan* p, jacobi_plan_info_t* info) {
+  if (!p || !info) return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_info: NULL argument");
+  info->n = p->n;
+  info->lda = p->lda;
+  info->rows = p->m;
+  info->row0 = p->row0;
+  info->dtype = p->dtype;
+  info->rank = p->rank;
+  info->nranks = p->nranks;
+  info->chunk_cols = p->chunk;
+  info->rows_per_warp = jacobi::sweep_rows_per_warp(p->dtype);
+  info->grid_ctas = p->grid;
+  info->threads_per_cta = jacobi::kThreads;
+  info->a_borrowed = p->a_borrowed ? 1 : 0;
+  info->sweeps_launched = p->sweeps_launched;
+  const double sA = p->dtype == JACOBI_F32 ? 4.0 : 8.0;
+  info->bytes_per_sweep = (double)p->m * (double)p->n * sA + 8.0 * (double)p->n + 16.0 * (double)p->m;
+  return 0;
+}
+
+static jacobi::SweepArgs sweep_args(const jacobi_plan* p, int blk) {
+  const int64_t mb = p->m / p->nblocks;
+  const int64_t esz = p->dtype == JACOBI_F32 ? 4 : 8;
+  jacobi::SweepArgs a;
+  a.A = (const char*)p->dA + (size_t)(blk * mb * p->lda * esz);
+  a.lda = p->lda;
+  a.n = p->n;
+  a.m = mb;
+  a.row0 = p->row0 + blk * mb;
+  a.diag = p->diag + blk * mb;
+  a.b = p->b + blk * mb;
+  a.x0buf = p->x[0];
+  a.x1buf = p->x[1];
+  a.part = p->part;
+  a.cnt = p->cnt;
+  a.dslot = p->dslot;
+  a.st = p->st;
+  a.chunk = p->chunk;
+  a.nchunks = (int)((p->n + p->chunk - 1) / p->chunk);
+  const int R = jacobi::sweep_rows_per_warp(p->dtype);
+  a.tiles = (int)((mb + R - 1) / R);
+  return a;
+}
+
+// Enqueue sweep j of a batch (all row blocks) plus, for distributed plans, the exchange
+// (SURVEY.md §8(a) a6): in-place allgather of the new x slice and max-allreduce of d_k's bits.
+static int enqueue_sweep(jacobi_plan* p, int j) {
+  for (int blk = 0; blk < p->nblocks; ++blk)
+    JCUDA(jacobi::launch_sweep(p->dtype, sweep_args(p, blk), j, p->grid, p->stream));
+  if (p->comm) {
+    // k = kbase + j + 1 with kbase a multiple of the batch size (a multiple of 4): parity is static.
+    double* xk = p->x[(j + 1) & 1];
+    JNCCL(ncclAllGather(xk + p->row0, xk, (size_t)p->m, ncclDouble, p->comm, p->stream));
+    JNCCL(ncclAllReduce(p->dslot + ((j + 1) & 3), p->dslot + ((j + 1) & 3), 1, ncclUint64, ncclMax, p->comm,
+                        p->stream));
+  }
+  return 0;
+}
+
+static int ensure_graph(jacobi_plan* p) {
+  if (p->graph && p->graph_batch == p->batch && p->graph_nblocks == p->nblocks) return 0;
+  if (p->graph) {
+    cudaGraphExecDestroy(p->graph);
+    p->graph = nullptr;
+  }
+  cudaGraph_t g = nullptr;
+  JCUDA(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+  int rc = 0;
+  for (int j = 0; j < p->batch && rc == 0; ++j) rc = enqueue_sweep(p, j);
+  if (rc == 0) {
+    cudaError_t e = jacobi::launch_advance(p->st, p->dslot, p->batch, p->stream);
+    if (e != cudaSuccess) rc = jacobi_set_error(JACOBI_ECUDA, std::string("k_advance: ") + cudaGetErrorString(e));
+  }
+  cudaError_t ee = cudaStreamEndCapture(p->stream, &g);
+  if (rc != 0) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (ee != cudaSuccess) return jacobi_set_error(JACOBI_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ee));
+  cudaError_t ie = cudaGraphInstantiate(&p->graph, g, 0);
+  cudaGraphDestroy(g);
+  if (ie != cudaSuccess) return jacobi_set_error(JACOBI_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
+  p->graph_batch = p->batch;
+  p->graph_nblocks = p->nblocks;
+  return 0;
+}
+
+// Copies inputs in, checks them, and resets the device stop state.  Returns 0, a negative status,
+// or 2 when max_iter == 0 (nothing to run).
+static int solve_prepare(jacobi_plan* p, const double* b, const double* x0, bool dev, int64_t max_iter, double tol,
+                         double* hist_dev) {
+  const cudaMemcpyKind kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  JCUDA(cudaMemcpyAsync(p->b, b, (size_t)p->m * 8, kind, p->stream));
+  JCUDA(cudaMemcpyAsync(p->x[0], x0, (size_t)p->n * 8, kind, p->stream));
+  JCUDA(cudaMemsetAsync(p->flag_dev, 0, 4, p->stream));
+  JCUDA(jacobi::launch_scan_nonfinite_vec(p->b, p->m, p->flag_dev, p->stream));
+  JCUDA(jacobi::launch_scan_nonfinite_vec(p->x[0], p->n, p->flag_dev, p->stream));
+  if (p->comm) JNCCL(ncclAllReduce(p->flag_dev, p->flag_dev, 1, ncclInt32, ncclMax, p->comm, p->stream));
+  jacobi::State s0{};
+  s0.kbase = 0;
+  s0.max_iter = max_iter;
+  s0.tol = tol;
+  s0.hist = hist_dev;
+  s0.done = 0;
+  s0.status = 0;
+  s0.iters = 0;
+  p->st_host[0] = s0;
+  JCUDA(cudaMemcpyAsync(p->st, &p->st_host[0], sizeof(jacobi::State), cudaMemcpyHostToDevice, p->stream));
+  JCUDA(cudaMemsetAsync(p->dslot, 0, 4 * 8, p->stream));
+  JCUDA(cudaMemsetAsync(p->cnt, 0, (size_t)p->m * 4, p->stream));
+  int nf = 0;
+  JCUDA(cudaMemcpyAsync(&p->st_host[1].status, p->flag_dev, 4, cudaMemcpyDeviceToHost, p->stream));
+  JCUDA(cudaStreamSynchronize(p->stream));
+  nf = p->st_host[1].status;
+  if (nf) return jacobi_set_error(JACOBI_ENONFINITE, "b or x0 contains NaN or Inf");
+  return max_iter == 0 ? 2 : 0;
+}
+
+// Runs graph batches until the device decides to stop.  Fills *fin with the final state.
+static int solve_run(jacobi_plan* p, int64_t max_iter, jacobi::State* fin) {
+  int rc = ensure_graph(p);
+  if (rc) return rc;
+  const int64_t K = p->batch;
+  const int64_t max_batches = (max_iter + K - 1) / K;  // the stop is decided within these
+  cudaEvent_t ev[kLookahead];
+  for (int i = 0; i < kLookahead; ++i) JCUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+  int64_t issued = 0, waited = 0;
+  bool done = false;
+  p->sweeps_launched = 0;
+  auto issue = [&]() -> int {
+    const int slot = (int)(issued % kLookahead);
+    JCUDA(cudaGraphLaunch(p->graph, p->stream));
+    JCUDA(cudaMemcpyAsync(&p->st_host[slot], p->st, sizeof(jacobi::State), cudaMemcpyDeviceToHost, p->stream));
+    JCUDA(cudaEventRecord(ev[slot], p->stream));
+    ++issued;
+    p->sweeps_launched += K * p->nblocks;
+    return 0;
+  };
+  while (rc == 0 && issued < std::min<int64_t>(kLookahead, max_batches)) rc = issue();
+  while (rc == 0 && !done) {
+    const int slot = (int)(waited % kLookahead);
+    cudaError_t e = cudaEventSynchronize(ev[slot]);
+    if (e != cudaSuccess) { rc = jacobi_set_error(JACOBI_ECUDA, std::string("sweep batch: ") + cudaGetErrorString(e)); break; }
+    if (p->comm) {
+      ncclResult_t ar = ncclSuccess;
+      ncclCommGetAsyncError(p->comm, &ar);
+      if (ar != ncclSuccess && ar != ncclInProgress) { rc = jacobi_set_error(JACOBI_ENCCL, ncclGetErrorString(ar)); break; }
+    }
+    ++waited;
+    if (p->st_host[slot].done) {
+      *fin = p->st_host[slot];
+      done = true;
+      break;
+    }
+    if (waited >= max_batches) {
+      rc = jacobi_set_error(JACOBI_ECUDA, "internal: stop not decided after max_iter sweeps");
+      break;
+    }
+    if (issued < max_batches) rc = issue();
+  }
+  cudaError_t se = cudaStreamSynchronize(p->stream);  // drain look-ahead no-op batches
+  for (int i = 0; i < kLookahead; ++i) cudaEventDestroy(ev[i]);
+  if (rc == 0 && se != cudaSuccess) rc = jacobi_set_error(JACOBI_ECUDA, std::string("sync: ") + cudaGetErrorString(se));
+  return rc;
+}
+
+static int solve_impl(jacobi_plan* p, const double* b, const double* x0, bool dev, int64_t max_iter, double tol,
+                      double* x_out, int64_t* iters_out, double* hist) {
+  if (!p || !b || !x0 || !x_out || !iters_out || max_iter < 0 || std::isnan(tol) || tol < 0)
+    return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_solve: bad argument (NULL pointer, max_iter < 0, tol < 0 or NaN)");
+  JCUDA(cudaSetDevice(p->device));
+  double* hist_dev = nullptr;
+  if (hist && max_iter > 0) {
+    if (dev) {
+      hist_dev = hist;
+    } else {
+      if (p->hist_cap < max_iter) {
+        cudaFree(p->hist_dev);
+        p->hist_dev = nullptr;
+        p->hist_cap = 0;
+        JCUDA(cudaMalloc(&p->hist_dev, (size_t)max_iter * 8));
+        p->hist_cap = max_iter;
+      }
+      hist_dev = p->hist_dev;
+    }
+  }
+  int rc = solve_prepare(p, b, x0, dev, max_iter, tol, hist_dev);
+  if (rc < 0) return rc;
+  jacobi::State fin{};
+  if (rc == 2) {  // max_iter == 0: X^0 (reading R14)
+    fin.status = JACOBI_MAX_ITER;
+    fin.iters = 0;
+  } else {
+    rc = solve_run(p, max_iter, &fin);
+    if (rc) return rc;
+  }
+  const cudaMemcpyKind kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  JCUDA(cudaMemcpyAsync(x_out, p->x[fin.iters & 1], (size_t)p->n * 8, kind, p->stream));
+  if (hist && !dev && fin.iters > 0)
+    JCUDA(cudaMemcpyAsync(hist, hist_dev, (size_t)fin.iters * 8, cudaMemcpyDeviceToHost, p->stream));
+  JCUDA(cudaStreamSynchronize(p->stream));
+  *iters_out = fin.iters;
+  return fin.status;
+}
+
+extern "C" int jacobi_plan_solve(jacobi_plan* p, const double* b, const double* x0, int64_t max_iter, double tol,
+                                 double* x_out, int64_t* iters_out, double* dist_hist) {
+  return solve_impl(p, b, x0, false, max_iter, tol, x_out, iters_out, dist_hist);
+}
+
+extern "C" int jacobi_plan_solve_device(jacobi_plan* p, const double* b, const double* x0, int64_t max_iter,
+                                        double tol, double* x_out, int64_t* iters_out, double* dist_hist) {
+  return solve_impl(p, b, x0, true, max_iter, tol, x_out, iters_out, dist_hist);
+}
+
+extern "C" int jacobi_plan_time_sweeps(jacobi_plan* p, const double* d_b, const double* d_x0, int sweeps,
+                                       float* ms_out) {
+  if (!p || !d_b || !d_x0 || sweeps < 1 || !ms_out)
+    return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_time_sweeps: bad argument");
+  JCUDA(cudaSetDevice(p->device));
+  int rc = solve_prepare(p, d_b, d_x0, true, sweeps, 0.0, nullptr);
+  if (rc < 0) return rc;
+  cudaEvent_t e0, e1;
+  JCUDA(cudaEventCreate(&e0));
+  JCUDA(cudaEventCreate(&e1));
+  for (int j = 0; j < sweeps && rc == 0; ++j) {
+    cudaEventRecord(e0, p->stream);
+    for (int blk = 0; blk < p->nblocks; ++blk) {
+      cudaError_t e = jacobi::launch_sweep(p->dtype, sweep_args(p, blk), j, p->grid, p->stream);
+      if (e != cudaSuccess) rc = jacobi_set_error(JACOBI_ECUDA, cudaGetErrorString(e));
+    }
+    cudaEventRecord(e1, p->stream);
+    if (rc == 0 && p->comm) rc = [&]() -> int {
+      double* xk = p->x[(j + 1) & 1];
+      JNCCL(ncclAllGather(xk + p->row0, xk, (size_t)p->m, ncclDouble, p->comm, p->stream));
+      JNCCL(ncclAllReduce(p->dslot + ((j + 1) & 3), p->dslot + ((j + 1) & 3), 1, ncclUint64, ncclMax, p->comm,
+                          p->stream));
+      return 0;
+    }();
+    cudaError_t se = cudaEventSynchronize(e1);
+    if (se != cudaSuccess && rc == 0) rc = jacobi_set_error(JACOBI_ECUDA, cudaGetErrorString(se));
+    if (rc == 0) cudaEventElapsedTime(&ms_out[j], e0, e1);
+  }
+  cudaStreamSynchronize(p->stream);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return rc;
+}
+
+static int solve_oneshot(int64_t n, int dtype, const void* A, const double* b, const double* x0, int64_t max_iter,
+                         double tol, double* x_out, int64_t* iters_out) {
+  if (n < 1 || !A || !b || !x0 || !x_out || !iters_out || max_iter < 0 || std::isnan(tol) || tol < 0)
+    return jacobi_set_error(JACOBI_EINVAL, "jacobi_solve: bad argument (n < 1, NULL pointer, max_iter < 0, tol < 0 or NaN)");
+  jacobi_plan* p = nullptr;
+  int rc = jacobi_plan_create(&p, n, dtype, A, n, 0, nullptr);
+  if (rc) return rc;
+  rc = jacobi_plan_solve(p, b, x0, max_iter, tol, x_out, iters_out, nullptr);
+  std::string keep = g_err;
+  jacobi_plan_destroy(p);
+  g_err = keep;
+  return rc;
+}
+
+extern "C" int jacobi_solve(int64_t n, const double* A, const double* b, const double* x0, int64_t max_iter,
+                            double tol, double* x_out, int64_t* iters_out) {
+  return solve_oneshot(n, JACOBI_F64, A, b, x0, max_iter, tol, x_out, iters_out);
+}
+
+extern "C" int jacobi_solve_f32a(int64_t n, const float* A, const double* b, const double* x0, int64_t max_iter,
+                                 double tol, double* x_out, int64_t* iters_out) {
+  return solve_oneshot(n, JACOBI_F32, A, b, x0, max_iter, tol, x_out, iters_out);
+}
+
+extern "C" int jacobi_bwprobe(int64_t nbytes, int reps, double* best_gbs) {
+  if (nbytes < (1 << 20) || reps < 1 || !best_gbs) return jacobi_set_error(JACOBI_EINVAL, "jacobi_bwprobe: bad argument");
+  double g = jacobi::bwprobe(nbytes, reps);
+  if (g < 0) return jacobi_set_error(JACOBI_ECUDA, "jacobi_bwprobe: CUDA failure");
+  *best_gbs = g;
+  return 0;
+}

@@ -1,0 +1,366 @@
+// sweep.cu — sm_100a kernels of the dense Jacobi sweep.
+//
+// k_sweep: one Jacobi sweep over the launch's rows, fused with the max-norm change
+// d_k = max_i |x_i^(k) - x_i^(k-1)| and the device-side stop test of PAPER.md:61-66.
+//
+// Work decomposition.  Rows are grouped into tiles of R rows, columns into chunks of `chunk`
+// columns (a function of n only).  A work item is (tile, chunk); a warp streams the R rows of its
+// item with 256-bit L1::no_allocate loads (each lane owns E consecutive columns per step: E = 4
+// doubles or 8 floats) and reads the matching x values once per step (L1-cached, reused by the R
+// rows and by the other warps of the CTA, which work on neighbouring tiles of the same chunk).
+// Items are dealt round-robin over a persistent grid sized to fill every SM.
+//
+// Summation order (fixed; depends only on column indices, never on the rank count, the row
+// placement, R or the grid): lane l accumulates its columns in ascending order with one DFMA chain
+// per row; the 32 lane sums are combined by a shfl_xor butterfly (16, 8, 4, 2, 1); the chunk sums
+// are added in ascending chunk order by the warp that completes the row tile (last arrival on a
+// per-tile counter).  That warp applies the fused epilogue x_i = (b_i - s_i) / a_ii (IEEE division),
+// stores x_i^(k), and folds |x_i^(k) - x_i^(k-1)| into the sweep's max with an unsigned 64-bit
+// atomicMax on the bit pattern (sign cleared): NaN > +Inf > finite, so the max is NaN-sticky and
+// order independent.
+#include "internal.h"
+#include <cstdio>
+
+namespace jacobi {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+template <typename T> struct VecOf;
+template <> struct VecOf<double> { static constexpr int E = 4; };
+template <> struct VecOf<float> { static constexpr int E = 8; };
+
+// 256-bit streaming load of A (read exactly once per sweep): no L1 allocation.
+__device__ __forceinline__ void ld_a(const double* p, double (&v)[4]) {
+  asm("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+__device__ __forceinline__ void ld_a(const float* p, float (&v)[8]) {
+  asm("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+      : "l"(p));
+}
+// x^(k-1) is read-only during the sweep (it lives in the other ping-pong buffer): L1-cached loads.
+__device__ __forceinline__ void ld_x4(const double* p, double* v) {
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+template <int E>
+__device__ __forceinline__ void ld_x(const double* p, double (&v)[E]) {
+#pragma unroll
+  for (int q = 0; q < E; q += 4) ld_x4(p + q, v + q);
+}
+
+// Prologue of sweep k (PAPER.md:64-66 evaluated on the device): decides whether sweep k runs.
+// Every CTA evaluates the same inputs and reaches the same decision; only the leader writes.
+__device__ __forceinline__ bool sweep_prologue(const SweepArgs& a, int j, bool leader) {
+  State* st = a.st;
+  if (*(volatile int32_t*)&st->done) return false;
+  const int64_t k = st->kbase + j + 1;
+  if (k >= 2) {
+    const double d = __longlong_as_double((long long)a.dslot[(k - 1) & 3]);
+    if (leader && st->hist) st->hist[k - 2] = d;
+    if (d < st->tol) {  // (b): ||X - X^t|| < tol  -> return X^(k-1)
+      if (leader) { st->status = JACOBI_CONVERGED; st->iters = k - 1; st->done = 1; }
+      return false;
+    }
+  }
+  if (k > st->max_iter) {  // step 3: iteration limit reached
+    if (leader) { st->status = JACOBI_MAX_ITER; st->iters = st->max_iter; st->done = 1; }
+    return false;
+  }
+  if (leader) a.dslot[(k + 1) & 3] = 0ull;  // next sweep's max accumulator
+  return true;
+}
+
+template <typename T, int R, int U>
+__global__ void __launch_bounds__(kThreads, 1) k_sweep(const SweepArgs a, const int j) {
+  constexpr int E = VecOf<T>::E;
+  constexpr int S = 32 * E;  // columns per warp step
+  __shared__ int s_go;
+  if (threadIdx.x == 0) s_go = sweep_prologue(a, j, blockIdx.x == 0);
+  __syncthreads();
+  if (!s_go) return;
+
+  const int64_t k = a.st->kbase + j + 1;
+  const double* __restrict__ xo = (k & 1) ? a.x0buf : a.x1buf;  // x^(k-1)
+  double* __restrict__ xn = (k & 1) ? a.x1buf : a.x0buf;        // x^(k)
+  const T* __restrict__ A = static_cast<const T*>(a.A);
+  const int lane = threadIdx.x & 31;
+  const int64_t W = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t items = (int64_t)a.tiles * a.nchunks;
+  const int nsteps = a.chunk / S;
+
+  for (int64_t it = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); it < items; it += W) {
+    const int tile = (int)(it % a.tiles);
+    const int c = (int)(it / a.tiles);
+    const int64_t r0 = (int64_t)tile * R;
+    const int64_t c0 = (int64_t)c * a.chunk;
+    const int64_t c1 = min(c0 + (int64_t)a.chunk, a.n);
+    const int64_t g0 = a.row0 + r0;  // global index of the tile's first row
+    const T* rowp[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) rowp[r] = A + min(r0 + r, a.m - 1) * a.lda;
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+
+    const bool masked = (c1 - c0 != a.chunk) || (g0 < c1 && g0 + R > c0);
+    if (!masked) {
+      for (int s = 0; s < nsteps; s += U) {
+        T av[U][R][E];
+        double xv[U][E];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int64_t col = c0 + (int64_t)((s + u) * 32 + lane) * E;
+          ld_x<E>(xo + col, xv[u]);
+#pragma unroll
+          for (int r = 0; r < R; ++r) ld_a(rowp[r] + col, av[u][r]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int e = 0; e < E; ++e) acc[r] = __fma_rn((double)av[u][r][e], xv[u][e], acc[r]);
+      }
+    } else {
+      // Diagonal chunk or ragged tail: same order, j == i and j >= n terms skipped.
+      for (int s = 0; s < nsteps; ++s) {
+        const int64_t col = c0 + (int64_t)(s * 32 + lane) * E;
+        if (col < a.n) {
+          T av[R][E];
+          double xv[E];
+          ld_x<E>(xo + col, xv);
+#pragma unroll
+          for (int r = 0; r < R; ++r) ld_a(rowp[r] + col, av[r]);
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+              const int64_t cc = col + e;
+              if (cc < a.n && cc != g0 + r) acc[r] = __fma_rn((double)av[r][e], xv[e], acc[r]);
+            }
+        }
+      }
+    }
+    // Butterfly: every lane ends with the same, order-fixed row sums.
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc[r] += __shfl_xor_sync(kFull, acc[r], off);
+
+    // Publish the chunk partials, then count arrivals for the tile.
+    double mine = 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (lane == r) mine = acc[r];
+    if (lane < R && r0 + lane < a.m) a.part[(int64_t)c * a.m + r0 + lane] = mine;
+    __threadfence();
+    __syncwarp();
+    unsigned last = 0;
+    if (lane == 0) last = (atomicAdd(&a.cnt[tile], 1u) == (unsigned)(a.nchunks - 1));
+    last = __shfl_sync(kFull, last, 0);
+    if (!last) continue;
+
+    // Finalize the tile (fused epilogue, PAPER.md:55 and the max-norm distance).
+    __threadfence();
+    unsigned long long dbits = 0ull;
+    if (lane < R && r0 + lane < a.m) {
+      const int64_t row = r0 + lane;
+      double s = __ldcg(a.part + row);
+      for (int cc = 1; cc < a.nchunks; ++cc) s += __ldcg(a.part + (int64_t)cc * a.m + row);
+      const double xnew = __ddiv_rn(__dsub_rn(a.b[row], s), a.diag[row]);
+      const int64_t gi = a.row0 + row;
+      const double xold = xo[gi];
+      xn[gi] = xnew;
+      dbits = (unsigned long long)__double_as_longlong(__dsub_rn(xnew, xold)) & 0x7fffffffffffffffull;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const unsigned long long o = __shfl_xor_sync(kFull, dbits, off);
+      dbits = o > dbits ? o : dbits;
+    }
+    if (lane == 0) {
+      atomicMax(&a.dslot[k & 3], dbits);
+      a.cnt[tile] = 0u;
+    }
+  }
+}
+
+// After a graph batch of K sweeps: settle the stop decision for the batch's last sweep (same rule
+// as the prologue) and advance the sweep counter.
+__global__ void k_advance(State* st, const unsigned long long* dslot, int K) {
+  if (st->done) return;
+  const int64_t k = st->kbase + K + 1;  // the sweep that would come next
+  const double d = __longlong_as_double((long long)dslot[(k - 1) & 3]);
+  if (st->hist) st->hist[k - 2] = d;
+  if (d < st->tol) { st->status = JACOBI_CONVERGED; st->iters = k - 1; st->done = 1; return; }
+  if (k > st->max_iter) { st->status = JACOBI_MAX_ITER; st->iters = st->max_iter; st->done = 1; return; }
+  st->kbase += K;
+}
+
+template <typename T>
+__global__ void k_setup_diag(const T* __restrict__ A, int64_t lda, int64_t m, int64_t row0,
+                             double* __restrict__ diag, unsigned long long* zero_min) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
+    const double v = (double)A[r * lda + row0 + r];
+    diag[r] = v;
+    if (v == 0.0) atomicMin(zero_min, (unsigned long long)(row0 + r));
+  }
+}
+
+__device__ __forceinline__ bool nonfinite(double v) {
+  return ((unsigned long long)__double_as_longlong(v) & 0x7ff0000000000000ull) == 0x7ff0000000000000ull;
+}
+__device__ __forceinline__ bool nonfinite(float v) {
+  return ((unsigned)__float_as_uint(v) & 0x7f800000u) == 0x7f800000u;
+}
+
+template <typename T>
+__global__ void k_scan_A(const T* __restrict__ A, int64_t lda, int64_t m, int64_t n, int* flag) {
+  const int lane = threadIdx.x & 31;
+  bool bad = false;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < m;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const T* row = A + r * lda;
+    for (int64_t jj = lane; jj < n; jj += 32) bad |= nonfinite(row[jj]);
+  }
+  if (__any_sync(kFull, bad) && lane == 0) *flag = 1;
+}
+
+__global__ void k_scan_vec(const double* __restrict__ v, int64_t len, int* flag) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
+    bad |= nonfinite(v[i]);
+  if (bad) *flag = 1;
+}
+
+template <typename T>
+__global__ void k_copy_pitched(const T* __restrict__ src, int64_t sld, T* __restrict__ dst, int64_t dld,
+                               int64_t rows, int64_t n) {
+  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y)
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < dld; c += (int64_t)gridDim.x * blockDim.x)
+      dst[r * dld + c] = c < n ? src[r * sld + c] : T(0);
+}
+
+__global__ void k_probe(const double* __restrict__ buf, int64_t nvec, double* out) {
+  double acc = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; i + stride < nvec; i += 2 * stride) {
+    double v0[4], v1[4];
+    ld_a(buf + 4 * i, v0);
+    ld_a(buf + 4 * (i + stride), v1);
+    acc += (v0[0] + v0[1]) + (v0[2] + v0[3]) + (v1[0] + v1[1]) + (v1[2] + v1[3]);
+  }
+  for (; i < nvec; i += stride) {
+    double v0[4];
+    ld_a(buf + 4 * i, v0);
+    acc += (v0[0] + v0[1]) + (v0[2] + v0[3]);
+  }
+  if (acc == 1234.5678) *out = acc;  // keeps the loads alive
+}
+
+__global__ void k_fill(double* buf, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    buf[i] = (double)(i & 1023);
+}
+
+// Sweep variants: (R rows per warp, U steps in flight).  All variants produce identical bits.
+constexpr int kR64 = 4, kU64 = 2;
+constexpr int kR32 = 4, kU32 = 1;
+
+}  // namespace
+
+int sweep_rows_per_warp(int dtype) { return dtype == JACOBI_F32 ? kR32 : kR64; }
+
+int chunk_for(int64_t n) {
+  // ~16+ chunks per row when n allows (load balance over the persistent grid), 512..4096 columns.
+  int64_t c = 512;
+  while (c < 4096 && c * 16 < n) c *= 2;
+  return (int)c;
+}
+
+int sweep_grid(int dtype, int num_sms) {
+  int per_sm = 0;
+  cudaError_t e = dtype == JACOBI_F32
+      ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<float, kR32, kU32>, kThreads, 0)
+      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<double, kR64, kU64>, kThreads, 0);
+  if (e != cudaSuccess || per_sm < 1) per_sm = 1;
+  return num_sms * per_sm;
+}
+
+cudaError_t launch_sweep(int dtype, const SweepArgs& a, int j, int grid, cudaStream_t s) {
+  if (dtype == JACOBI_F32) k_sweep<float, kR32, kU32><<<grid, kThreads, 0, s>>>(a, j);
+  else k_sweep<double, kR64, kU64><<<grid, kThreads, 0, s>>>(a, j);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_advance(State* st, unsigned long long* dslot, int K, cudaStream_t s) {
+  k_advance<<<1, 1, 0, s>>>(st, dslot, K);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_setup_diag(int dtype, const void* A, int64_t lda, int64_t m, int64_t row0, double* diag,
+                              unsigned long long* zero_min, cudaStream_t s) {
+  const int grid = (int)std::min<int64_t>((m + 255) / 256, 4096);
+  if (dtype == JACOBI_F32) k_setup_diag<float><<<grid, 256, 0, s>>>((const float*)A, lda, m, row0, diag, zero_min);
+  else k_setup_diag<double><<<grid, 256, 0, s>>>((const double*)A, lda, m, row0, diag, zero_min);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scan_nonfinite_A(int dtype, const void* A, int64_t lda, int64_t m, int64_t n, int* flag,
+                                    cudaStream_t s) {
+  const int grid = (int)std::min<int64_t>((m + 7) / 8, 148 * 16);
+  if (dtype == JACOBI_F32) k_scan_A<float><<<grid, 256, 0, s>>>((const float*)A, lda, m, n, flag);
+  else k_scan_A<double><<<grid, 256, 0, s>>>((const double*)A, lda, m, n, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scan_nonfinite_vec(const double* v, int64_t len, int* flag, cudaStream_t s) {
+  const int grid = (int)std::min<int64_t>((len + 255) / 256, 1024);
+  k_scan_vec<<<grid, 256, 0, s>>>(v, len, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy_pitched(int dtype, const void* src, int64_t sld, void* dst, int64_t dld, int64_t rows,
+                                int64_t n, cudaStream_t s) {
+  dim3 grid((unsigned)std::min<int64_t>((dld + 255) / 256, 64), (unsigned)std::min<int64_t>(rows, 65535));
+  if (dtype == JACOBI_F32) k_copy_pitched<float><<<grid, 256, 0, s>>>((const float*)src, sld, (float*)dst, dld, rows, n);
+  else k_copy_pitched<double><<<grid, 256, 0, s>>>((const double*)src, sld, (double*)dst, dld, rows, n);
+  return cudaGetLastError();
+}
+
+double bwprobe(int64_t nbytes, int reps) {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1.0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  double* buf = nullptr;
+  double* out = nullptr;
+  if (cudaMalloc(&buf, nbytes) != cudaSuccess) return -1.0;
+  if (cudaMalloc(&out, 8) != cudaSuccess) { cudaFree(buf); return -1.0; }
+  const int64_t n = nbytes / 8, nvec = n / 4;
+  k_fill<<<sms * 8, 256>>>(buf, n);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int r = 0; r < reps + 1; ++r) {
+    cudaEventRecord(e0);
+    k_probe<<<sms * 2, 1024>>>(buf, nvec, out);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (r > 0 && ms < best) best = ms;  // first pass is a warm-up
+  }
+  cudaError_t err = cudaGetLastError();
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(buf);
+  cudaFree(out);
+  if (err != cudaSuccess) return -1.0;
+  return (double)(nvec * 32) / (best * 1e-3) / 1e9;
+}
+
+}  // namespace jacobi

@@ -1,0 +1,81 @@
+"""C-ABI library checks that need no GPU: it loads, exports every symbol include/jacobi.h declares,
+validates arguments before touching CUDA, partitions rows, and has no CPU fallback."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_functions():
+    src = open(os.path.join(ROOT, "include", "jacobi.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(jacobi_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def jb():
+    import subprocess
+    so = os.path.join(ROOT, "paper_1403_5805_b200", "libjacobi.so")
+    if not os.path.exists(so):
+        r = subprocess.run(["make", "-C", ROOT, "lib"], capture_output=True, text=True)
+        assert r.returncode == 0, r.stdout + r.stderr
+    import paper_1403_5805_b200 as jb
+    return jb
+
+
+def test_exports_every_header_symbol(jb):
+    names = _header_functions()
+    assert len(names) >= 16
+    lib = ctypes.CDLL(jb.LIB_PATH)
+    for name in names:
+        assert hasattr(lib, name), f"libjacobi.so does not export {name}"
+    assert set(names) == set(jb.EXPORTS)
+    assert jb.version() == 100
+
+
+def test_einval_before_any_cuda_call(jb):
+    lib = jb._lib
+    x = np.zeros(4)
+    it = ctypes.c_int64(-7)
+    A = np.eye(4)
+    # n < 1, NULL pointers, max_iter < 0, tol < 0 / NaN
+    assert lib.jacobi_solve(0, A.ctypes.data, x.ctypes.data, x.ctypes.data, 5, 0.0, x.ctypes.data, ctypes.byref(it)) == jb.EINVAL
+    assert lib.jacobi_solve(4, None, x.ctypes.data, x.ctypes.data, 5, 0.0, x.ctypes.data, ctypes.byref(it)) == jb.EINVAL
+    assert lib.jacobi_solve(4, A.ctypes.data, x.ctypes.data, x.ctypes.data, -1, 0.0, x.ctypes.data, ctypes.byref(it)) == jb.EINVAL
+    assert lib.jacobi_solve(4, A.ctypes.data, x.ctypes.data, x.ctypes.data, 5, -1.0, x.ctypes.data, ctypes.byref(it)) == jb.EINVAL
+    assert lib.jacobi_solve(4, A.ctypes.data, x.ctypes.data, x.ctypes.data, 5, float("nan"), x.ctypes.data, ctypes.byref(it)) == jb.EINVAL
+    assert it.value == -7  # outputs untouched on error
+    assert "bad argument" in jb.last_error()
+    h = ctypes.c_void_p()
+    assert lib.jacobi_plan_create(ctypes.byref(h), 4, 7, A.ctypes.data, 4, 0, None) == jb.EINVAL
+    assert lib.jacobi_plan_create(ctypes.byref(h), 4, 0, A.ctypes.data, 3, 0, None) == jb.EINVAL
+    assert lib.jacobi_plan_solve(None, x.ctypes.data, x.ctypes.data, 5, 0.0, x.ctypes.data, ctypes.byref(it), None) == jb.EINVAL
+    with pytest.raises(jb.JacobiError) as e:
+        jb.solve(np.eye(3), np.ones(3), max_iter=-2)
+    assert e.value.status == jb.EINVAL
+
+
+def test_partition(jb):
+    assert jb.partition(8, 2, 0) == (0, 4) and jb.partition(8, 2, 1) == (4, 4)
+    assert jb.partition(8, 8, 5) == (5, 1)
+    with pytest.raises(jb.JacobiError) as e:
+        jb.partition(8, 3, 0)
+    assert e.value.status == jb.EINDIVISIBLE
+    for n in (1, 12, 96, 1024):
+        for p in [d for d in range(1, 17) if n % d == 0]:
+            cover = []
+            for r in range(p):
+                r0, m = jb.partition(n, p, r)
+                cover.extend(range(r0, r0 + m))
+            assert cover == list(range(n))
+
+
+@pytest.mark.skipif(os.path.exists("/dev/nvidia0"), reason="checks the no-GPU path")
+def test_no_cpu_fallback_without_gpu(jb):
+    with pytest.raises(jb.JacobiError) as e:
+        jb.solve(np.array([[2.0, 1.0], [1.0, 3.0]]), np.array([3.0, 4.0]), max_iter=5)
+    assert e.value.status == jb.ECUDA

@@ -1,0 +1,289 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star): relative L-inf error <= 1e-10 for fp64 and <= 1e-4 for fp32
+A storage (self-checked at 1e-10: both sides accumulate in fp64 on identical fp32 values), and the
+same iteration count.  Bitwise checks where the arithmetic fixes the bits: sweep 1 from x0 = 0
+(P3), row-block invariance (P12a), determinism (P13), split runs (P11), batch-size invariance.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import jacobi_gen as g
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL64 = 1e-10
+TOL32 = 1e-4
+
+
+@pytest.fixture(scope="module")
+def jb():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1403_5805_b200 as jb
+    return jb
+
+
+def rel_linf(x, ref):
+    den = np.max(np.abs(ref))
+    err = np.max(np.abs(np.asarray(x) - ref))
+    return err / den if den > 0 else err
+
+
+def dominant(n, seed, scale=None, f32=False):
+    rng = np.random.default_rng(seed)
+    A = rng.uniform(-1, 1, (n, n))
+    np.fill_diagonal(A, 0.0)
+    rs = np.abs(A).sum(1)
+    d = rs * scale if scale else rs + rng.uniform(1, 2, n)
+    np.fill_diagonal(A, d * rng.choice([-1.0, 1.0], n))
+    if f32:
+        A = A.astype(np.float32)
+    xs = rng.uniform(-1, 1, n)
+    b = A.astype(np.float64) @ xs
+    return A, b, xs
+
+
+# ------------------------------------------------------------------ configs c1 / c2
+def test_c1_fixed_200_and_tol_stop(jb):
+    A, b, xs = g.host_system(g.CONFIGS["c1"])
+    st_o, x_o, it_o, h_o = oracle.jacobi(A, b, None, 200, 0.0, nthreads=8, history=True)
+    with jb.Plan(A) as p:
+        r = p.solve(b, None, 200, 0.0, history=True)
+        assert (r.status, r.iters) == (jb.MAX_ITER, it_o) == (jb.MAX_ITER, 200)
+        assert rel_linf(r.x, x_o) <= TOL64
+        assert np.max(np.abs(r.x - xs)) <= 1e-12  # P8 planted
+        # tol = 1e-12 stop run (BASELINE.json configs[0]); same iteration count as the oracle
+        st_o, x_o, it_o, h_o = oracle.jacobi(A, b, None, 200, 1e-12, history=True)
+        r = p.solve(b, None, 200, 1e-12, history=True)
+        assert (r.status, r.iters) == (st_o, it_o) == (jb.CONVERGED, 12)
+        assert rel_linf(r.x, x_o) <= TOL64
+        np.testing.assert_allclose(r.hist, h_o, rtol=1e-6, atol=1e-15)
+
+
+def test_c2_parity_and_planted(jb):
+    A, b, xs = g.host_system(g.CONFIGS["c2"])
+    st_o, x_o, it_o, h_o = oracle.jacobi(A, b, None, 40, 0.0, nthreads=16, history=True)
+    with jb.Plan(A) as p:
+        r = p.solve(b, None, 40, 0.0, history=True)
+        assert r.iters == 40 and rel_linf(r.x, x_o) <= TOL64
+        np.testing.assert_allclose(r.hist[:8], h_o[:8], rtol=1e-9)
+        r = p.solve(b, None, 500, 0.0)  # configs[1]: fixed 500 iterations
+        assert (r.status, r.iters) == (jb.MAX_ITER, 500)
+        assert np.max(np.abs(r.x - xs)) <= 1e-12
+
+
+# ------------------------------------------------------------------ early sweeps (in-place race guard)
+def test_early_sweeps_match_one_by_one(jb):
+    A, b, _ = dominant(1500, 1, scale=1.05)
+    x0 = np.random.default_rng(2).uniform(-1, 1, 1500)
+    with jb.Plan(A) as p:
+        xo = x0.copy()
+        for k in range(1, 9):
+            xo = oracle.sweep_rows(A, 0, b, xo)
+            r = p.solve(b, x0, k, 0.0)
+            assert r.iters == k and rel_linf(r.x, xo) <= 1e-13, k
+
+
+# ------------------------------------------------------------------ P3: sweep 1 from zero, bitwise
+@pytest.mark.parametrize("n", [1, 2, 3, 7, 31, 33, 127, 257, 1000, 4099])
+def test_p3_first_sweep_bitwise_ragged(jb, n):
+    A, b, _ = dominant(n, n)
+    st, x_o, it = oracle.jacobi(A, b, None, 1, 0.0)
+    r = jb.solve(A, b, None, 1, 0.0)
+    assert r.iters == 1 and np.array_equal(r.x, x_o)
+
+
+# ------------------------------------------------------------------ ragged sizes, tol stops
+@pytest.mark.parametrize("n", [1, 2, 5, 64, 255, 513, 2049, 5000])
+def test_ragged_sizes_parity(jb, n):
+    A, b, xs = dominant(n, 100 + n, scale=1.05)
+    st_o, x_o, it_o, h_o = oracle.jacobi(A, b, None, 30, 0.0, nthreads=8, history=True)
+    with jb.Plan(A) as p:
+        r = p.solve(b, None, 30, 0.0, history=True)
+        assert r.iters == 30 and rel_linf(r.x, x_o) <= TOL64
+        st_o, x_o, it_o = oracle.jacobi(A, b, None, 1000, 1e-9, nthreads=8)
+        r = p.solve(b, None, 1000, 1e-9)
+        assert (r.status, r.iters) == (st_o, it_o)
+        assert rel_linf(r.x, x_o) <= TOL64
+
+
+def test_fp32_storage_parity(jb):
+    for n in (1000, 3000):
+        A, b, xs = dominant(n, 7 + n, scale=1.2, f32=True)
+        st_o, x_o, it_o = oracle.jacobi(A, b, None, 25, 0.0, nthreads=8)
+        r = jb.solve(A, b, None, 25, 0.0)
+        assert r.iters == 25 and rel_linf(r.x, x_o) <= 1e-10  # self-check; official bar TOL32
+        st_o, x_o, it_o = oracle.jacobi(A, b, None, 2000, 1e-6, nthreads=8)
+        r = jb.solve(A, b, None, 2000, 1e-6)
+        assert (r.status, r.iters) == (st_o, it_o) and rel_linf(r.x, x_o) <= TOL32
+    cfg = g.GenConfig(2048, a_dtype=g.F32, diag_mode=g.DIAG_SCALE, diag_scale=1.2)  # c5 recipe, small n
+    A, b, xs = g.host_system(cfg)
+    st_o, x_o, it_o = oracle.jacobi(A, b, None, 2000, 1e-6, nthreads=8)
+    r = jb.solve(A, b, None, 2000, 1e-6)
+    assert (r.status, r.iters) == (st_o, it_o) and rel_linf(r.x, x_o) <= TOL32
+
+
+# ------------------------------------------------------------------ invariances (bitwise)
+def test_p12a_row_block_launches_bitwise(jb):
+    A, b, _ = dominant(4096, 12, scale=1.05)
+    with jb.Plan(A) as p:
+        ref = p.solve(b, None, 15, 0.0, history=True)
+        for nb in (2, 4, 8, 16):
+            p.set_row_blocks(nb)
+            r = p.solve(b, None, 15, 0.0, history=True)
+            assert np.array_equal(r.x, ref.x) and np.array_equal(r.hist, ref.hist), nb
+        p.set_row_blocks(4)
+        r1 = p.solve(b, None, 500, 1e-10)
+        p.set_row_blocks(1)
+        r2 = p.solve(b, None, 500, 1e-10)
+        assert r1.iters == r2.iters and np.array_equal(r1.x, r2.x)
+
+
+def test_p13_p11_determinism_split_and_batch(jb):
+    A, b, _ = dominant(3000, 13, scale=1.02)
+    with jb.Plan(A) as p:
+        a = p.solve(b, None, 37, 0.0, history=True)
+        a2 = p.solve(b, None, 37, 0.0, history=True)
+        assert np.array_equal(a.x, a2.x) and np.array_equal(a.hist, a2.hist)  # P13
+        h1 = p.solve(b, None, 20, 0.0, history=True)
+        h2 = p.solve(b, h1.x, 17, 0.0, history=True)
+        assert np.array_equal(h2.x, a.x) and np.array_equal(np.concatenate([h1.hist, h2.hist]), a.hist)  # P11
+        for K in (4, 8, 64, 1024):
+            p.set_batch(K)
+            r = p.solve(b, None, 37, 0.0, history=True)
+            assert r.iters == 37 and np.array_equal(r.x, a.x), K
+            c = p.solve(b, None, 5000, 1e-11)
+            p.set_batch(32)
+            c32 = p.solve(b, None, 5000, 1e-11)
+            assert (c.status, c.iters) == (c32.status, c32.iters) and np.array_equal(c.x, c32.x)
+
+
+# ------------------------------------------------------------------ P14: divergent paper regime
+@pytest.mark.parametrize("n", [8, 64, 512])
+def test_p14_divergence_nan_semantics(jb, n):
+    rng = np.random.default_rng(14)
+    A = rng.uniform(0, 1, (n, n))
+    b = rng.uniform(0, 1, n)
+    x0 = rng.uniform(0, 1, n)
+    st_o, x_o, it_o, h_o = oracle.jacobi(A, b, x0, 1000, 1e-8, history=True)
+    with jb.Plan(A) as p:
+        r = p.solve(b, x0, 1000, 1e-8, history=True)
+    assert (r.status, r.iters) == (st_o, it_o) == (jb.MAX_ITER, 1000)
+    bad_o = np.argmax(~np.isfinite(h_o))
+    bad_g = np.argmax(~np.isfinite(r.hist))
+    assert abs(int(bad_o) - int(bad_g)) <= 1 and (~np.isfinite(r.hist[bad_g:])).all()
+    assert not np.isfinite(r.x).all() and not np.isfinite(x_o).all()
+
+
+# ------------------------------------------------------------------ errors and edge cases
+def test_errors_and_edges_on_gpu(jb):
+    A = np.array([[2.0, 1.0], [1.0, 3.0]])
+    b = np.array([3.0, 4.0])
+    r = jb.solve(A, b, None, 1000, 1e-12)
+    assert (r.status, r.iters) == (jb.CONVERGED, 33)  # P1 on the GPU
+    Z = np.eye(6)
+    Z[4, 4] = 0.0
+    Z[2, 2] = 0.0
+    with pytest.raises(jb.JacobiError) as e:
+        jb.solve(Z, np.ones(6), None, 5, 0.0)
+    assert e.value.status == jb.EZERODIAG and "i = 2" in str(e.value)
+    An = np.eye(3)
+    An[0, 2] = np.nan
+    with pytest.raises(jb.JacobiError) as e:
+        jb.solve(An, np.ones(3), None, 5, 0.0)
+    assert e.value.status == jb.ENONFINITE
+    with pytest.raises(jb.JacobiError) as e:
+        jb.solve(np.eye(3), np.array([1.0, np.inf, 0.0]), None, 5, 0.0)
+    assert e.value.status == jb.ENONFINITE
+    x0 = np.array([0.25, -0.5])
+    r = jb.solve(A, b, x0, 0, 1e-3)
+    assert (r.status, r.iters) == (jb.MAX_ITER, 0) and np.array_equal(r.x, x0)
+    r = jb.solve(A, b, None, 7, math.inf)
+    assert (r.status, r.iters) == (jb.CONVERGED, 1)
+    P5A = np.array([[4.0, -2, 1], [1, 5, -3], [2, 2, 6]])
+    r = jb.solve(P5A, np.array([3.0, 2, 24]), np.array([1.0, 2, 3]), 10, 1e-300)
+    assert (r.status, r.iters) == (jb.CONVERGED, 1) and np.array_equal(r.x, [1.0, 2.0, 3.0])  # P5
+
+
+def test_device_borrowed_A_and_device_solve(jb):
+    import torch
+    n = 3000
+    A, b, xs = dominant(n, 21)
+    dA = torch.empty((n, 3008), dtype=torch.float64, device="cuda")
+    dA[:, n:] = float("nan")  # padding must never be read into a sum
+    dA[:, :n] = torch.from_numpy(A).cuda()
+    st_o, x_o, it_o = oracle.jacobi(A, b, None, 20, 0.0, nthreads=8)
+    with jb.Plan(dA[:, :n], n=n) as p:
+        assert p.info.a_borrowed == 1 and p.info.lda == 3008
+        db = torch.from_numpy(b).cuda()
+        dx0 = torch.zeros(n, dtype=torch.float64, device="cuda")
+        dxo = torch.empty(n, dtype=torch.float64, device="cuda")
+        hist = torch.empty(20, dtype=torch.float64, device="cuda")
+        r = p.solve_device(db, dx0, dxo, 20, 0.0, hist=hist)
+        assert r.iters == 20 and rel_linf(dxo.cpu().numpy(), x_o) <= TOL64
+        r2 = p.solve(b, None, 20, 0.0, history=True)
+        assert np.array_equal(r2.x, dxo.cpu().numpy()) and np.array_equal(r2.hist, hist.cpu().numpy())
+        ms = p.time_sweeps(db, dx0, 3)
+        assert ms.shape == (3,) and (ms > 0).all()
+
+
+def test_bwprobe_sane(jb):
+    gbs = jb.bwprobe(4 << 30, 3)
+    assert 3000 < gbs < 9000
+
+
+# ------------------------------------------------------------------ full-size configs (sampled parity)
+def _device_system(jb, cfg):
+    import torch
+    n = cfg.n
+    dt = torch.float32 if cfg.a_dtype == g.F32 else torch.float64
+    dA = torch.empty((n, n), dtype=dt, device="cuda")
+    db = torch.empty(n, dtype=torch.float64, device="cuda")
+    g.device_rows(cfg, 0, n, dA.data_ptr(), n, db.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    return dA, db
+
+
+@pytest.mark.parametrize("name", ["c4", "c5"])
+def test_full_size_sampled_parity(jb, name):
+    """BASELINE.json configs[3]/[4] at full size in the bench's launch configuration: sweeps 1 and 2
+    on sampled rows against the oracle (rows regenerated on the host), generator twin parity on the
+    same rows, and the planted solution after the fixed iteration count."""
+    import torch
+    cfg = g.CONFIGS[name]
+    n = cfg.n
+    dA, db = _device_system(jb, cfg)
+    rng = np.random.default_rng(0)
+    rows = np.unique(np.concatenate([[0, 1, n // 2, n - 2, n - 1], rng.integers(0, n, 11)]))
+    diag_all, b_all = g.host_diag_b(cfg, 0, n)  # oracle-side inputs from the host generator
+    assert np.array_equal(db.cpu().numpy(), b_all)  # device twin == host generator (b)
+    x1_orc = b_all / diag_all  # P3 closed form of sweep 1 from x0 = 0 (exact for any summation order)
+    with jb.Plan(dA) as p:
+        dx0 = torch.zeros(n, dtype=torch.float64, device="cuda")
+        dxo = torch.empty(n, dtype=torch.float64, device="cuda")
+        r = p.solve_device(db, dx0, dxo, 1, 0.0)
+        x1 = dxo.cpu().numpy()
+        r = p.solve_device(db, dx0, dxo, 2, 0.0)
+        x2 = dxo.cpu().numpy()
+        for i in rows:
+            Ar, br = g.host_rows(cfg, int(i), int(i) + 1)
+            assert np.array_equal(dA[int(i)].cpu().numpy(), Ar[0])  # device twin == host generator (A)
+            x1_i = oracle.sweep_rows(Ar, int(i), br, np.zeros(n))
+            assert x1[i] == x1_i[0] == x1_orc[i]  # P3 bitwise (oracle row and closed form)
+            x2_i = oracle.sweep_rows(Ar, int(i), br, x1_orc)
+            assert abs(x2[i] - x2_i[0]) <= TOL64 * np.max(np.abs(x1_orc))
+        if name == "c4":
+            r = p.solve_device(db, dx0, dxo, 100, 0.0)  # configs[3]: fixed 100 iterations
+            assert (r.status, r.iters) == (jb.MAX_ITER, 100)
+        else:
+            r = p.solve_device(db, dx0, dxo, 2000, 1e-6)  # configs[4]: tol 1e-6 or 2000
+            assert r.status == jb.CONVERGED and 2 <= r.iters <= 10
+        xs = g.host_xstar(cfg)
+        err = np.max(np.abs(dxo.cpu().numpy() - xs))
+        assert err <= (1e-12 if name == "c4" else 1e-5)
+    del dA
+    torch.cuda.empty_cache()
