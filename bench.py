@@ -319,7 +319,7 @@ def main():
             "effective_gbs_per_gpu": achieved, "effective_gbs_aggregate": achieved * world,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(args.workload),
-                         "peak_source": peak_src, "kernel": "k_sweep<double,4,2>" if dt == torch.float64 else "k_sweep<float,4,1>",
+                         "peak_source": peak_src, "kernel": f"k_sweep<{'double' if dt == torch.float64 else 'float'},R={info.rows_per_warp}>",
                          "bytes_per_launch": bytes_sweep, "avg_launch_ms": sweep_ms,
                          "kernel_only_ms": kernel_ms, "kernel_only_gbs": bytes_sweep / (kernel_ms * 1e-3) / 1e9,
                          "read_ceiling_gbs": ceiling,

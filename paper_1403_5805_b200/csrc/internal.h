@@ -40,10 +40,8 @@ struct SweepArgs {
   int tiles;                // ceil(m / R)
 };
 
-enum { kThreads = 512 };    // threads per CTA of the sweep kernel
-
 // Launchers (sweep.cu).  Return cudaGetLastError() of the launch.
-cudaError_t launch_sweep(int dtype, const SweepArgs& a, int j, int grid, cudaStream_t s);
+cudaError_t launch_sweep(int dtype, int variant, const SweepArgs& a, int j, int grid, cudaStream_t s);
 cudaError_t launch_advance(State* st, unsigned long long* dslot, int K, cudaStream_t s);
 cudaError_t launch_setup_diag(int dtype, const void* A, int64_t lda, int64_t m, int64_t row0,
                               double* diag, unsigned long long* zero_min, cudaStream_t s);
@@ -52,8 +50,11 @@ cudaError_t launch_scan_nonfinite_A(int dtype, const void* A, int64_t lda, int64
 cudaError_t launch_scan_nonfinite_vec(const double* v, int64_t len, int* flag, cudaStream_t s);
 cudaError_t launch_copy_pitched(int dtype, const void* src, int64_t src_ld, void* dst, int64_t dst_ld,
                                 int64_t rows, int64_t n, cudaStream_t s);
-int sweep_rows_per_warp(int dtype);
-int sweep_grid(int dtype, int num_sms);
+int num_variants();
+int default_variant(int dtype);
+int variant_rows(int variant);
+int variant_threads(int variant);
+int sweep_grid(int dtype, int variant, int num_sms);
 int chunk_for(int64_t n);
 double bwprobe(int64_t nbytes, int reps);
 
@@ -65,6 +66,7 @@ struct jacobi_plan {
   int dtype = JACOBI_F64, rank = 0, nranks = 1;
   int device = 0, num_sms = 0, grid = 0;
   int nblocks = 1;               // P12(a) row-block emulation
+  int variant = 0;               // sweep kernel variant (R, U, threads); default per dtype, JACOBI_SWEEP_VARIANT overrides
   int batch = 32;                // sweeps per graph batch
   bool own_stream = false, a_borrowed = false;
   cudaStream_t stream = nullptr;

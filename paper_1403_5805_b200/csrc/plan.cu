@@ -8,6 +8,7 @@
 #include "internal.h"
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -86,7 +87,12 @@ int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dty
     }
   }
   p->chunk = jacobi::chunk_for(n);
-  p->grid = jacobi::sweep_grid(dtype, p->num_sms);
+  p->variant = jacobi::default_variant(dtype);
+  if (const char* v = getenv("JACOBI_SWEEP_VARIANT")) {
+    int vi = atoi(v);
+    if (vi >= 0 && vi < jacobi::num_variants()) p->variant = vi;
+  }
+  p->grid = jacobi::sweep_grid(dtype, p->variant, p->num_sms);
   p->x_len = round_up(n, 256) + 256;
   const int64_t nchunks = (n + p->chunk - 1) / p->chunk;
   JCUDA(cudaMalloc(&p->diag, (size_t)m * 8));
@@ -179,9 +185,9 @@ extern "C" int jacobi_plan_info(const jacobi_plan* p, jacobi_plan_info_t* info) 
   info->rank = p->rank;
   info->nranks = p->nranks;
   info->chunk_cols = p->chunk;
-  info->rows_per_warp = jacobi::sweep_rows_per_warp(p->dtype);
+  info->rows_per_warp = jacobi::variant_rows(p->variant);
   info->grid_ctas = p->grid;
-  info->threads_per_cta = jacobi::kThreads;
+  info->threads_per_cta = jacobi::variant_threads(p->variant);
   info->a_borrowed = p->a_borrowed ? 1 : 0;
   info->sweeps_launched = p->sweeps_launched;
   const double sA = p->dtype == JACOBI_F32 ? 4.0 : 8.0;
@@ -208,7 +214,7 @@ static jacobi::SweepArgs sweep_args(const jacobi_plan* p, int blk) {
   a.st = p->st;
   a.chunk = p->chunk;
   a.nchunks = (int)((p->n + p->chunk - 1) / p->chunk);
-  const int R = jacobi::sweep_rows_per_warp(p->dtype);
+  const int R = jacobi::variant_rows(p->variant);
   a.tiles = (int)((mb + R - 1) / R);
   return a;
 }
@@ -217,7 +223,7 @@ static jacobi::SweepArgs sweep_args(const jacobi_plan* p, int blk) {
 // (SURVEY.md §8(a) a6): in-place allgather of the new x slice and max-allreduce of d_k's bits.
 static int enqueue_sweep(jacobi_plan* p, int j) {
   for (int blk = 0; blk < p->nblocks; ++blk)
-    JCUDA(jacobi::launch_sweep(p->dtype, sweep_args(p, blk), j, p->grid, p->stream));
+    JCUDA(jacobi::launch_sweep(p->dtype, p->variant, sweep_args(p, blk), j, p->grid, p->stream));
   if (p->comm) {
     // k = kbase + j + 1 with kbase a multiple of the batch size (a multiple of 4): parity is static.
     double* xk = p->x[(j + 1) & 1];
@@ -397,7 +403,7 @@ extern "C" int jacobi_plan_time_sweeps(jacobi_plan* p, const double* d_b, const 
   for (int j = 0; j < sweeps && rc == 0; ++j) {
     cudaEventRecord(e0, p->stream);
     for (int blk = 0; blk < p->nblocks; ++blk) {
-      cudaError_t e = jacobi::launch_sweep(p->dtype, sweep_args(p, blk), j, p->grid, p->stream);
+      cudaError_t e = jacobi::launch_sweep(p->dtype, p->variant, sweep_args(p, blk), j, p->grid, p->stream);
       if (e != cudaSuccess) rc = jacobi_set_error(JACOBI_ECUDA, cudaGetErrorString(e));
     }
     cudaEventRecord(e1, p->stream);

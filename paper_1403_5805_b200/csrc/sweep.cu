@@ -72,8 +72,8 @@ __device__ __forceinline__ bool sweep_prologue(const SweepArgs& a, int j, bool l
   return true;
 }
 
-template <typename T, int R, int U>
-__global__ void __launch_bounds__(kThreads, 1) k_sweep(const SweepArgs a, const int j) {
+template <typename T, int R, int U, int NT>
+__global__ void __launch_bounds__(NT, (NT < 512 ? 512 / NT : 1)) k_sweep(const SweepArgs a, const int j) {
   constexpr int E = VecOf<T>::E;
   constexpr int S = 32 * E;  // columns per warp step
   __shared__ int s_go;
@@ -266,13 +266,31 @@ __global__ void k_fill(double* buf, int64_t n) {
     buf[i] = (double)(i & 1023);
 }
 
-// Sweep variants: (R rows per warp, U steps in flight).  All variants produce identical bits.
-constexpr int kR64 = 4, kU64 = 2;
-constexpr int kR32 = 4, kU32 = 1;
+// Sweep variants: (R rows per warp, U steps in flight per lane, threads per CTA).  All variants
+// produce identical bits (the summation order does not depend on R, U or the grid); the default is
+// chosen from measurements (profiles/), others stay selectable with JACOBI_SWEEP_VARIANT for tuning.
+struct Variant {
+  int R, threads;
+  void (*f64)(const SweepArgs, const int);
+  void (*f32)(const SweepArgs, const int);
+};
+const Variant kVariants[] = {
+    {4, 512, k_sweep<double, 4, 2, 512>, k_sweep<float, 4, 1, 512>},
+    {8, 512, k_sweep<double, 8, 1, 512>, k_sweep<float, 8, 1, 512>},
+    {2, 512, k_sweep<double, 2, 4, 512>, k_sweep<float, 2, 2, 512>},
+    {4, 512, k_sweep<double, 4, 1, 512>, k_sweep<float, 4, 2, 512>},
+    {4, 256, k_sweep<double, 4, 2, 256>, k_sweep<float, 4, 1, 256>},
+    {2, 1024, k_sweep<double, 2, 1, 1024>, k_sweep<float, 2, 1, 1024>},
+};
+constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 }  // namespace
 
-int sweep_rows_per_warp(int dtype) { return dtype == JACOBI_F32 ? kR32 : kR64; }
+int num_variants() { return kNumVariants; }
+// Measured on B200 (profiles/variants_r01_*.jsonl): fp64 R=8,U=1 (7150 GB/s at c4); fp32 R=4,U=1.
+int default_variant(int dtype) { return dtype == JACOBI_F32 ? 0 : 1; }
+int variant_rows(int v) { return kVariants[v].R; }
+int variant_threads(int v) { return kVariants[v].threads; }
 
 int chunk_for(int64_t n) {
   // ~16+ chunks per row when n allows (load balance over the persistent grid), 512..4096 columns.
@@ -281,18 +299,19 @@ int chunk_for(int64_t n) {
   return (int)c;
 }
 
-int sweep_grid(int dtype, int num_sms) {
+int sweep_grid(int dtype, int v, int num_sms) {
   int per_sm = 0;
-  cudaError_t e = dtype == JACOBI_F32
-      ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<float, kR32, kU32>, kThreads, 0)
-      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sweep<double, kR64, kU64>, kThreads, 0);
+  const Variant& V = kVariants[v];
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dtype == JACOBI_F32 ? V.f32 : V.f64,
+                                                                V.threads, 0);
   if (e != cudaSuccess || per_sm < 1) per_sm = 1;
   return num_sms * per_sm;
 }
 
-cudaError_t launch_sweep(int dtype, const SweepArgs& a, int j, int grid, cudaStream_t s) {
-  if (dtype == JACOBI_F32) k_sweep<float, kR32, kU32><<<grid, kThreads, 0, s>>>(a, j);
-  else k_sweep<double, kR64, kU64><<<grid, kThreads, 0, s>>>(a, j);
+cudaError_t launch_sweep(int dtype, int v, const SweepArgs& a, int j, int grid, cudaStream_t s) {
+  const Variant& V = kVariants[v];
+  if (dtype == JACOBI_F32) V.f32<<<grid, V.threads, 0, s>>>(a, j);
+  else V.f64<<<grid, V.threads, 0, s>>>(a, j);
   return cudaGetLastError();
 }
 
