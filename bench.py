@@ -214,9 +214,8 @@ def main():
     dxo = torch.empty(n, dtype=torch.float64, device="cuda")
     torch.cuda.synchronize()
     if world > 1:
-        uid = [jb.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        plan = jb.Plan(dA, n=n, stream=sh, dist=(uid[0], rank, world))
+        from paper_1403_5805_b200.dist import dist_plan
+        plan = dist_plan(dA, n, stream=sh)
     else:
         plan = jb.Plan(dA, n=n, stream=sh)
     K = 20 if sweeps % 20 == 0 else 4
