@@ -51,7 +51,9 @@ cudaError_t launch_scan_nonfinite_vec(const double* v, int64_t len, int* flag, c
 cudaError_t launch_copy_pitched(int dtype, const void* src, int64_t src_ld, void* dst, int64_t dst_ld,
                                 int64_t rows, int64_t n, cudaStream_t s);
 int num_variants();
-int default_variant(int dtype);
+int default_variant(int dtype, int nchunks);
+bool variant_is_cta(int variant);
+bool variant_fits(int variant, int nchunks);
 int variant_rows(int variant);
 int variant_threads(int variant);
 int sweep_grid(int dtype, int variant, int num_sms);

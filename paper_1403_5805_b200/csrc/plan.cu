@@ -87,10 +87,11 @@ int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dty
     }
   }
   p->chunk = jacobi::chunk_for(n);
-  p->variant = jacobi::default_variant(dtype);
-  if (const char* v = getenv("JACOBI_SWEEP_VARIANT")) {
+  const int nch = (int)((n + p->chunk - 1) / p->chunk);
+  p->variant = jacobi::default_variant(dtype, nch);
+  if (const char* v = getenv("JACOBI_SWEEP_VARIANT")) {  // tuning override (all variants: same bits)
     int vi = atoi(v);
-    if (vi >= 0 && vi < jacobi::num_variants()) p->variant = vi;
+    if (vi >= 0 && vi < jacobi::num_variants() && jacobi::variant_fits(vi, nch)) p->variant = vi;
   }
   p->grid = jacobi::sweep_grid(dtype, p->variant, p->num_sms);
   p->x_len = round_up(n, 256) + 256;

@@ -72,10 +72,73 @@ __device__ __forceinline__ bool sweep_prologue(const SweepArgs& a, int j, bool l
   return true;
 }
 
-template <typename T, int R, int U, int NT>
-__global__ void __launch_bounds__(NT, (NT < 512 ? 512 / NT : 1)) k_sweep(const SweepArgs a, const int j) {
+// Sum of one column chunk [c0, c1) of R rows against x^(k-1), in the fixed order every kernel
+// variant shares: lane l owns columns c0 + (32*s + l)*E + e, accumulated in ascending s then e with
+// one DFMA chain per row; j == i (the diagonal) and j >= n are skipped.  Rows r >= nv
+// are not loaded (their sums are unused).
+template <typename T, int R, int U>
+__device__ __forceinline__ void accumulate_chunk(const T* const (&rowp)[R], const int nv,
+                                                 const double* __restrict__ xo, const int64_t c0,
+                                                 const int64_t c1, const int chunk, const int64_t n,
+                                                 const int64_t g0, const int lane, double (&acc)[R]) {
   constexpr int E = VecOf<T>::E;
   constexpr int S = 32 * E;  // columns per warp step
+  const int nsteps = chunk / S;
+  const bool masked = (c1 - c0 != chunk) || (g0 < c1 && g0 + R > c0);
+  if (!masked) {
+    for (int s = 0; s < nsteps; s += U) {
+      T av[U][R][E];
+      double xv[U][E];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t col = c0 + (int64_t)((s + u) * 32 + lane) * E;
+        ld_x<E>(xo + col, xv[u]);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (r < nv) ld_a(rowp[r] + col, av[u][r]);
+          else {
+#pragma unroll
+            for (int e = 0; e < E; ++e) av[u][r][e] = T(0);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int e = 0; e < E; ++e) acc[r] = __fma_rn((double)av[u][r][e], xv[u][e], acc[r]);
+    }
+  } else {
+    // Diagonal chunk or ragged tail: same order, j == i and j >= n terms skipped.
+    for (int s = 0; s < nsteps; ++s) {
+      const int64_t col = c0 + (int64_t)(s * 32 + lane) * E;
+      if (col < n) {
+        T av[R][E];
+        double xv[E];
+        ld_x<E>(xo + col, xv);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (r < nv) ld_a(rowp[r] + col, av[r]);
+          else {
+#pragma unroll
+            for (int e = 0; e < E; ++e) av[r][e] = T(0);
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int64_t cc = col + e;
+            if (cc < n && cc != g0 + r) acc[r] = __fma_rn((double)av[r][e], xv[e], acc[r]);
+          }
+      }
+    }
+  }
+}
+
+template <typename T, int R, int U, int NT>
+__global__ void __launch_bounds__(NT, (NT < 512 ? 512 / NT : 1)) k_sweep(const SweepArgs a, const int j) {
   __shared__ int s_go;
   if (threadIdx.x == 0) s_go = sweep_prologue(a, j, blockIdx.x == 0);
   __syncthreads();
@@ -88,7 +151,6 @@ __global__ void __launch_bounds__(NT, (NT < 512 ? 512 / NT : 1)) k_sweep(const S
   const int lane = threadIdx.x & 31;
   const int64_t W = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t items = (int64_t)a.tiles * a.nchunks;
-  const int nsteps = a.chunk / S;
 
   for (int64_t it = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); it < items; it += W) {
     const int tile = (int)(it % a.tiles);
@@ -104,45 +166,7 @@ __global__ void __launch_bounds__(NT, (NT < 512 ? 512 / NT : 1)) k_sweep(const S
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[r] = 0.0;
 
-    const bool masked = (c1 - c0 != a.chunk) || (g0 < c1 && g0 + R > c0);
-    if (!masked) {
-      for (int s = 0; s < nsteps; s += U) {
-        T av[U][R][E];
-        double xv[U][E];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t col = c0 + (int64_t)((s + u) * 32 + lane) * E;
-          ld_x<E>(xo + col, xv[u]);
-#pragma unroll
-          for (int r = 0; r < R; ++r) ld_a(rowp[r] + col, av[u][r]);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-          for (int r = 0; r < R; ++r)
-#pragma unroll
-            for (int e = 0; e < E; ++e) acc[r] = __fma_rn((double)av[u][r][e], xv[u][e], acc[r]);
-      }
-    } else {
-      // Diagonal chunk or ragged tail: same order, j == i and j >= n terms skipped.
-      for (int s = 0; s < nsteps; ++s) {
-        const int64_t col = c0 + (int64_t)(s * 32 + lane) * E;
-        if (col < a.n) {
-          T av[R][E];
-          double xv[E];
-          ld_x<E>(xo + col, xv);
-#pragma unroll
-          for (int r = 0; r < R; ++r) ld_a(rowp[r] + col, av[r]);
-#pragma unroll
-          for (int r = 0; r < R; ++r)
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-              const int64_t cc = col + e;
-              if (cc < a.n && cc != g0 + r) acc[r] = __fma_rn((double)av[r][e], xv[e], acc[r]);
-            }
-        }
-      }
-    }
+    accumulate_chunk<T, R, U>(rowp, R, xo, c0, c1, a.chunk, a.n, g0, lane, acc);
     // Butterfly: every lane ends with the same, order-fixed row sums.
 #pragma unroll
     for (int r = 0; r < R; ++r)
@@ -185,6 +209,118 @@ __global__ void __launch_bounds__(NT, (NT < 512 ? 512 / NT : 1)) k_sweep(const S
       a.cnt[tile] = 0u;
     }
   }
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// k_sweep_cta: the large-n sweep.  CTA b of G owns the contiguous rows [b*m/G, (b+1)*m/G) (balanced
+// to one row), processed in tiles of R rows.  For each tile, warp w streams the chunks c = w, w+NW,
+// ... of the tile's rows (same per-chunk order as accumulate_chunk) and lane 0 publishes the R
+// butterfly sums to a shared-memory slot; an mbarrier per slot counts the NW contributions.  The
+// tile's finalizer warp (tile % NW, one tile late so it never idles on its own tile) adds the chunk
+// partials in ascending chunk order — exactly the order of k_sweep — and applies the fused epilogue.
+// No global atomics or fences per tile: one atomicMax of the warp's max|dx| bits per sweep.
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n W_%=: mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n @!p bra W_%=;\n}" ::"r"(
+          (unsigned)__cvta_generic_to_shared(b)),
+      "r"(parity)
+      : "memory");
+}
+
+constexpr int kSlots = 4;
+
+template <typename T, int R, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, const int j) {
+  extern __shared__ __align__(16) double s_part[];  // [kSlots][nchunks][R]
+  __shared__ __align__(8) uint64_t s_full[kSlots], s_empty[kSlots];
+  __shared__ int s_go;
+  if (threadIdx.x == 0) {
+    s_go = sweep_prologue(a, j, blockIdx.x == 0);
+    for (int q = 0; q < kSlots; ++q) {
+      mbar_init(&s_full[q], NW);
+      mbar_init(&s_empty[q], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (!s_go) return;
+
+  const int64_t k = a.st->kbase + j + 1;
+  const double* __restrict__ xo = (k & 1) ? a.x0buf : a.x1buf;  // x^(k-1)
+  double* __restrict__ xn = (k & 1) ? a.x1buf : a.x0buf;        // x^(k)
+  const T* __restrict__ A = static_cast<const T*>(a.A);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nch = a.nchunks;
+  const int64_t rb = (int64_t)blockIdx.x * a.m / gridDim.x;
+  const int64_t re = (int64_t)(blockIdx.x + 1) * a.m / gridDim.x;
+  const int ntile = (int)((re - rb + R - 1) / R);
+  unsigned long long dmax = 0ull;
+
+  auto finalize = [&](int t) {
+    const int q = t % kSlots;
+    mbar_wait(&s_full[q], (unsigned)((t / kSlots) & 1));
+    const int64_t r0 = rb + (int64_t)t * R;
+    const int nv = (int)min((int64_t)R, re - r0);
+    if (lane < nv) {
+      const double* sp = s_part + (size_t)q * nch * R + lane;
+      double s = sp[0];
+      for (int c = 1; c < nch; ++c) s += sp[(size_t)c * R];
+      const int64_t row = r0 + lane;
+      const double xnew = __ddiv_rn(__dsub_rn(a.b[row], s), a.diag[row]);
+      const int64_t gi = a.row0 + row;
+      xn[gi] = xnew;
+      const unsigned long long bits =
+          (unsigned long long)__double_as_longlong(__dsub_rn(xnew, xo[gi])) & 0x7fffffffffffffffull;
+      dmax = bits > dmax ? bits : dmax;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&s_empty[q]);
+  };
+
+  for (int t = 0; t < ntile; ++t) {
+    const int q = t % kSlots;
+    const int64_t r0 = rb + (int64_t)t * R;
+    const int nv = (int)min((int64_t)R, re - r0);
+    if (t >= kSlots) mbar_wait(&s_empty[q], (unsigned)(((t / kSlots) - 1) & 1));
+    const T* rowp[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) rowp[r] = A + (r0 + min(r, nv - 1)) * a.lda;
+    const int64_t g0 = a.row0 + r0;
+    for (int c = w; c < nch; c += NW) {
+      double acc[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] = 0.0;
+      const int64_t c0 = (int64_t)c * a.chunk;
+      const int64_t c1 = min(c0 + (int64_t)a.chunk, a.n);
+      accumulate_chunk<T, R, 1>(rowp, nv, xo, c0, c1, a.chunk, a.n, g0, lane, acc);
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc[r] += __shfl_xor_sync(kFull, acc[r], off);
+      if (lane == 0) {
+        double* dst = s_part + ((size_t)q * nch + c) * R;
+#pragma unroll
+        for (int r = 0; r < R; ++r) dst[r] = acc[r];
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&s_full[q]);
+    if (t >= 1 && (t - 1) % NW == w) finalize(t - 1);
+  }
+  if (ntile >= 1 && (ntile - 1) % NW == w) finalize(ntile - 1);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const unsigned long long o = __shfl_xor_sync(kFull, dmax, off);
+    dmax = o > dmax ? o : dmax;
+  }
+  if (lane == 0) atomicMax(&a.dslot[k & 3], dmax);
 }
 
 // After a graph batch of K sweeps: settle the stop decision for the batch's last sweep (same rule
@@ -270,25 +406,38 @@ __global__ void k_fill(double* buf, int64_t n) {
 // produce identical bits (the summation order does not depend on R, U or the grid); the default is
 // chosen from measurements (profiles/), others stay selectable with JACOBI_SWEEP_VARIANT for tuning.
 struct Variant {
-  int R, threads;
+  int R, threads, cta;  // cta = 1: k_sweep_cta (needs nchunks >= threads/32 and shared memory)
   void (*f64)(const SweepArgs, const int);
   void (*f32)(const SweepArgs, const int);
 };
 const Variant kVariants[] = {
-    {4, 512, k_sweep<double, 4, 2, 512>, k_sweep<float, 4, 1, 512>},
-    {8, 512, k_sweep<double, 8, 1, 512>, k_sweep<float, 8, 1, 512>},
-    {2, 512, k_sweep<double, 2, 4, 512>, k_sweep<float, 2, 2, 512>},
-    {4, 512, k_sweep<double, 4, 1, 512>, k_sweep<float, 4, 2, 512>},
-    {4, 256, k_sweep<double, 4, 2, 256>, k_sweep<float, 4, 1, 256>},
-    {2, 1024, k_sweep<double, 2, 1, 1024>, k_sweep<float, 2, 1, 1024>},
+    {4, 512, 0, k_sweep<double, 4, 2, 512>, k_sweep<float, 4, 1, 512>},
+    {8, 512, 0, k_sweep<double, 8, 1, 512>, k_sweep<float, 8, 1, 512>},
+    {2, 512, 0, k_sweep<double, 2, 4, 512>, k_sweep<float, 2, 2, 512>},
+    {4, 512, 0, k_sweep<double, 4, 1, 512>, k_sweep<float, 4, 2, 512>},
+    {4, 256, 0, k_sweep<double, 4, 2, 256>, k_sweep<float, 4, 1, 256>},
+    {2, 1024, 0, k_sweep<double, 2, 1, 1024>, k_sweep<float, 2, 1, 1024>},
+    {8, 512, 1, k_sweep_cta<double, 8, 16>, k_sweep_cta<float, 8, 16>},
+    {4, 512, 1, k_sweep_cta<double, 4, 16>, k_sweep_cta<float, 4, 16>},
+    {8, 256, 1, k_sweep_cta<double, 8, 8>, k_sweep_cta<float, 4, 8>},
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 }  // namespace
 
 int num_variants() { return kNumVariants; }
-// Measured on B200 (profiles/variants_r01_*.jsonl): fp64 R=8,U=1 (7150 GB/s at c4); fp32 R=4,U=1.
-int default_variant(int dtype) { return dtype == JACOBI_F32 ? 0 : 1; }
+bool variant_is_cta(int v) { return kVariants[v].cta != 0; }
+size_t variant_smem(int v, int nchunks) { return kVariants[v].cta ? (size_t)kSlots * nchunks * kVariants[v].R * 8 : 0; }
+bool variant_fits(int v, int nchunks) {
+  return !kVariants[v].cta || (nchunks >= kVariants[v].threads / 32 && variant_smem(v, nchunks) <= 48 * 1024);
+}
+// Defaults from B200 measurements (profiles/variants_r01_*.jsonl): the CTA-cooperative kernel when
+// n has at least 16 chunks, else the item kernel (fp64 R=8,U=1; fp32 R=4,U=1).
+int default_variant(int dtype, int nchunks) {
+  const int big = dtype == JACOBI_F32 ? 7 : 6;
+  if (variant_fits(big, nchunks)) return big;
+  return dtype == JACOBI_F32 ? 0 : 1;
+}
 int variant_rows(int v) { return kVariants[v].R; }
 int variant_threads(int v) { return kVariants[v].threads; }
 
@@ -303,15 +452,16 @@ int sweep_grid(int dtype, int v, int num_sms) {
   int per_sm = 0;
   const Variant& V = kVariants[v];
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dtype == JACOBI_F32 ? V.f32 : V.f64,
-                                                                V.threads, 0);
+                                                                V.threads, V.cta ? 48 * 1024 : 0);
   if (e != cudaSuccess || per_sm < 1) per_sm = 1;
   return num_sms * per_sm;
 }
 
 cudaError_t launch_sweep(int dtype, int v, const SweepArgs& a, int j, int grid, cudaStream_t s) {
   const Variant& V = kVariants[v];
-  if (dtype == JACOBI_F32) V.f32<<<grid, V.threads, 0, s>>>(a, j);
-  else V.f64<<<grid, V.threads, 0, s>>>(a, j);
+  const size_t smem = variant_smem(v, a.nchunks);
+  if (dtype == JACOBI_F32) V.f32<<<grid, V.threads, smem, s>>>(a, j);
+  else V.f64<<<grid, V.threads, smem, s>>>(a, j);
   return cudaGetLastError();
 }
 

@@ -16,13 +16,15 @@ import paper_1403_5805_b200 as jb  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c4"
 sweeps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
-variants = [int(v) for v in sys.argv[3].split(",")] if len(sys.argv) > 3 else list(range(6))
+variants = [int(v) for v in sys.argv[3].split(",")] if len(sys.argv) > 3 else list(range(9))
 cfg = g.CONFIGS[name]
 n = cfg.n
 dt = torch.float32 if cfg.a_dtype == g.F32 else torch.float64
-dA = torch.empty((n, n), dtype=dt, device="cuda")
+pad = int(sys.argv[4]) if len(sys.argv) > 4 else 0  # row pitch padding (elements) experiment
+dA_full = torch.empty((n, n + pad), dtype=dt, device="cuda")
 db = torch.empty(n, dtype=torch.float64, device="cuda")
-g.device_rows(cfg, 0, n, dA.data_ptr(), n, db.data_ptr(), 0)
+g.device_rows(cfg, 0, n, dA_full.data_ptr(), n + pad, db.data_ptr(), 0)
+dA = dA_full[:, :n]
 dx0 = torch.zeros(n, dtype=torch.float64, device="cuda")
 xo = torch.empty(n, dtype=torch.float64, device="cuda")
 torch.cuda.synchronize()
@@ -39,5 +41,5 @@ for v in variants:
             ref = x
         med = float(np.median(ms[1:]))
         print(json.dumps({"workload": name, "variant": v, "R": inf.rows_per_warp, "threads": inf.threads_per_cta,
-                          "grid": inf.grid_ctas, "chunk": inf.chunk_cols, "median_ms": med, "min_ms": float(ms[1:].min()),
+                          "grid": inf.grid_ctas, "chunk": inf.chunk_cols, "lda": inf.lda, "median_ms": med, "min_ms": float(ms[1:].min()),
                           "gbs": inf.bytes_per_sweep / (med * 1e-3) / 1e9, "bitwise_equal_v0": same}), flush=True)

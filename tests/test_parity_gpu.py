@@ -289,3 +289,29 @@ def test_full_size_sampled_parity(jb, name):
         assert err <= (1e-12 if name == "c4" else 1e-5)
     del dA
     torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------------ kernel variants (same bits by design)
+@pytest.mark.parametrize("n", [3000, 8190, 16384])
+def test_all_sweep_variants_bitwise_identical(jb, n, monkeypatch):
+    """Every sweep-kernel variant (item kernel with R in {2,4,8}, CTA-cooperative kernel) must give
+    identical bits: the per-row summation order depends only on column indices (R10)."""
+    A, b, _ = dominant(n, 31 + n, scale=1.05)
+    st_o, x_o, it_o, h_o = oracle.jacobi(A, b, None, 12, 0.0, nthreads=16, history=True)
+    ref = None
+    for v in range(9):
+        monkeypatch.setenv("JACOBI_SWEEP_VARIANT", str(v))
+        with jb.Plan(A) as p:
+            r = p.solve(b, None, 12, 0.0, history=True)
+            c = p.solve(b, None, 500, 1e-11)
+            if n == 8190 and v in (6, 7):
+                for nb in (2, 3, 5):  # P12a through the CTA kernel, ragged rows per CTA
+                    p.set_row_blocks(nb)
+                    rb = p.solve(b, None, 12, 0.0, history=True)
+                    assert np.array_equal(rb.x, r.x) and np.array_equal(rb.hist, r.hist), (v, nb)
+                p.set_row_blocks(1)
+        assert rel_linf(r.x, x_o) <= TOL64
+        if ref is None:
+            ref = (r, c)
+        assert np.array_equal(r.x, ref[0].x) and np.array_equal(r.hist, ref[0].hist), v
+        assert (c.status, c.iters) == (ref[1].status, ref[1].iters) and np.array_equal(c.x, ref[1].x), v
