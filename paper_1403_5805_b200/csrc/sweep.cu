@@ -431,12 +431,12 @@ size_t variant_smem(int v, int nchunks) { return kVariants[v].cta ? (size_t)kSlo
 bool variant_fits(int v, int nchunks) {
   return !kVariants[v].cta || (nchunks >= kVariants[v].threads / 32 && variant_smem(v, nchunks) <= 48 * 1024);
 }
-// Defaults from B200 measurements (profiles/variants_r01_*.jsonl): the CTA-cooperative kernel when
-// n has at least 16 chunks, else the item kernel (fp64 R=8,U=1; fp32 R=4,U=1).
+// Defaults from B200 measurements (profiles/variants*_r01_*.jsonl): fp64 uses the CTA-cooperative
+// kernel (R=4) when n has at least 16 chunks (c4: 7180 GB/s), else the item kernel R=8,U=1; fp32 uses
+// the item kernel R=4,U=1 (c5: 6830 GB/s).
 int default_variant(int dtype, int nchunks) {
-  const int big = dtype == JACOBI_F32 ? 7 : 6;
-  if (variant_fits(big, nchunks)) return big;
-  return dtype == JACOBI_F32 ? 0 : 1;
+  if (dtype == JACOBI_F32) return 0;
+  return variant_fits(7, nchunks) ? 7 : 1;
 }
 int variant_rows(int v) { return kVariants[v].R; }
 int variant_threads(int v) { return kVariants[v].threads; }
