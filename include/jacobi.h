@@ -103,6 +103,8 @@ typedef struct {
   int a_borrowed;               /* 1 if the caller's device A is used in place                 */
   int64_t sweeps_launched;      /* sweep kernels launched by the last solve (incl. no-ops)     */
   double bytes_per_sweep;       /* algorithmic HBM bytes per sweep: rows*n*s_A + 8n + 16*rows  */
+  int variant;                  /* sweep kernel variant in use (JACOBI_SWEEP_VARIANT overrides)  */
+  int num_variants;             /* variants compiled in (all give bitwise-identical results)    */
 } jacobi_plan_info_t;
 int jacobi_plan_info(const jacobi_plan* plan, jacobi_plan_info_t* info);
 

@@ -43,7 +43,8 @@ class PlanInfo(ctypes.Structure):
                 ("row0", ctypes.c_int64), ("dtype", ctypes.c_int), ("rank", ctypes.c_int),
                 ("nranks", ctypes.c_int), ("chunk_cols", ctypes.c_int), ("rows_per_warp", ctypes.c_int),
                 ("grid_ctas", ctypes.c_int), ("threads_per_cta", ctypes.c_int), ("a_borrowed", ctypes.c_int),
-                ("sweeps_launched", ctypes.c_int64), ("bytes_per_sweep", ctypes.c_double)]
+                ("sweeps_launched", ctypes.c_int64), ("bytes_per_sweep", ctypes.c_double),
+                ("variant", ctypes.c_int), ("num_variants", ctypes.c_int)]
 
 
 def _load():

@@ -51,12 +51,13 @@ cudaError_t launch_scan_nonfinite_vec(const double* v, int64_t len, int* flag, c
 cudaError_t launch_copy_pitched(int dtype, const void* src, int64_t src_ld, void* dst, int64_t dst_ld,
                                 int64_t rows, int64_t n, cudaStream_t s);
 int num_variants();
-int default_variant(int dtype, int nchunks);
+int default_variant(int dtype, int nchunks, int chunk);
 bool variant_is_cta(int variant);
-bool variant_fits(int variant, int nchunks);
+bool variant_fits(int variant, int nchunks, int dtype, int chunk);
+int variant_rows_dt(int variant, int dtype);
 int variant_rows(int variant);
 int variant_threads(int variant);
-int sweep_grid(int dtype, int variant, int num_sms);
+int sweep_grid(int dtype, int variant, int num_sms, int nchunks, int chunk);
 int chunk_for(int64_t n);
 double bwprobe(int64_t nbytes, int reps);
 

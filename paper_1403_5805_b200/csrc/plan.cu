@@ -88,12 +88,12 @@ int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dty
   }
   p->chunk = jacobi::chunk_for(n);
   const int nch = (int)((n + p->chunk - 1) / p->chunk);
-  p->variant = jacobi::default_variant(dtype, nch);
+  p->variant = jacobi::default_variant(dtype, nch, p->chunk);
   if (const char* v = getenv("JACOBI_SWEEP_VARIANT")) {  // tuning override (all variants: same bits)
     int vi = atoi(v);
-    if (vi >= 0 && vi < jacobi::num_variants() && jacobi::variant_fits(vi, nch)) p->variant = vi;
+    if (vi >= 0 && vi < jacobi::num_variants() && jacobi::variant_fits(vi, nch, dtype, p->chunk)) p->variant = vi;
   }
-  p->grid = jacobi::sweep_grid(dtype, p->variant, p->num_sms);
+  p->grid = jacobi::sweep_grid(dtype, p->variant, p->num_sms, nch, p->chunk);
   p->x_len = round_up(n, 256) + 256;
   const int64_t nchunks = (n + p->chunk - 1) / p->chunk;
   JCUDA(cudaMalloc(&p->diag, (size_t)m * 8));
@@ -186,13 +186,15 @@ extern "C" int jacobi_plan_info(const jacobi_plan* p, jacobi_plan_info_t* info) 
   info->rank = p->rank;
   info->nranks = p->nranks;
   info->chunk_cols = p->chunk;
-  info->rows_per_warp = jacobi::variant_rows(p->variant);
+  info->rows_per_warp = jacobi::variant_rows_dt(p->variant, p->dtype);
   info->grid_ctas = p->grid;
   info->threads_per_cta = jacobi::variant_threads(p->variant);
   info->a_borrowed = p->a_borrowed ? 1 : 0;
   info->sweeps_launched = p->sweeps_launched;
   const double sA = p->dtype == JACOBI_F32 ? 4.0 : 8.0;
   info->bytes_per_sweep = (double)p->m * (double)p->n * sA + 8.0 * (double)p->n + 16.0 * (double)p->m;
+  info->variant = p->variant;
+  info->num_variants = jacobi::num_variants();
   return 0;
 }
 
@@ -215,7 +217,7 @@ static jacobi::SweepArgs sweep_args(const jacobi_plan* p, int blk) {
   a.st = p->st;
   a.chunk = p->chunk;
   a.nchunks = (int)((p->n + p->chunk - 1) / p->chunk);
-  const int R = jacobi::variant_rows(p->variant);
+  const int R = jacobi::variant_rows_dt(p->variant, p->dtype);
   a.tiles = (int)((mb + R - 1) / R);
   return a;
 }

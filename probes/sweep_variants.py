@@ -16,7 +16,7 @@ import paper_1403_5805_b200 as jb  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c4"
 sweeps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
-variants = [int(v) for v in sys.argv[3].split(",")] if len(sys.argv) > 3 else list(range(9))
+variants = [int(v) for v in sys.argv[3].split(",")] if len(sys.argv) > 3 else list(range(11))
 cfg = g.CONFIGS[name]
 n = cfg.n
 dt = torch.float32 if cfg.a_dtype == g.F32 else torch.float64
@@ -40,6 +40,6 @@ for v in variants:
         if ref is None:
             ref = x
         med = float(np.median(ms[1:]))
-        print(json.dumps({"workload": name, "variant": v, "R": inf.rows_per_warp, "threads": inf.threads_per_cta,
+        print(json.dumps({"workload": name, "variant": inf.variant, "requested": v, "R": inf.rows_per_warp, "threads": inf.threads_per_cta,
                           "grid": inf.grid_ctas, "chunk": inf.chunk_cols, "lda": inf.lda, "median_ms": med, "min_ms": float(ms[1:].min()),
                           "gbs": inf.bytes_per_sweep / (med * 1e-3) / 1e9, "bitwise_equal_v0": same}), flush=True)
