@@ -58,7 +58,7 @@ int variant_rows_dt(int variant, int dtype);
 int variant_rows(int variant);
 int variant_threads(int variant);
 int sweep_grid(int dtype, int variant, int num_sms, int nchunks, int chunk);
-int chunk_for(int64_t n);
+int chunk_for(int64_t n, int dtype);
 double bwprobe(int64_t nbytes, int reps);
 
 }  // namespace jacobi

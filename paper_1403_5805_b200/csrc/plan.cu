@@ -86,7 +86,7 @@ int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dty
                               (size_t)m, cudaMemcpyHostToDevice, p->stream));
     }
   }
-  p->chunk = jacobi::chunk_for(n);
+  p->chunk = jacobi::chunk_for(n, dtype);
   const int nch = (int)((n + p->chunk - 1) / p->chunk);
   p->variant = jacobi::default_variant(dtype, nch, p->chunk);
   if (const char* v = getenv("JACOBI_SWEEP_VARIANT")) {  // tuning override (all variants: same bits)

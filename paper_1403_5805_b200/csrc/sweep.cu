@@ -323,167 +323,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
   if (lane == 0) atomicMax(&a.dslot[k & 3], dmax);
 }
 
-// ---------------------------------------------------------------------------------------------
-// k_sweep_tma: A streamed by the bulk-copy engine (cp.async.bulk, TMA 1D) into a ring of shared-
-// memory stages.  CTA b owns rows [b*m/G, (b+1)*m/G); its units are (chunk c, tile of R rows) in
-// chunk-major order (x^(k-1)[chunk] stays hot in L1).  One producer thread issues R row-segment
-// copies per unit (mbarrier complete_tx); NC consumer warps take units round-robin and run exactly
-// accumulate_chunk's per-lane order from shared memory (two LDS.128 per 32-byte lane slice, half-
-// swapped by lane so a quarter-warp touches all 32 banks once).  Chunk partials go to part[c*m+row];
-// after the last unit the CTA adds them in ascending chunk order and applies the fused epilogue.
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)),
-               "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   (unsigned)__cvta_generic_to_shared(dst)),
-               "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
-               : "memory");
-}
-
-// 32 bytes of row data for lane `lane` from shared memory: two conflict-free LDS.128.
-__device__ __forceinline__ void lds32(const unsigned char* p, int lane, double (&v)[4]) {
-  const int h = (lane >> 2) & 1;
-  const double2 a = *reinterpret_cast<const double2*>(p + 16 * h);
-  const double2 b = *reinterpret_cast<const double2*>(p + 16 * (1 - h));
-  v[0] = h ? b.x : a.x; v[1] = h ? b.y : a.y; v[2] = h ? a.x : b.x; v[3] = h ? a.y : b.y;
-}
-__device__ __forceinline__ void lds32(const unsigned char* p, int lane, float (&v)[8]) {
-  const int h = (lane >> 2) & 1;
-  const float4 a = *reinterpret_cast<const float4*>(p + 16 * h);
-  const float4 b = *reinterpret_cast<const float4*>(p + 16 * (1 - h));
-  const float4 lo = h ? b : a, hi = h ? a : b;
-  v[0] = lo.x; v[1] = lo.y; v[2] = lo.z; v[3] = lo.w; v[4] = hi.x; v[5] = hi.y; v[6] = hi.z; v[7] = hi.w;
-}
-
-template <typename T, int R, int NC, int ST>
-__global__ void __launch_bounds__((NC + 1) * 32, 1) k_sweep_tma(const SweepArgs a, const int j) {
-  constexpr int E = VecOf<T>::E;
-  extern __shared__ __align__(128) unsigned char s_stage[];  // [ST][R][chunk] of T
-  __shared__ __align__(8) uint64_t s_full[ST], s_empty[ST];
-  __shared__ int s_go;
-  if (threadIdx.x == 0) {
-    s_go = sweep_prologue(a, j, blockIdx.x == 0);
-    for (int q = 0; q < ST; ++q) {
-      mbar_init(&s_full[q], 1);
-      mbar_init(&s_empty[q], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (!s_go) return;
-
-  const int64_t k = a.st->kbase + j + 1;
-  const double* __restrict__ xo = (k & 1) ? a.x0buf : a.x1buf;  // x^(k-1)
-  double* __restrict__ xn = (k & 1) ? a.x1buf : a.x0buf;        // x^(k)
-  const T* __restrict__ A = static_cast<const T*>(a.A);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int nch = a.nchunks, C = a.chunk;
-  const int64_t rb = (int64_t)blockIdx.x * a.m / gridDim.x;
-  const int64_t re = (int64_t)(blockIdx.x + 1) * a.m / gridDim.x;
-  const int ntile = (int)((re - rb + R - 1) / R);
-  const int64_t units = (int64_t)nch * ntile;
-  const size_t row_bytes = (size_t)C * sizeof(T);
-  const size_t stage_bytes = row_bytes * R;
-
-  if (w == NC) {  // producer
-    if (lane == 0) {
-      for (int64_t u = 0; u < units; ++u) {
-        const int q = (int)(u % ST);
-        if (u >= ST) mbar_wait(&s_empty[q], (unsigned)(((u / ST) - 1) & 1));
-        const int c = (int)(u / ntile), t = (int)(u % ntile);
-        const int64_t r0 = rb + (int64_t)t * R;
-        const int nv = (int)min((int64_t)R, re - r0);
-        const int64_t c0 = (int64_t)c * C;
-        const int64_t clen = min((int64_t)C, a.n - c0);
-        const unsigned bytes = (unsigned)(((clen + 7) / 8) * 8 * sizeof(T));  // lda >= round_up(n, 8)
-        mbar_arrive_tx(&s_full[q], bytes * nv);
-        unsigned char* st = s_stage + q * stage_bytes;
-        for (int r = 0; r < nv; ++r) bulk_g2s(st + r * row_bytes, A + (r0 + r) * a.lda + c0, bytes, &s_full[q]);
-      }
-    }
-  } else {  // consumers
-    constexpr int S = 32 * E;
-    const int nsteps = C / S;
-    for (int64_t u = w; u < units; u += NC) {
-      const int q = (int)(u % ST);
-      mbar_wait(&s_full[q], (unsigned)((u / ST) & 1));
-      const int c = (int)(u / ntile), t = (int)(u % ntile);
-      const int64_t r0 = rb + (int64_t)t * R;
-      const int nv = (int)min((int64_t)R, re - r0);
-      const int64_t c0 = (int64_t)c * C;
-      const int64_t c1 = min(c0 + (int64_t)C, a.n);
-      const int64_t g0 = a.row0 + r0;
-      const unsigned char* st = s_stage + q * stage_bytes;
-      double acc[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) acc[r] = 0.0;
-      const bool masked = (c1 - c0 != C) || (g0 < c1 && g0 + R > c0);
-      for (int s = 0; s < nsteps; ++s) {
-        const int cr = (s * 32 + lane) * E;  // column relative to c0
-        if (!masked || c0 + cr < a.n) {
-          double xv[E];
-          ld_x<E>(xo + c0 + cr, xv);
-          T av[R][E];
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            if (r < nv) lds32(st + r * row_bytes + cr * sizeof(T), lane, av[r]);
-            else {
-#pragma unroll
-              for (int e = 0; e < E; ++e) av[r][e] = T(0);
-            }
-          }
-          if (!masked) {
-#pragma unroll
-            for (int r = 0; r < R; ++r)
-#pragma unroll
-              for (int e = 0; e < E; ++e) acc[r] = __fma_rn((double)av[r][e], xv[e], acc[r]);
-          } else {
-#pragma unroll
-            for (int r = 0; r < R; ++r)
-#pragma unroll
-              for (int e = 0; e < E; ++e) {
-                const int64_t cc = c0 + cr + e;
-                if (cc < a.n && cc != g0 + r) acc[r] = __fma_rn((double)av[r][e], xv[e], acc[r]);
-              }
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[q]);
-#pragma unroll
-      for (int r = 0; r < R; ++r)
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) acc[r] += __shfl_xor_sync(kFull, acc[r], off);
-      if (lane < nv) {
-        double mine = acc[0];
-#pragma unroll
-        for (int r = 1; r < R; ++r)
-          if (lane == r) mine = acc[r];
-        a.part[(int64_t)c * a.m + r0 + lane] = mine;
-      }
-    }
-  }
-  __syncthreads();  // every chunk partial of the CTA's rows is written
-  unsigned long long dmax = 0ull;
-  for (int64_t row = rb + threadIdx.x; row < re; row += blockDim.x) {
-    double s = __ldcg(a.part + row);
-    for (int c = 1; c < nch; ++c) s += __ldcg(a.part + (int64_t)c * a.m + row);
-    const double xnew = __ddiv_rn(__dsub_rn(a.b[row], s), a.diag[row]);
-    const int64_t gi = a.row0 + row;
-    xn[gi] = xnew;
-    const unsigned long long bits =
-        (unsigned long long)__double_as_longlong(__dsub_rn(xnew, xo[gi])) & 0x7fffffffffffffffull;
-    dmax = bits > dmax ? bits : dmax;
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    const unsigned long long o = __shfl_xor_sync(kFull, dmax, off);
-    dmax = o > dmax ? o : dmax;
-  }
-  if (lane == 0) atomicMax(&a.dslot[k & 3], dmax);
-}
 
 // After a graph batch of K sweeps: settle the stop decision for the batch's last sweep (same rule
 // as the prologue) and advance the sweep counter.
@@ -568,7 +407,7 @@ __global__ void k_fill(double* buf, int64_t n) {
 // produce identical bits (the summation order does not depend on R, U or the grid); the default is
 // chosen from measurements (profiles/), others stay selectable with JACOBI_SWEEP_VARIANT for tuning.
 struct Variant {
-  int R, threads, cta;  // cta = 1: k_sweep_cta (needs nchunks >= threads/32); 2: k_sweep_tma
+  int R, threads, cta;  // cta = 1: k_sweep_cta (needs nchunks >= threads/32 and its partial slots)
   void (*f64)(const SweepArgs, const int);
   void (*f32)(const SweepArgs, const int);
 };
@@ -582,8 +421,6 @@ const Variant kVariants[] = {
     {8, 512, 1, k_sweep_cta<double, 8, 16>, k_sweep_cta<float, 8, 16>},
     {4, 512, 1, k_sweep_cta<double, 4, 16>, k_sweep_cta<float, 4, 16>},
     {8, 256, 1, k_sweep_cta<double, 8, 8>, k_sweep_cta<float, 4, 8>},
-    {4, 160, 2, k_sweep_tma<double, 4, 4, 6>, k_sweep_tma<float, 8, 4, 6>},
-    {8, 288, 2, k_sweep_tma<double, 8, 8, 3>, k_sweep_tma<float, 8, 8, 6>},
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
@@ -591,39 +428,33 @@ constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 int num_variants() { return kNumVariants; }
 bool variant_is_cta(int v) { return kVariants[v].cta != 0; }
-// Shared memory of a variant: CTA kernel = partial slots; TMA kernel = stage ring (chunk known per plan).
-size_t variant_smem(int v, int nchunks, int dtype, int chunk) {
+// Shared memory of a variant: the CTA kernel's partial slots.
+size_t variant_smem(int v, int nchunks, int /*dtype*/, int /*chunk*/) {
   const Variant& V = kVariants[v];
-  if (V.cta == 1) return (size_t)kSlots * nchunks * V.R * 8;
-  if (V.cta == 2) {
-    const int st = v == 9 ? 6 : (dtype == JACOBI_F32 ? 6 : 3);
-    const int R = dtype == JACOBI_F32 ? 8 : V.R;
-    return (size_t)st * R * chunk * (dtype == JACOBI_F32 ? 4 : 8);
-  }
-  return 0;
+  return V.cta ? (size_t)kSlots * nchunks * V.R * 8 : 0;
 }
 bool variant_fits(int v, int nchunks, int dtype, int chunk) {
   const Variant& V = kVariants[v];
-  if (V.cta == 1) return nchunks >= V.threads / 32 && variant_smem(v, nchunks, dtype, chunk) <= 48 * 1024;
-  if (V.cta == 2) return variant_smem(v, nchunks, dtype, chunk) <= 200 * 1024;
-  return true;
+  return !V.cta || (nchunks >= V.threads / 32 && variant_smem(v, nchunks, dtype, chunk) <= 48 * 1024);
 }
-int variant_rows_dt(int v, int dtype) {
-  return (kVariants[v].cta == 2 && dtype == JACOBI_F32) ? 8 : kVariants[v].R;
-}
+int variant_rows_dt(int v, int /*dtype*/) { return kVariants[v].R; }
 // Defaults from B200 measurements (profiles/variants*_r01_*.jsonl): fp64 uses the CTA-cooperative
 // kernel (R=4) when n has at least 16 chunks (c4: 7180 GB/s), else the item kernel R=8,U=1; fp32 uses
 // the item kernel R=4,U=1 (c5: 6830 GB/s).
 int default_variant(int dtype, int nchunks, int chunk) {
-  if (dtype == JACOBI_F32) return 0;
-  return variant_fits(7, nchunks, dtype, chunk) ? 7 : 1;
+  if (variant_fits(7, nchunks, dtype, chunk)) return 7;
+  return dtype == JACOBI_F32 ? 0 : 1;
 }
 int variant_rows(int v) { return kVariants[v].R; }
 int variant_threads(int v) { return kVariants[v].threads; }
 
-int chunk_for(int64_t n) {
-  // 1024 columns (8 KB of an fp64 row) from n = 16384 up, 512 below; a function of n only.
-  return n >= 16384 ? 1024 : 512;
+int chunk_for(int64_t n, int dtype) {
+  // 8 KB of row data per chunk (1024 fp64 / 2048 fp32 columns) when n has >= 16 such chunks, halved
+  // down to 512 columns otherwise.  A function of (n, dtype) only, so every rank count and every
+  // kernel variant sums each row in the same order.
+  int c = dtype == JACOBI_F32 ? 2048 : 1024;
+  while (c > 512 && (int64_t)c * 16 > n) c /= 2;
+  return c;
 }
 
 int sweep_grid(int dtype, int v, int num_sms, int nchunks, int chunk) {
@@ -631,7 +462,6 @@ int sweep_grid(int dtype, int v, int num_sms, int nchunks, int chunk) {
   const Variant& V = kVariants[v];
   const size_t smem = variant_smem(v, nchunks, dtype, chunk);
   auto fn = dtype == JACOBI_F32 ? V.f32 : V.f64;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, V.threads, smem);
   if (e != cudaSuccess || per_sm < 1) per_sm = 1;
   return num_sms * per_sm;

@@ -292,20 +292,20 @@ def test_full_size_sampled_parity(jb, name):
 
 
 # ------------------------------------------------------------------ kernel variants (same bits by design)
-@pytest.mark.parametrize("n", [3000, 8190, 16384])
-def test_all_sweep_variants_bitwise_identical(jb, n, monkeypatch):
+@pytest.mark.parametrize("n,f32", [(3000, False), (8190, False), (16384, False), (16384, True)])
+def test_all_sweep_variants_bitwise_identical(jb, n, f32, monkeypatch):
     """Every sweep-kernel variant (item kernel with R in {2,4,8}, CTA-cooperative kernel) must give
     identical bits: the per-row summation order depends only on column indices (R10)."""
-    A, b, _ = dominant(n, 31 + n, scale=1.05)
+    A, b, _ = dominant(n, 31 + n, scale=1.05, f32=f32)
     st_o, x_o, it_o, h_o = oracle.jacobi(A, b, None, 12, 0.0, nthreads=16, history=True)
     ref = None
-    for v in range(11):
+    for v in range(9):
         monkeypatch.setenv("JACOBI_SWEEP_VARIANT", str(v))
         with jb.Plan(A) as p:
-            assert p.info.num_variants == 11
+            assert p.info.num_variants == 9
             r = p.solve(b, None, 12, 0.0, history=True)
             c = p.solve(b, None, 500, 1e-11)
-            if n == 8190 and v in (6, 7, 9, 10):
+            if n == 8190 and v in (6, 7):
                 for nb in (2, 3, 5):  # P12a through the CTA kernel, ragged rows per CTA
                     p.set_row_blocks(nb)
                     rb = p.solve(b, None, 12, 0.0, history=True)
