@@ -236,7 +236,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
 
 constexpr int kSlots = 4;
 
-template <typename T, int R, int NW>
+template <typename T, int R, int NW, int U = 1>
 __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, const int j) {
   extern __shared__ __align__(16) double s_part[];  // [kSlots][nchunks][R]
   __shared__ __align__(8) uint64_t s_full[kSlots], s_empty[kSlots];
@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
       for (int r = 0; r < R; ++r) acc[r] = 0.0;
       const int64_t c0 = (int64_t)c * a.chunk;
       const int64_t c1 = min(c0 + (int64_t)a.chunk, a.n);
-      accumulate_chunk<T, R, 1>(rowp, nv, xo, c0, c1, a.chunk, a.n, g0, lane, acc);
+      accumulate_chunk<T, R, U>(rowp, nv, xo, c0, c1, a.chunk, a.n, g0, lane, acc);
 #pragma unroll
       for (int r = 0; r < R; ++r)
 #pragma unroll
@@ -421,6 +421,8 @@ const Variant kVariants[] = {
     {8, 512, 1, k_sweep_cta<double, 8, 16>, k_sweep_cta<float, 8, 16>},
     {4, 512, 1, k_sweep_cta<double, 4, 16>, k_sweep_cta<float, 4, 16>},
     {8, 256, 1, k_sweep_cta<double, 8, 8>, k_sweep_cta<float, 4, 8>},
+    {4, 512, 1, k_sweep_cta<double, 4, 16, 2>, k_sweep_cta<float, 4, 16, 2>},
+    {2, 512, 1, k_sweep_cta<double, 2, 16, 4>, k_sweep_cta<float, 2, 16, 2>},
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
