@@ -36,6 +36,10 @@ def _load():
         lib.oracle_jacobi.restype = ctypes.c_int
         lib.oracle_sweep_rows.argtypes = [i64, ctypes.c_int, vp, i64, i64, i64, dp, dp, dp]
         lib.oracle_sweep_rows.restype = None
+        lib.oracle_jacobi_norm.argtypes = lib.oracle_jacobi.argtypes + [ctypes.c_int]
+        lib.oracle_jacobi_norm.restype = ctypes.c_int
+        lib.oracle_l2_dist.argtypes = [i64, dp, dp]
+        lib.oracle_l2_dist.restype = ctypes.c_double
         lib.oracle_maxnorm_dist.argtypes = [i64, dp, dp]
         lib.oracle_maxnorm_dist.restype = ctypes.c_double
         lib.oracle_ge_solve.argtypes = [i64, dp, dp, dp]
@@ -55,9 +59,10 @@ def _f64vec(v, n, name):
     return v
 
 
-def jacobi(A, b, x0=None, max_iter=100, tol=0.0, nthreads=1, history=False):
-    """PAPER.md:59-66 with the max-norm distance.  A: (n, n) float64 or float32 (fp32 values are
-    widened exactly).  Returns (status, x, iters[, hist]); x is None when status < 0."""
+def jacobi(A, b, x0=None, max_iter=100, tol=0.0, nthreads=1, history=False, norm="max"):
+    """PAPER.md:59-66 with the max-norm distance (norm="max", north_star) or the paper's Euclidean
+    distance of PAPER.md:94 (norm="l2").  A: (n, n) float64 or float32 (fp32 values are widened
+    exactly).  Returns (status, x, iters[, hist]); x is None when status < 0."""
     A = np.asarray(A)
     if A.ndim != 2 or A.shape[0] != A.shape[1]:
         raise ValueError("A must be square")
@@ -69,8 +74,9 @@ def jacobi(A, b, x0=None, max_iter=100, tol=0.0, nthreads=1, history=False):
     x = np.empty(n)
     it = ctypes.c_int64(-1)
     hist = np.full(max(int(max_iter), 1), np.nan) if history else None
-    st = _load().oracle_jacobi(n, a_f32, A.ctypes.data, n, _dp(b), _dp(x0), int(max_iter), float(tol),
-                               _dp(x), ctypes.byref(it), _dp(hist) if history else None, int(nthreads))
+    st = _load().oracle_jacobi_norm(n, a_f32, A.ctypes.data, n, _dp(b), _dp(x0), int(max_iter), float(tol),
+                                    _dp(x), ctypes.byref(it), _dp(hist) if history else None, int(nthreads),
+                                    {"max": 0, "l2": 1}[norm])
     out = (st, x if st >= 0 else None, it.value if st >= 0 else None)
     if history:
         out = out + ((hist[: it.value] if st >= 0 else None),)
@@ -95,6 +101,12 @@ def maxnorm_dist(u, v):
     u = np.ascontiguousarray(u, dtype=np.float64)
     v = np.ascontiguousarray(v, dtype=np.float64)
     return _load().oracle_maxnorm_dist(u.shape[0], _dp(u), _dp(v))
+
+
+def l2_dist(u, v):
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    return _load().oracle_l2_dist(u.shape[0], _dp(u), _dp(v))
 
 
 def ge_solve(A, b):

@@ -15,7 +15,9 @@
  *     the iteration limit has been reached" -> return X^(L).
  *   - The distance is the max norm max_i |x_i^(k) - x_i^(k-1)| (BASELINE.json north_star and
  *     configs; PAPER.md:51/94 say Euclidean — reading R1), NaN-sticky (reading R12), compared
- *     with strict "<" (R2), checked after every sweep including the first (R3).
+ *     with strict "<" (R2), checked after every sweep including the first (R3).  The paper's own
+ *     Euclidean distance sqrt(sum_i (x_i^(k+1) - x_i^(k))^2) of PAPER.md:94 is the norm = 1 option
+ *     of oracle_jacobi_norm (NEXT-2 row), summed in ascending i.
  *   - PAPER.md:53: "the algorithm will fail if a_ii = 0" -> status EZERODIAG with the lowest i.
  *   - Gaussian elimination with partial pivoting (oracle_ge_solve): the textbook direct solve used
  *     only to pin the converged Jacobi value (north_star: "checked on tiny systems against a direct
@@ -63,6 +65,17 @@ void oracle_sweep_rows(int64_t n, int a_f32, const void* A_rows, int64_t lda, in
   }
 }
 
+/* Euclidean distance of PAPER.md:94 (§3.1): sqrt( sum_i (u_i - v_i)^2 ), ascending i (NEXT-2 row). */
+double oracle_l2_dist(int64_t n, const double* u, const double* v) {
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double t = u[i] - v[i];
+    double t2 = t * t;
+    s = s + t2;
+  }
+  return sqrt(s);
+}
+
 /* max_i |u_i - v_i|, NaN-sticky: once a NaN difference is seen the result is NaN (R12). */
 double oracle_maxnorm_dist(int64_t n, const double* u, const double* v) {
   double d = 0.0;
@@ -107,10 +120,11 @@ static int all_finite(int64_t cnt, const double* v) {
  * hist (nullable, length >= max_iter) receives d_k for k = 1..iters.
  * Validation order: EINVAL, then EZERODIAG (lowest i), then ENONFINITE.
  * x_out / iters_out are written only when the status is >= 0; x_out may alias x0. */
-int oracle_jacobi(int64_t n, int a_f32, const void* A, int64_t lda, const double* b, const double* x0,
-                  int64_t max_iter, double tol, double* x_out, int64_t* iters_out, double* hist,
-                  int nthreads) {
-  if (n < 1 || !A || !b || !x0 || !x_out || !iters_out || lda < n || max_iter < 0 || isnan(tol) || tol < 0)
+int oracle_jacobi_norm(int64_t n, int a_f32, const void* A, int64_t lda, const double* b, const double* x0,
+                       int64_t max_iter, double tol, double* x_out, int64_t* iters_out, double* hist,
+                       int nthreads, int norm) {
+  if (n < 1 || !A || !b || !x0 || !x_out || !iters_out || lda < n || max_iter < 0 || isnan(tol) || tol < 0 ||
+      (norm != 0 && norm != 1))
     return OR_EINVAL;
   for (int64_t i = 0; i < n; ++i)
     if (a_at(A, a_f32, lda, i, i) == 0.0) return OR_EZERODIAG;
@@ -148,7 +162,8 @@ int oracle_jacobi(int64_t n, int a_f32, const void* A, int64_t lda, const double
     xo_ptr = xt; xn_ptr = x;
     if (nthreads > 1) { pthread_barrier_wait(&bar); pthread_barrier_wait(&bar); }
     else oracle_sweep_rows(n, a_f32, A, lda, 0, n, b, xt, x); /* (a) */
-    double d = oracle_maxnorm_dist(n, x, xt);                  /* (b) ||X - X^t|| (max norm) */
+    double d = norm ? oracle_l2_dist(n, x, xt)                 /* (b) ||X - X^t||: Euclidean */
+                    : oracle_maxnorm_dist(n, x, xt);           /*     or max norm (north_star, R1) */
     if (hist) hist[k - 1] = d;
     if (d < tol) { status = OR_CONVERGED; break; }             /*     < tol: return X */
     k = k + 1;                                                 /* (c) */
@@ -169,6 +184,12 @@ int oracle_jacobi(int64_t n, int a_f32, const void* A, int64_t lda, const double
   *iters_out = iters;
   free(xt); free(x);
   return status;
+}
+
+/* Max-norm entry point (the north star's stop rule). */
+int oracle_jacobi(int64_t n, int a_f32, const void* A, int64_t lda, const double* b, const double* x0,
+                  int64_t max_iter, double tol, double* x_out, int64_t* iters_out, double* hist, int nthreads) {
+  return oracle_jacobi_norm(n, a_f32, A, lda, b, x0, max_iter, tol, x_out, iters_out, hist, nthreads, 0);
 }
 
 /* Gaussian elimination with partial pivoting on a copy of A (fp64, row-major, lda = n).

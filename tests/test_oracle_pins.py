@@ -293,3 +293,33 @@ def test_fp32_storage_widens_exactly():
     r32 = oracle.jacobi(A32, b, None, 12, 0.0, history=True)
     r64 = oracle.jacobi(A32.astype(np.float64), b, None, 12, 0.0, history=True)
     assert np.array_equal(r32[1], r64[1]) and np.array_equal(r32[3], r64[3])
+
+
+# ---------------------------------------------------------------- NEXT-2: the paper's Euclidean stop rule
+def test_l2_distance_pins():
+    """PAPER.md:94: ||X^(k+1) - X^(k)|| = sqrt(sum_i (X_i^(k+1) - X_i^(k))^2)."""
+    assert oracle.l2_dist([3.0, 0.0], [0.0, 4.0]) == 5.0  # SPEC.md:79 (3-4-5)
+    assert oracle.l2_dist([1.0, 1, 1, 1], [0.0, 0, 0, 0]) == 2.0  # SPEC.md:80
+    assert oracle.l2_dist([1.0, 2, 3], [1.0, 2, 3]) == 0.0
+    # 2x2 closed form (P1): d_2m = 5 * 6^-m (a 3-4-5 triangle scaled by 6^-m), d_2m+1 = sqrt(145)/6 * 6^-m
+    A = np.array([[2.0, 1.0], [1.0, 3.0]])
+    b = np.array([3.0, 4.0])
+    st, x, it, h = oracle.jacobi(A, b, None, 1000, 1e-12, history=True, norm="l2")
+    for k in range(1, it + 1):
+        m = k // 2
+        ref = 5 * 6.0 ** -m if k % 2 == 0 else math.sqrt(145) / 6 * 6.0 ** -m
+        assert h[k - 1] == pytest.approx(ref, rel=1e-9)
+    assert (st, it) == (oracle.CONVERGED, 33) and h[31] >= 1e-12 > h[32]  # d_32 = 5*6^-16 = 1.77e-12
+    # exact-rational iterates (P2 golden) with the Euclidean distance
+    A3, b3, rows = _read_golden_p2()
+    for k, xs, d in rows:
+        st, x, it, h = oracle.jacobi(A3, b3, None, k, 0.0, history=True, norm="l2")
+        prev = [Fraction(0)] * 3 if k == 1 else rows[k - 2][1]
+        ref = math.sqrt(float(sum((xs[i] - prev[i]) ** 2 for i in range(3))))
+        assert h[-1] == pytest.approx(ref, rel=1e-14)
+    # L2 >= max norm, so with the same tol the L2 rule never stops earlier
+    rng = np.random.default_rng(21)
+    A, b, _ = dominant_system(40, rng, margin=(0.05, 0.3))
+    r_max = oracle.jacobi(A, b, None, 5000, 1e-10)
+    r_l2 = oracle.jacobi(A, b, None, 5000, 1e-10, norm="l2")
+    assert r_l2[2] >= r_max[2]
