@@ -61,6 +61,10 @@ enum {
 };
 
 enum { JACOBI_F64 = 0, JACOBI_F32 = 1 };
+/* Distance of the stop test: the north star's max norm (default) or the paper's Euclidean norm
+ * sqrt(sum_i (x_i^(k) - x_i^(k-1))^2) of PAPER.md:94 (summed in a fixed order: trees over blocks of
+ * 256 rows, then the block sums; bitwise independent of the rank count when 256 divides n/P). */
+enum { JACOBI_NORM_MAX = 0, JACOBI_NORM_L2 = 1 };
 
 typedef struct jacobi_plan jacobi_plan;
 
@@ -90,6 +94,8 @@ void jacobi_plan_destroy(jacobi_plan* plan);
 /* Test hook for SURVEY.md pin P12(a): run each sweep of a single-GPU plan as `nblocks` row-block
  * launches (nblocks must divide the plan's rows).  Results must be bitwise identical to 1. */
 int jacobi_plan_set_row_blocks(jacobi_plan* plan, int nblocks);
+/* Select the stop-test norm (JACOBI_NORM_MAX or JACOBI_NORM_L2) for subsequent solves. */
+int jacobi_plan_set_norm(jacobi_plan* plan, int norm);
 /* Sweeps per captured CUDA graph batch (multiple of 4, 4..1024; default 32).  The stop state is
  * polled on the host once per batch; sweeps after the stop decision are no-op launches. */
 int jacobi_plan_set_batch(jacobi_plan* plan, int sweeps_per_batch);

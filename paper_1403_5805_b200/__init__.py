@@ -21,13 +21,14 @@ LIB_PATH = os.path.join(_HERE, "libjacobi.so")
 CONVERGED, MAX_ITER = 0, 1
 EINVAL, EZERODIAG, ENONFINITE, ENOMEM, ECUDA, ENCCL, EINDIVISIBLE = -1, -2, -3, -4, -5, -6, -7
 F64, F32 = 0, 1
+NORM_MAX, NORM_L2 = 0, 1
 STATUS_NAMES = {0: "CONVERGED", 1: "MAX_ITER", -1: "EINVAL", -2: "EZERODIAG", -3: "ENONFINITE",
                 -4: "ENOMEM", -5: "ECUDA", -6: "ENCCL", -7: "EINDIVISIBLE"}
 
 # Every symbol include/jacobi.h declares (checked by tests/test_capi.py).
 EXPORTS = ("jacobi_solve", "jacobi_solve_f32a", "jacobi_plan_create", "jacobi_plan_solve",
            "jacobi_plan_solve_device", "jacobi_plan_destroy", "jacobi_plan_set_row_blocks",
-           "jacobi_plan_set_batch", "jacobi_plan_info", "jacobi_plan_time_sweeps", "jacobi_partition",
+           "jacobi_plan_set_batch", "jacobi_plan_set_norm", "jacobi_plan_info", "jacobi_plan_time_sweeps", "jacobi_partition",
            "jacobi_nccl_unique_id", "jacobi_dist_plan_create", "jacobi_bwprobe", "jacobi_last_error",
            "jacobi_version")
 
@@ -63,6 +64,7 @@ def _load():
         "jacobi_plan_destroy": ([vp], None),
         "jacobi_plan_set_row_blocks": ([vp, i32], i32),
         "jacobi_plan_set_batch": ([vp, i32], i32),
+        "jacobi_plan_set_norm": ([vp, i32], i32),
         "jacobi_plan_info": ([vp, P(PlanInfo)], i32),
         "jacobi_plan_time_sweeps": ([vp, vp, vp, i32, P(ctypes.c_float)], i32),
         "jacobi_partition": ([i64, i32, i32, P(i64), P(i64)], i32),
@@ -202,6 +204,10 @@ class Plan:
 
     def set_row_blocks(self, nblocks):
         _check(_lib.jacobi_plan_set_row_blocks(self._h, int(nblocks)))
+
+    def set_norm(self, norm):
+        """'max' (north_star, default) or 'l2' (the paper's Euclidean distance)."""
+        _check(_lib.jacobi_plan_set_norm(self._h, {"max": NORM_MAX, "l2": NORM_L2}.get(norm, -1)))
 
     def set_batch(self, k):
         _check(_lib.jacobi_plan_set_batch(self._h, int(k)))

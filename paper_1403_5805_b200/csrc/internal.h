@@ -35,6 +35,8 @@ struct SweepArgs {
   unsigned* cnt;            // per row-tile arrival counters (reset by the finalizing warp)
   unsigned long long* dslot;// 4-slot ring of max|dx| bit patterns; sweep k uses slot k & 3
   State* st;
+  double* sq;               // norm == L2: (x_i^(k) - x_i^(k-1))^2 of the launch's rows
+  int norm;                 // JACOBI_NORM_MAX / JACOBI_NORM_L2
   int chunk;                // columns per work item (multiple of 512, depends on n only)
   int nchunks;              // ceil(n / chunk)
   int tiles;                // ceil(m / R)
@@ -59,6 +61,10 @@ int variant_rows(int variant);
 int variant_threads(int variant);
 int sweep_grid(int dtype, int variant, int num_sms, int nchunks, int chunk);
 int chunk_for(int64_t n, int dtype);
+enum { kL2Block = 256 };  // rows per L2 partial sum (P-invariant when it divides the rows per rank)
+cudaError_t launch_l2_partials(const double* sq, int64_t m, double* blk, const State* st, cudaStream_t s);
+cudaError_t launch_l2_final(const double* blk, int64_t nblk, unsigned long long* dslot, State* st, int j,
+                            cudaStream_t s);
 double bwprobe(int64_t nbytes, int reps);
 
 }  // namespace jacobi
@@ -71,6 +77,11 @@ struct jacobi_plan {
   int nblocks = 1;               // P12(a) row-block emulation
   int variant = 0;               // sweep kernel variant (R, U, threads); default per dtype, JACOBI_SWEEP_VARIANT overrides
   int batch = 32;                // sweeps per graph batch
+  int norm = JACOBI_NORM_MAX;    // distance of the stop test
+  double* sq = nullptr;          // per-row squared change (L2)
+  double* blk = nullptr;         // local L2 block partials (ceil(m / kL2Block))
+  double* blk_all = nullptr;     // all ranks' block partials (distributed L2)
+  int64_t nblk = 0;
   bool own_stream = false, a_borrowed = false;
   cudaStream_t stream = nullptr;
   const void* dA = nullptr;      // device A (owned or borrowed)
@@ -90,7 +101,7 @@ struct jacobi_plan {
   unsigned long long* zmin_dev = nullptr;
   ncclComm_t comm = nullptr;     // distributed plans only
   cudaGraphExec_t graph = nullptr;
-  int graph_batch = 0, graph_nblocks = 0;
+  int graph_batch = 0, graph_nblocks = 0, graph_norm = -1;
   int64_t sweeps_launched = 0;
   int chunk = 0;
 };

@@ -41,6 +41,9 @@ static int plan_free(jacobi_plan* p) {
   cudaFree(p->dslot);
   cudaFree(p->st);
   cudaFree(p->hist_dev);
+  cudaFree(p->sq);
+  cudaFree(p->blk);
+  cudaFree(p->blk_all);
   cudaFree(p->flag_dev);
   cudaFree(p->zmin_dev);
   if (p->st_host) cudaFreeHost(p->st_host);
@@ -102,6 +105,9 @@ int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dty
   JCUDA(cudaMalloc(&p->x[1], (size_t)p->x_len * 8));
   JCUDA(cudaMalloc(&p->part, (size_t)(nchunks * m) * 8));
   JCUDA(cudaMalloc(&p->cnt, (size_t)m * 4));
+  p->nblk = (m + jacobi::kL2Block - 1) / jacobi::kL2Block;
+  JCUDA(cudaMalloc(&p->sq, (size_t)m * 8));
+  JCUDA(cudaMalloc(&p->blk, (size_t)p->nblk * 8));
   JCUDA(cudaMalloc(&p->dslot, 4 * 8));
   JCUDA(cudaMalloc(&p->st, sizeof(jacobi::State)));
   JCUDA(cudaMalloc(&p->flag_dev, 16));
@@ -169,6 +175,16 @@ extern "C" int jacobi_plan_set_row_blocks(jacobi_plan* p, int nblocks) {
   return 0;
 }
 
+extern "C" int jacobi_plan_set_norm(jacobi_plan* p, int norm) {
+  if (!p || (norm != JACOBI_NORM_MAX && norm != JACOBI_NORM_L2))
+    return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_set_norm: norm must be JACOBI_NORM_MAX or JACOBI_NORM_L2");
+  if (norm == JACOBI_NORM_L2 && p->comm && !p->blk_all) {
+    JCUDA(cudaMalloc(&p->blk_all, (size_t)(p->nblk * p->nranks) * 8));
+  }
+  p->norm = norm;
+  return 0;
+}
+
 extern "C" int jacobi_plan_set_batch(jacobi_plan* p, int K) {
   if (!p || K < 4 || K > 1024 || K % 4 != 0)
     return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_set_batch: K must be a multiple of 4 in [4, 1024]");
@@ -215,6 +231,8 @@ static jacobi::SweepArgs sweep_args(const jacobi_plan* p, int blk) {
   a.cnt = p->cnt;
   a.dslot = p->dslot;
   a.st = p->st;
+  a.sq = p->sq + blk * mb;
+  a.norm = p->norm;
   a.chunk = p->chunk;
   a.nchunks = (int)((p->n + p->chunk - 1) / p->chunk);
   const int R = jacobi::variant_rows_dt(p->variant, p->dtype);
@@ -231,14 +249,26 @@ static int enqueue_sweep(jacobi_plan* p, int j) {
     // k = kbase + j + 1 with kbase a multiple of the batch size (a multiple of 4): parity is static.
     double* xk = p->x[(j + 1) & 1];
     JNCCL(ncclAllGather(xk + p->row0, xk, (size_t)p->m, ncclDouble, p->comm, p->stream));
-    JNCCL(ncclAllReduce(p->dslot + ((j + 1) & 3), p->dslot + ((j + 1) & 3), 1, ncclUint64, ncclMax, p->comm,
-                        p->stream));
+    if (p->norm == JACOBI_NORM_MAX)
+      JNCCL(ncclAllReduce(p->dslot + ((j + 1) & 3), p->dslot + ((j + 1) & 3), 1, ncclUint64, ncclMax, p->comm,
+                          p->stream));
+  }
+  if (p->norm == JACOBI_NORM_L2) {  // PAPER.md:94 Euclidean distance, fixed-order reduction
+    JCUDA(jacobi::launch_l2_partials(p->sq, p->m, p->blk, p->st, p->stream));
+    const double* all = p->blk;
+    int64_t nall = p->nblk;
+    if (p->comm) {
+      JNCCL(ncclAllGather(p->blk, p->blk_all, (size_t)p->nblk, ncclDouble, p->comm, p->stream));
+      all = p->blk_all;
+      nall = p->nblk * p->nranks;
+    }
+    JCUDA(jacobi::launch_l2_final(all, nall, p->dslot, p->st, j, p->stream));
   }
   return 0;
 }
 
 static int ensure_graph(jacobi_plan* p) {
-  if (p->graph && p->graph_batch == p->batch && p->graph_nblocks == p->nblocks) return 0;
+  if (p->graph && p->graph_batch == p->batch && p->graph_nblocks == p->nblocks && p->graph_norm == p->norm) return 0;
   if (p->graph) {
     cudaGraphExecDestroy(p->graph);
     p->graph = nullptr;
@@ -262,6 +292,7 @@ static int ensure_graph(jacobi_plan* p) {
   if (ie != cudaSuccess) return jacobi_set_error(JACOBI_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
   p->graph_batch = p->batch;
   p->graph_nblocks = p->nblocks;
+  p->graph_norm = p->norm;
   return 0;
 }
 
@@ -356,6 +387,9 @@ static int solve_impl(jacobi_plan* p, const double* b, const double* x0, bool de
     } else {
       if (p->hist_cap < max_iter) {
         cudaFree(p->hist_dev);
+  cudaFree(p->sq);
+  cudaFree(p->blk);
+  cudaFree(p->blk_all);
         p->hist_dev = nullptr;
         p->hist_cap = 0;
         JCUDA(cudaMalloc(&p->hist_dev, (size_t)max_iter * 8));

@@ -195,9 +195,10 @@ __global__ void __launch_bounds__(NT, (NT < 512 ? 512 / NT : 1)) k_sweep(const S
       for (int cc = 1; cc < a.nchunks; ++cc) s += __ldcg(a.part + (int64_t)cc * a.m + row);
       const double xnew = __ddiv_rn(__dsub_rn(a.b[row], s), a.diag[row]);
       const int64_t gi = a.row0 + row;
-      const double xold = xo[gi];
+      const double dx = __dsub_rn(xnew, xo[gi]);
       xn[gi] = xnew;
-      dbits = (unsigned long long)__double_as_longlong(__dsub_rn(xnew, xold)) & 0x7fffffffffffffffull;
+      dbits = (unsigned long long)__double_as_longlong(dx) & 0x7fffffffffffffffull;
+      if (a.norm == JACOBI_NORM_L2) a.sq[row] = __dmul_rn(dx, dx);
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -275,10 +276,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
       const int64_t row = r0 + lane;
       const double xnew = __ddiv_rn(__dsub_rn(a.b[row], s), a.diag[row]);
       const int64_t gi = a.row0 + row;
+      const double dx = __dsub_rn(xnew, xo[gi]);
       xn[gi] = xnew;
-      const unsigned long long bits =
-          (unsigned long long)__double_as_longlong(__dsub_rn(xnew, xo[gi])) & 0x7fffffffffffffffull;
+      const unsigned long long bits = (unsigned long long)__double_as_longlong(dx) & 0x7fffffffffffffffull;
       dmax = bits > dmax ? bits : dmax;
+      if (a.norm == JACOBI_NORM_L2) a.sq[row] = __dmul_rn(dx, dx);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&s_empty[q]);
@@ -323,6 +325,35 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
   if (lane == 0) atomicMax(&a.dslot[k & 3], dmax);
 }
 
+
+// Euclidean distance (NEXT-2 row), deterministic: k_l2_partials sums each block of
+// kL2Block rows' squared changes with a fixed smem tree; k_l2_final (one warp) sums the block partials
+// of all ranks (lane l: blocks l, l+32, ... ascending; then a shfl_xor butterfly) and stores the
+// bits of sqrt(sum) in the sweep's distance slot, overwriting the max-norm bits.
+__global__ void __launch_bounds__(kL2Block) k_l2_partials(const double* __restrict__ sq, int64_t m,
+                                                          double* __restrict__ blk, const State* st) {
+  if (*(volatile const int32_t*)&st->done) return;
+  __shared__ double s[kL2Block];
+  const int64_t i = (int64_t)blockIdx.x * kL2Block + threadIdx.x;
+  s[threadIdx.x] = i < m ? sq[i] : 0.0;
+  __syncthreads();
+  for (int off = kL2Block / 2; off > 0; off >>= 1) {
+    if (threadIdx.x < off) s[threadIdx.x] = __dadd_rn(s[threadIdx.x], s[threadIdx.x + off]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) blk[blockIdx.x] = s[0];
+}
+
+__global__ void k_l2_final(const double* __restrict__ blk, int64_t nblk, unsigned long long* dslot, State* st,
+                           int j) {
+  if (*(volatile int32_t*)&st->done) return;
+  const int64_t k = st->kbase + j + 1;
+  double s = 0.0;
+  for (int64_t q = threadIdx.x; q < nblk; q += 32) s = __dadd_rn(s, blk[q]);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s = __dadd_rn(s, __shfl_xor_sync(kFull, s, off));
+  if (threadIdx.x == 0) dslot[k & 3] = (unsigned long long)__double_as_longlong(__dsqrt_rn(s));
+}
 
 // After a graph batch of K sweeps: settle the stop decision for the batch's last sweep (same rule
 // as the prologue) and advance the sweep counter.
@@ -440,11 +471,13 @@ bool variant_fits(int v, int nchunks, int dtype, int chunk) {
   return !V.cta || (nchunks >= V.threads / 32 && variant_smem(v, nchunks, dtype, chunk) <= 48 * 1024);
 }
 int variant_rows_dt(int v, int /*dtype*/) { return kVariants[v].R; }
-// Defaults from B200 measurements (profiles/variants*_r01_*.jsonl): fp64 uses the CTA-cooperative
-// kernel (R=4) when n has at least 16 chunks (c4: 7180 GB/s), else the item kernel R=8,U=1; fp32 uses
-// the item kernel R=4,U=1 (c5: 6830 GB/s).
+// Defaults from B200 measurements (profiles/variants5_r01_*.jsonl, sustained 100-sweep graph solves):
+// the CTA-cooperative kernel when n has at least 16 chunks — fp64 R=4 with 2 steps in flight (c4:
+// 7178 GB/s sustained, 7232 burst), fp32 R=4 (c5: 6734 burst) — else the item kernel R=8,U=1 (fp64)
+// or R=4,U=1 (fp32).
 int default_variant(int dtype, int nchunks, int chunk) {
-  if (variant_fits(7, nchunks, dtype, chunk)) return 7;
+  const int big = dtype == JACOBI_F32 ? 7 : 9;
+  if (variant_fits(big, nchunks, dtype, chunk)) return big;
   return dtype == JACOBI_F32 ? 0 : 1;
 }
 int variant_rows(int v) { return kVariants[v].R; }
@@ -474,6 +507,17 @@ cudaError_t launch_sweep(int dtype, int v, const SweepArgs& a, int j, int grid, 
   const size_t smem = variant_smem(v, a.nchunks, dtype, a.chunk);
   if (dtype == JACOBI_F32) V.f32<<<grid, V.threads, smem, s>>>(a, j);
   else V.f64<<<grid, V.threads, smem, s>>>(a, j);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_l2_partials(const double* sq, int64_t m, double* blk, const State* st, cudaStream_t s) {
+  k_l2_partials<<<(unsigned)((m + kL2Block - 1) / kL2Block), kL2Block, 0, s>>>(sq, m, blk, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_l2_final(const double* blk, int64_t nblk, unsigned long long* dslot, State* st, int j,
+                            cudaStream_t s) {
+  k_l2_final<<<1, 32, 0, s>>>(blk, nblk, dslot, st, j);
   return cudaGetLastError();
 }
 

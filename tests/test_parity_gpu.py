@@ -317,3 +317,39 @@ def test_all_sweep_variants_bitwise_identical(jb, n, f32, monkeypatch):
             ref = (r, c)
         assert np.array_equal(r.x, ref[0].x) and np.array_equal(r.hist, ref[0].hist), v
         assert (c.status, c.iters) == (ref[1].status, ref[1].iters) and np.array_equal(c.x, ref[1].x), v
+
+
+# ------------------------------------------------------------------ NEXT-2: Euclidean stop rule
+def test_l2_norm_parity_and_pins(jb):
+    A2 = np.array([[2.0, 1.0], [1.0, 3.0]])
+    b2 = np.array([3.0, 4.0])
+    with jb.Plan(A2) as p:
+        p.set_norm("l2")
+        r = p.solve(b2, None, 1000, 1e-12, history=True)
+    assert (r.status, r.iters) == (jb.CONVERGED, 33)  # closed form: d_32 = 5*6^-16 >= tol > d_33
+    assert r.hist[1] == pytest.approx(5 / 6, rel=1e-12) and r.hist[0] == pytest.approx(math.sqrt(145) / 6, rel=1e-12)
+    for n, scale in ((300, 1.02), (3000, 1.02), (8192, 1.05)):
+        A, b, _ = dominant(n, 41 + n, scale=scale)
+        st_o, x_o, it_o, h_o = oracle.jacobi(A, b, None, 3000, 1e-10, nthreads=16, history=True, norm="l2")
+        st_m, _, it_m = oracle.jacobi(A, b, None, 3000, 1e-10, nthreads=16, norm="max")
+        with jb.Plan(A) as p:
+            p.set_norm("l2")
+            r = p.solve(b, None, 3000, 1e-10, history=True)
+            assert (r.status, r.iters) == (st_o, it_o) and rel_linf(r.x, x_o) <= TOL64
+            np.testing.assert_allclose(r.hist, h_o, rtol=1e-9, atol=1e-14)
+            if n == 8192:  # P12a with the L2 reduction: row blocks that are multiples of 256 rows
+                for nb in (2, 4, 8):
+                    p.set_row_blocks(nb)
+                    rb = p.solve(b, None, 3000, 1e-10, history=True)
+                    assert rb.iters == r.iters and np.array_equal(rb.x, r.x) and np.array_equal(rb.hist, r.hist)
+                p.set_row_blocks(1)
+            p.set_norm("max")
+            rm = p.solve(b, None, 3000, 1e-10)
+            assert rm.iters == it_m <= r.iters  # ||.||_2 >= ||.||_inf: never stops earlier
+    # divergent paper regime: NaN/Inf-sticky with the L2 sum too
+    rng = np.random.default_rng(14)
+    A = rng.uniform(0, 1, (64, 64))
+    with jb.Plan(A) as p:
+        p.set_norm("l2")
+        r = p.solve(rng.uniform(0, 1, 64), None, 500, 1e-8, history=True)
+    assert (r.status, r.iters) == (jb.MAX_ITER, 500) and not np.isfinite(r.hist[-1])
