@@ -8,6 +8,7 @@
 #include "internal.h"
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -27,33 +28,45 @@ int jacobi_set_error(int code, const std::string& msg) {
 extern "C" const char* jacobi_last_error(void) { return g_err.c_str(); }
 extern "C" int jacobi_version(void) { return 100; }
 
+// Frees everything the plan owns.  Every release is checked; the first failure is reported through
+// jacobi_last_error (destroy itself cannot return a status) and the runtime's error state is cleared.
 static int plan_free(jacobi_plan* p) {
   if (!p) return 0;
-  if (p->graph) cudaGraphExecDestroy(p->graph);
+  std::string first;
+  auto chk = [&](cudaError_t e, const char* what) {
+    if (e != cudaSuccess && first.empty()) first = std::string(what) + ": " + cudaGetErrorString(e);
+  };
+  if (p->graph) chk(cudaGraphExecDestroy(p->graph), "cudaGraphExecDestroy");
   if (p->comm) ncclCommDestroy(p->comm);
-  cudaFree(p->dA_owned);
-  cudaFree(p->diag);
-  cudaFree(p->b);
-  cudaFree(p->x[0]);
-  cudaFree(p->x[1]);
-  cudaFree(p->part);
-  cudaFree(p->cnt);
-  cudaFree(p->dslot);
-  cudaFree(p->st);
-  cudaFree(p->hist_dev);
-  cudaFree(p->sq);
-  cudaFree(p->blk);
-  cudaFree(p->blk_all);
-  cudaFree(p->flag_dev);
-  cudaFree(p->zmin_dev);
-  if (p->st_host) cudaFreeHost(p->st_host);
-  if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
+  void* dev[] = {p->dA_owned, p->diag, p->b, p->x[0], p->x[1], p->part, p->cnt, p->dslot, p->st,
+                 p->hist_dev, p->flag_dev, p->zmin_dev, p->sq, p->blk, p->blk_all};
+  const char* names[] = {"A", "diag", "b", "x0", "x1", "part", "cnt", "dslot", "state", "hist", "flag", "zmin",
+                         "sq", "blk", "blk_all"};
+  for (size_t i = 0; i < sizeof(dev) / sizeof(dev[0]); ++i)
+    if (dev[i]) chk(cudaFree(dev[i]), names[i]);
+  if (p->st_host) chk(cudaFreeHost(p->st_host), "cudaFreeHost(state)");
+  if (p->own_stream && p->stream) chk(cudaStreamDestroy(p->stream), "cudaStreamDestroy");
   delete p;
+  cudaGetLastError();
+  if (!first.empty()) return jacobi_set_error(JACOBI_ECUDA, "plan release: " + first);
   return 0;
 }
 
+// Attribute a pending (asynchronously reported) CUDA error to the step that produced it.
+static int check_last(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return jacobi_set_error(JACOBI_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return 0;
+}
+#define JLAST(what)                  \
+  do {                               \
+    int _rc = check_last(what);      \
+    if (_rc) return _rc;             \
+  } while (0)
+
 int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dtype, const void* A, int64_t lda,
                      int a_on_device, void* stream) {
+  JLAST("pending CUDA error before plan creation");
   p->n = n;
   p->m = m;
   p->row0 = row0;
@@ -96,7 +109,9 @@ int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dty
     int vi = atoi(v);
     if (vi >= 0 && vi < jacobi::num_variants() && jacobi::variant_fits(vi, nch, dtype, p->chunk)) p->variant = vi;
   }
+  JLAST("A upload");
   p->grid = jacobi::sweep_grid(dtype, p->variant, p->num_sms, nch, p->chunk);
+  JLAST("sweep kernel occupancy query");
   p->x_len = round_up(n, 256) + 256;
   const int64_t nchunks = (n + p->chunk - 1) / p->chunk;
   JCUDA(cudaMalloc(&p->diag, (size_t)m * 8));
@@ -116,6 +131,7 @@ int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dty
   JCUDA(cudaMemsetAsync(p->x[0], 0, (size_t)p->x_len * 8, p->stream));
   JCUDA(cudaMemsetAsync(p->x[1], 0, (size_t)p->x_len * 8, p->stream));
   JCUDA(cudaMemsetAsync(p->cnt, 0, (size_t)m * 4, p->stream));
+  JLAST("plan buffers");
   return 0;
 }
 
@@ -165,7 +181,8 @@ extern "C" int jacobi_plan_create(jacobi_plan** out, int64_t n, int dtype, const
 
 extern "C" void jacobi_plan_destroy(jacobi_plan* p) {
   if (p && p->stream) cudaStreamSynchronize(p->stream);
-  plan_free(p);
+  int rc = plan_free(p);
+  if (rc && getenv("JACOBI_DEBUG")) fprintf(stderr, "jacobi_plan_destroy: %s\n", jacobi_last_error());
 }
 
 extern "C" int jacobi_plan_set_row_blocks(jacobi_plan* p, int nblocks) {
@@ -387,9 +404,6 @@ static int solve_impl(jacobi_plan* p, const double* b, const double* x0, bool de
     } else {
       if (p->hist_cap < max_iter) {
         cudaFree(p->hist_dev);
-  cudaFree(p->sq);
-  cudaFree(p->blk);
-  cudaFree(p->blk_all);
         p->hist_dev = nullptr;
         p->hist_cap = 0;
         JCUDA(cudaMalloc(&p->hist_dev, (size_t)max_iter * 8));
@@ -413,6 +427,7 @@ static int solve_impl(jacobi_plan* p, const double* b, const double* x0, bool de
   if (hist && !dev && fin.iters > 0)
     JCUDA(cudaMemcpyAsync(hist, hist_dev, (size_t)fin.iters * 8, cudaMemcpyDeviceToHost, p->stream));
   JCUDA(cudaStreamSynchronize(p->stream));
+  JLAST("solve");
   *iters_out = fin.iters;
   return fin.status;
 }
