@@ -353,3 +353,35 @@ def test_l2_norm_parity_and_pins(jb):
         p.set_norm("l2")
         r = p.solve(rng.uniform(0, 1, 64), None, 500, 1e-8, history=True)
     assert (r.status, r.iters) == (jb.MAX_ITER, 500) and not np.isfinite(r.hist[-1])
+
+
+# ------------------------------------------------------------------ distributed plan (NCCL path), one rank
+def test_dist_plan_single_rank_matches_plain_plan(jb):
+    """jacobi_dist_plan_create with nranks = 1 runs the captured NCCL allgather / u64 max-allreduce /
+    L2 block allgather path on one GPU; it must equal the plain plan bitwise (pin P12 at P = 1)."""
+    import torch
+    n = 4096
+    A, b, _ = dominant(n, 77, scale=1.05)
+    uid = jb.nccl_unique_id()
+    with jb.Plan(A) as p0:
+        ref = p0.solve(b, None, 60, 1e-11, history=True)
+        p0.set_norm("l2")
+        ref2 = p0.solve(b, None, 60, 1e-11, history=True)
+    dA = torch.from_numpy(A).cuda()
+    with jb.Plan(dA, n=n, dist=(uid, 0, 1)) as p:
+        inf = p.info
+        assert (inf.rank, inf.nranks, inf.rows, inf.row0) == (0, 1, n, 0)
+        r = p.solve(b, None, 60, 1e-11, history=True)
+        assert (r.status, r.iters) == (ref.status, ref.iters)
+        assert np.array_equal(r.x, ref.x) and np.array_equal(r.hist, ref.hist)
+        p.set_norm("l2")
+        r2 = p.solve(b, None, 60, 1e-11, history=True)
+        assert (r2.status, r2.iters) == (ref2.status, ref2.iters) and np.array_equal(r2.x, ref2.x)
+        db = torch.from_numpy(b).cuda()
+        ms = p.time_sweeps(db, torch.zeros(n, dtype=torch.float64, device="cuda"), 3)
+        assert (ms > 0).all()
+    Z = A.copy()
+    Z[5, 5] = 0.0
+    with pytest.raises(jb.JacobiError) as e:
+        jb.Plan(Z, dist=(jb.nccl_unique_id(), 0, 1))
+    assert e.value.status == jb.EZERODIAG and "i = 5" in str(e.value)
