@@ -41,13 +41,18 @@ __device__ __forceinline__ void ld_a(const float* p, float (&v)[8]) {
       : "l"(p));
 }
 // x^(k-1) is read-only during the sweep (it lives in the other ping-pong buffer): L1-cached loads.
+template <int XL>
 __device__ __forceinline__ void ld_x4(const double* p, double* v) {
-  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+  if (XL)  // keep x^(k-1) in L1 with priority over everything else
+    asm("ld.global.nc.L1::evict_last.v4.f64 {%0,%1,%2,%3}, [%4];"
+        : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+  else
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
 }
-template <int E>
+template <int E, int XL = 0>
 __device__ __forceinline__ void ld_x(const double* p, double (&v)[E]) {
 #pragma unroll
-  for (int q = 0; q < E; q += 4) ld_x4(p + q, v + q);
+  for (int q = 0; q < E; q += 4) ld_x4<XL>(p + q, v + q);
 }
 
 // Prologue of sweep k (PAPER.md:64-66 evaluated on the device): decides whether sweep k runs.
@@ -76,7 +81,7 @@ __device__ __forceinline__ bool sweep_prologue(const SweepArgs& a, int j, bool l
 // variant shares: lane l owns columns c0 + (32*s + l)*E + e, accumulated in ascending s then e with
 // one DFMA chain per row; j == i (the diagonal) and j >= n are skipped.  Rows r >= nv
 // are not loaded (their sums are unused).
-template <typename T, int R, int U>
+template <typename T, int R, int U, int XL = 0>
 __device__ __forceinline__ void accumulate_chunk(const T* const (&rowp)[R], const int nv,
                                                  const double* __restrict__ xo, const int64_t c0,
                                                  const int64_t c1, const int chunk, const int64_t n,
@@ -116,7 +121,7 @@ __device__ __forceinline__ void accumulate_chunk(const T* const (&rowp)[R], cons
       if (col < n) {
         T av[R][E];
         double xv[E];
-        ld_x<E>(xo + col, xv);
+        ld_x<E, XL>(xo + col, xv);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           if (r < nv) ld_a(rowp[r] + col, av[r]);
@@ -237,7 +242,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
 
 constexpr int kSlots = 4;
 
-template <typename T, int R, int NW, int U = 1>
+template <typename T, int R, int NW, int U = 1, int XL = 0>
 __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, const int j) {
   extern __shared__ __align__(16) double s_part[];  // [kSlots][nchunks][R]
   __shared__ __align__(8) uint64_t s_full[kSlots], s_empty[kSlots];
@@ -301,7 +306,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
       for (int r = 0; r < R; ++r) acc[r] = 0.0;
       const int64_t c0 = (int64_t)c * a.chunk;
       const int64_t c1 = min(c0 + (int64_t)a.chunk, a.n);
-      accumulate_chunk<T, R, U>(rowp, nv, xo, c0, c1, a.chunk, a.n, g0, lane, acc);
+      accumulate_chunk<T, R, U, XL>(rowp, nv, xo, c0, c1, a.chunk, a.n, g0, lane, acc);
 #pragma unroll
       for (int r = 0; r < R; ++r)
 #pragma unroll
@@ -454,6 +459,8 @@ const Variant kVariants[] = {
     {8, 256, 1, k_sweep_cta<double, 8, 8>, k_sweep_cta<float, 4, 8>},
     {4, 512, 1, k_sweep_cta<double, 4, 16, 2>, k_sweep_cta<float, 4, 16, 2>},
     {2, 512, 1, k_sweep_cta<double, 2, 16, 4>, k_sweep_cta<float, 2, 16, 2>},
+    {4, 512, 1, k_sweep_cta<double, 4, 16, 2, 1>, k_sweep_cta<float, 4, 16, 1, 1>},
+    {8, 512, 1, k_sweep_cta<double, 8, 16, 1, 1>, k_sweep_cta<float, 4, 16, 2, 1>},
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
