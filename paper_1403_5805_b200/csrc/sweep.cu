@@ -459,8 +459,6 @@ const Variant kVariants[] = {
     {8, 256, 1, k_sweep_cta<double, 8, 8>, k_sweep_cta<float, 4, 8>},
     {4, 512, 1, k_sweep_cta<double, 4, 16, 2>, k_sweep_cta<float, 4, 16, 2>},
     {2, 512, 1, k_sweep_cta<double, 2, 16, 4>, k_sweep_cta<float, 2, 16, 2>},
-    {4, 512, 1, k_sweep_cta<double, 4, 16, 2, 1>, k_sweep_cta<float, 4, 16, 1, 1>},
-    {8, 512, 1, k_sweep_cta<double, 8, 16, 1, 1>, k_sweep_cta<float, 4, 16, 2, 1>},
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 

@@ -16,7 +16,7 @@ import paper_1403_5805_b200 as jb  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c4"
 sweeps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
-variants = [int(v) for v in sys.argv[3].split(",")] if len(sys.argv) > 3 else list(range(13))
+variants = [int(v) for v in sys.argv[3].split(",")] if len(sys.argv) > 3 else list(range(11))
 cfg = g.CONFIGS[name]
 n = cfg.n
 dt = torch.float32 if cfg.a_dtype == g.F32 else torch.float64

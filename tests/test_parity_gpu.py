@@ -299,14 +299,14 @@ def test_all_sweep_variants_bitwise_identical(jb, n, f32, monkeypatch):
     A, b, _ = dominant(n, 31 + n, scale=1.05, f32=f32)
     st_o, x_o, it_o, h_o = oracle.jacobi(A, b, None, 12, 0.0, nthreads=16, history=True)
     ref = None
-    nvar = 13
+    nvar = 11
     for v in range(nvar):
         monkeypatch.setenv("JACOBI_SWEEP_VARIANT", str(v))
         with jb.Plan(A) as p:
             assert p.info.num_variants == nvar
             r = p.solve(b, None, 12, 0.0, history=True)
             c = p.solve(b, None, 500, 1e-11)
-            if n == 8190 and v in (6, 7, 9, 10, 11, 12):
+            if n == 8190 and v in (6, 7, 9, 10):
                 for nb in (2, 3, 5):  # P12a through the CTA kernel, ragged rows per CTA
                     p.set_row_blocks(nb)
                     rb = p.solve(b, None, 12, 0.0, history=True)
