@@ -10,7 +10,7 @@ NVFLAGS   := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v
 NCCL_DIR  := $(shell $(PY) -c "import nvidia.nccl, os; print(list(nvidia.nccl.__path__)[0])" 2>/dev/null)
 PKG       := paper_1403_5805_b200
 
-LIB_SRCS  := $(PKG)/csrc/sweep.cu $(PKG)/csrc/plan.cu $(PKG)/csrc/dist.cu
+LIB_SRCS  := $(PKG)/csrc/sweep.cu $(PKG)/csrc/cluster.cu $(PKG)/csrc/plan.cu $(PKG)/csrc/dist.cu
 LIB_HDRS  := include/jacobi.h $(PKG)/csrc/internal.h
 
 all: oracle gen lib probe

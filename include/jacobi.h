@@ -111,6 +111,9 @@ typedef struct {
   double bytes_per_sweep;       /* algorithmic HBM bytes per sweep: rows*n*s_A + 8n + 16*rows  */
   int variant;                  /* sweep kernel variant in use (JACOBI_SWEEP_VARIANT overrides)  */
   int num_variants;             /* variants compiled in (all give bitwise-identical results)    */
+  int cluster_ctas;             /* > 0: small-n plan, each solve runs in one thread-block-cluster
+                                   launch with A resident in shared memory (same bits); 0: graph
+                                   of sweep kernels.  JACOBI_SMALL_N=0 in the environment disables */
 } jacobi_plan_info_t;
 int jacobi_plan_info(const jacobi_plan* plan, jacobi_plan_info_t* info);
 

@@ -1,0 +1,276 @@
+// cluster.cu — small-n solver: a whole solve in one thread-block-cluster
+// launch, A resident in shared memory, x exchanged through distributed shared memory (DSMEM).
+//
+// For small n the graph-of-sweeps path is launch-latency bound (c1, n = 256: ~7 µs per sweep for
+// ~1 µs of work).  Here a cluster of C CTAs (16 when the part allows non-portable clusters, else 8)
+// splits the rows; CTA r loads its rows of A into shared memory once, and each sweep
+//   1. computes its rows in the canonical summation order of sweep.cu (chunks of chunk(n, dtype)
+//      columns; lane l owns columns c0 + (32 s + l)·E + e, one DFMA chain, shfl_xor butterfly, chunk
+//      sums ascending; diagonal and j >= n skipped — PAPER.md:55), so every bit equals the sweep
+//      kernels' result;
+//   2. stores x_i^(k) into every CTA's copy of x (DSMEM stores, lanes 0..C-1 one peer each) and its
+//      max |dx| bits (or, for the Euclidean rule, dx^2) into every CTA's slot;
+//   3. one cluster barrier; then every CTA evaluates the same stop test: max of the
+//      C slots, or the fixed 256-row tree + strided warp sum of k_l2_partials / k_l2_final.
+// A launch runs at most kMaxSweepsPerLaunch sweeps and writes x and the stop state back, so long
+// runs stay interruptible; the next launch resumes from global x.
+#include "internal.h"
+#include <cooperative_groups.h>
+
+namespace cg = cooperative_groups;
+
+namespace jacobi {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kCT = 256;  // threads per CTA
+constexpr int kMaxC = 16;
+
+template <typename T> struct EOf;
+template <> struct EOf<double> { static constexpr int E = 4; };
+template <> struct EOf<float> { static constexpr int E = 8; };
+
+__host__ __device__ inline size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
+
+struct Layout {  // dynamic shared memory of one CTA
+  size_t a_off, xs_off, sq_off, dsl_off, red_off, blk_off, total;
+  int lds, xlen, n256;
+};
+
+__host__ __device__ inline Layout layout(int n, int C, int esz) {
+  Layout L;
+  const int rows_max = (n + C - 1) / C;
+  L.lds = (n + 7) / 8 * 8;
+  L.xlen = L.lds;
+  L.n256 = (n + kL2Block - 1) / kL2Block * kL2Block;
+  L.a_off = 0;
+  L.xs_off = align16((size_t)rows_max * L.lds * esz);
+  L.sq_off = L.xs_off + align16((size_t)2 * L.xlen * 8);
+  L.dsl_off = L.sq_off + align16((size_t)2 * L.n256 * 8);
+  L.red_off = L.dsl_off + align16((size_t)2 * kMaxC * 8);
+  L.blk_off = L.red_off + align16((size_t)kCT * 8);
+  L.total = L.blk_off + align16((size_t)(L.n256 / kL2Block) * 8 + 8 * 8);
+  return L;
+}
+
+struct ClusterArgs {
+  const void* A;
+  int64_t lda;
+  int n, chunk, nchunks, norm;
+  const double* diag;
+  const double* b;
+  double* x0buf;
+  double* x1buf;
+  State* st;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, const int64_t k0, const int64_t k1) {
+  constexpr int E = EOf<T>::E;
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = (int)cl.num_blocks();
+  const int rank = (int)cl.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = a.n;
+  const Layout L = layout(n, C, (int)sizeof(T));
+  extern __shared__ __align__(16) unsigned char sm[];
+  T* As = reinterpret_cast<T*>(sm + L.a_off);
+  double* xs = reinterpret_cast<double*>(sm + L.xs_off);
+  double* sq = reinterpret_cast<double*>(sm + L.sq_off);
+  unsigned long long* dsl = reinterpret_cast<unsigned long long*>(sm + L.dsl_off);
+  double* red = reinterpret_cast<double*>(sm + L.red_off);
+  double* blk = reinterpret_cast<double*>(sm + L.blk_off);
+  __shared__ unsigned long long s_wmax[kCT / 32];
+
+  State* st = a.st;
+  if (*(volatile int32_t*)&st->done) return;  // uniform for the whole cluster
+  const double tol = st->tol;
+  const int64_t max_iter = st->max_iter;
+  double* hist = st->hist;
+  const int r_begin = (int)((int64_t)rank * n / C), r_end = (int)((int64_t)(rank + 1) * n / C);
+  const int nr = r_end - r_begin;
+
+  // Resident data: own rows of A (zero padded to lds), x^(k0-1), zeroed L2 buffers.
+  const T* Ag = static_cast<const T*>(a.A);
+  for (int64_t idx = tid; idx < (int64_t)nr * L.lds; idx += kCT) {
+    const int r = (int)(idx / L.lds), c = (int)(idx % L.lds);
+    As[idx] = c < n ? Ag[(int64_t)(r_begin + r) * a.lda + c] : T(0);
+  }
+  const int p0 = (int)((k0 - 1) & 1);
+  const double* xg = p0 ? a.x1buf : a.x0buf;
+  for (int i = tid; i < L.xlen; i += kCT) xs[p0 * L.xlen + i] = i < n ? xg[i] : 0.0;
+  for (int i = tid; i < 2 * L.n256; i += kCT) sq[i] = 0.0;
+  cl.sync();
+
+  const int nsteps = a.chunk / (32 * E);
+  int stop = 0;  // 1 converged, 2 iteration limit
+  int64_t k = k0;
+  for (; k <= k1; ++k) {
+    const int par = (int)(k & 1);
+    const double* xo = xs + (1 - par) * L.xlen;
+    unsigned long long dmax = 0ull;
+    for (int r = warp; r < nr; r += kCT / 32) {
+      const int grow = r_begin + r;
+      const T* arow = As + (size_t)r * L.lds;
+      double s = 0.0;
+      for (int c = 0; c < a.nchunks; ++c) {
+        const int c0 = c * a.chunk;
+        double acc = 0.0;
+        for (int step = 0; step < nsteps; ++step) {
+          const int col = c0 + (step * 32 + lane) * E;
+          if (col < n) {
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+              const int cc = col + e;
+              if (cc < n && cc != grow) acc = __fma_rn((double)arow[cc], xo[cc], acc);
+            }
+          }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(kFull, acc, off);
+        s = c == 0 ? acc : s + acc;
+      }
+      const double xnew = __ddiv_rn(__dsub_rn(a.b[grow], s), a.diag[grow]);
+      const double dx = __dsub_rn(xnew, xo[grow]);
+      if (lane < C) {
+        double* px = cl.map_shared_rank(xs + par * L.xlen, lane);
+        px[grow] = xnew;
+        if (a.norm == JACOBI_NORM_L2) {
+          double* ps = cl.map_shared_rank(sq + par * L.n256, lane);
+          ps[grow] = __dmul_rn(dx, dx);
+        }
+      }
+      const unsigned long long bits = (unsigned long long)__double_as_longlong(dx) & 0x7fffffffffffffffull;
+      dmax = bits > dmax ? bits : dmax;
+    }
+    if (lane == 0) s_wmax[warp] = dmax;
+    __syncthreads();
+    if (tid < C) {
+      unsigned long long m = 0ull;
+#pragma unroll
+      for (int w = 0; w < kCT / 32; ++w) m = s_wmax[w] > m ? s_wmax[w] : m;
+      unsigned long long* pd = cl.map_shared_rank(dsl + par * kMaxC, tid);
+      pd[rank] = m;
+    }
+    cl.sync();  // x^(k), the maxima and dx^2 of every row are visible in every CTA
+
+    double d;
+    if (a.norm == JACOBI_NORM_L2) {  // identical arithmetic to k_l2_partials + k_l2_final
+      const double* sqk = sq + par * L.n256;
+      const int nblk = L.n256 / kL2Block;
+      for (int q = 0; q < nblk; ++q) {
+        red[tid] = sqk[q * kL2Block + tid];  // rows >= n hold 0.0
+        __syncthreads();
+        for (int off = kL2Block / 2; off > 0; off >>= 1) {
+          if (tid < off) red[tid] = __dadd_rn(red[tid], red[tid + off]);
+          __syncthreads();
+        }
+        if (tid == 0) blk[q] = red[0];
+        __syncthreads();
+      }
+      double t = 0.0;
+      for (int q = lane; q < nblk; q += 32) t = __dadd_rn(t, blk[q]);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) t = __dadd_rn(t, __shfl_xor_sync(kFull, t, off));
+      d = __dsqrt_rn(t);
+    } else {
+      unsigned long long m = 0ull;
+      for (int q = 0; q < C; ++q) m = dsl[par * kMaxC + q] > m ? dsl[par * kMaxC + q] : m;
+      d = __longlong_as_double((long long)m);
+    }
+    if (rank == 0 && tid == 0 && hist) hist[k - 1] = d;
+    if (d < tol) { stop = 1; break; }        // return X
+    if (k == max_iter) { stop = 2; break; }  // iteration limit
+  }
+  const int64_t klast = stop ? k : k1;
+  double* xgo = (klast & 1) ? a.x1buf : a.x0buf;
+  const double* xsl = xs + (int)(klast & 1) * L.xlen;
+  for (int r = tid; r < nr; r += kCT) xgo[r_begin + r] = xsl[r_begin + r];
+  if (rank == 0 && tid == 0) {
+    if (stop == 1) { st->status = JACOBI_CONVERGED; st->iters = klast; st->done = 1; }
+    if (stop == 2) { st->status = JACOBI_MAX_ITER; st->iters = max_iter; st->done = 1; }
+    st->kbase = klast;
+  }
+  cl.sync();  // no CTA leaves while a peer may still write into its shared memory
+}
+
+template <typename T>
+cudaError_t try_cluster(int n, int C, size_t* smem_out, int* ok) {
+  const Layout L = layout(n, C, (int)sizeof(T));
+  *ok = 0;
+  *smem_out = L.total;
+  int maxsm = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (L.total > (size_t)maxsm) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k_solve_cluster<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+  if (e != cudaSuccess) return e;
+  if (C > 8) {
+    e = cudaFuncSetAttribute(k_solve_cluster<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) { cudaGetLastError(); return cudaSuccess; }
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(kCT);
+  cfg.dynamicSmemBytes = L.total;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  e = cudaOccupancyMaxActiveClusters(&nclusters, k_solve_cluster<T>, &cfg);
+  if (e != cudaSuccess) { cudaGetLastError(); return cudaSuccess; }
+  *ok = nclusters >= 1;
+  return cudaSuccess;
+}
+
+}  // namespace
+
+// Largest usable cluster (16, else 8) for an n x n system of this dtype; 0 when A does not fit.
+int cluster_plan(int64_t n, int dtype, size_t* smem) {
+  if (n < 1 || n > 4096) return 0;
+  for (int C : {16, 8}) {
+    int ok = 0;
+    cudaError_t e = dtype == JACOBI_F32 ? try_cluster<float>((int)n, C, smem, &ok)
+                                        : try_cluster<double>((int)n, C, smem, &ok);
+    if (e != cudaSuccess) { cudaGetLastError(); return 0; }
+    if (ok) return C;
+  }
+  return 0;
+}
+
+cudaError_t launch_solve_cluster(int dtype, int C, size_t smem, const void* A, int64_t lda, int64_t n, int chunk,
+                                 int norm, const double* diag, const double* b, double* x0buf, double* x1buf,
+                                 State* st, int64_t k0, int64_t k1, cudaStream_t s) {
+  ClusterArgs a;
+  a.A = A;
+  a.lda = lda;
+  a.n = (int)n;
+  a.chunk = chunk;
+  a.nchunks = (int)((n + chunk - 1) / chunk);
+  a.norm = norm;
+  a.diag = diag;
+  a.b = b;
+  a.x0buf = x0buf;
+  a.x1buf = x1buf;
+  a.st = st;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(kCT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (dtype == JACOBI_F32) return cudaLaunchKernelEx(&cfg, k_solve_cluster<float>, a, k0, k1);
+  return cudaLaunchKernelEx(&cfg, k_solve_cluster<double>, a, k0, k1);
+}
+
+}  // namespace jacobi

@@ -61,6 +61,12 @@ int variant_rows(int variant);
 int variant_threads(int variant);
 int sweep_grid(int dtype, int variant, int num_sms, int nchunks, int chunk);
 int chunk_for(int64_t n, int dtype);
+// cluster.cu (NEXT-3 small-n solver)
+int cluster_plan(int64_t n, int dtype, size_t* smem);
+cudaError_t launch_solve_cluster(int dtype, int C, size_t smem, const void* A, int64_t lda, int64_t n, int chunk,
+                                 int norm, const double* diag, const double* b, double* x0buf, double* x1buf,
+                                 State* st, int64_t k0, int64_t k1, cudaStream_t s);
+enum { kMaxSweepsPerLaunch = 4096 };
 enum { kL2Block = 256 };  // rows per L2 partial sum (P-invariant when it divides the rows per rank)
 cudaError_t launch_l2_partials(const double* sq, int64_t m, double* blk, const State* st, cudaStream_t s);
 cudaError_t launch_l2_final(const double* blk, int64_t nblk, unsigned long long* dslot, State* st, int j,
@@ -78,6 +84,8 @@ struct jacobi_plan {
   int variant = 0;               // sweep kernel variant (R, U, threads); default per dtype, JACOBI_SWEEP_VARIANT overrides
   int batch = 32;                // sweeps per graph batch
   int norm = JACOBI_NORM_MAX;    // distance of the stop test
+  int cluster_C = 0;             // > 0: small-n solves run in one cluster launch (cluster.cu)
+  size_t cluster_smem = 0;
   double* sq = nullptr;          // per-row squared change (L2)
   double* blk = nullptr;         // local L2 block partials (ceil(m / kL2Block))
   double* blk_all = nullptr;     // all ranks' block partials (distributed L2)

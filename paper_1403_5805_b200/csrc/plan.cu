@@ -165,6 +165,11 @@ extern "C" int jacobi_plan_create(jacobi_plan** out, int64_t n, int dtype, const
     return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_create: bad argument (out/A NULL, n < 1, lda < n or dtype)");
   jacobi_plan* p = new jacobi_plan();
   int rc = plan_init_common(p, n, n, 0, dtype, A, lda, a_on_device, cuda_stream);
+  if (rc == 0) {
+    const char* e = getenv("JACOBI_SMALL_N");
+    if (!(e && e[0] == '0')) p->cluster_C = jacobi::cluster_plan(n, dtype, &p->cluster_smem);
+    rc = check_last("small-n cluster setup");
+  }
   unsigned long long zr = 0;
   int nf = 0;
   if (rc == 0) rc = plan_validate_A(p, &zr, &nf);
@@ -228,6 +233,7 @@ extern "C" int jacobi_plan_info(const jacobi_plan* p, jacobi_plan_info_t* info) 
   info->bytes_per_sweep = (double)p->m * (double)p->n * sA + 8.0 * (double)p->n + 16.0 * (double)p->m;
   info->variant = p->variant;
   info->num_variants = jacobi::num_variants();
+  info->cluster_ctas = (p->cluster_C && p->nblocks == 1 && !p->comm) ? p->cluster_C : 0;
   return 0;
 }
 
@@ -392,6 +398,25 @@ static int solve_run(jacobi_plan* p, int64_t max_iter, jacobi::State* fin) {
   return rc;
 }
 
+// Small-n path (NEXT-3): the whole solve in cluster launches of at most kMaxSweepsPerLaunch sweeps.
+static int solve_cluster(jacobi_plan* p, int64_t max_iter, jacobi::State* fin) {
+  p->sweeps_launched = 0;
+  for (int64_t k0 = 1;;) {
+    const int64_t k1 = std::min<int64_t>(k0 + jacobi::kMaxSweepsPerLaunch - 1, max_iter);
+    JCUDA(jacobi::launch_solve_cluster(p->dtype, p->cluster_C, p->cluster_smem, p->dA, p->lda, p->n, p->chunk,
+                                       p->norm, p->diag, p->b, p->x[0], p->x[1], p->st, k0, k1, p->stream));
+    JCUDA(cudaMemcpyAsync(&p->st_host[0], p->st, sizeof(jacobi::State), cudaMemcpyDeviceToHost, p->stream));
+    JCUDA(cudaStreamSynchronize(p->stream));
+    p->sweeps_launched += 1;
+    if (p->st_host[0].done) {
+      *fin = p->st_host[0];
+      return 0;
+    }
+    if (k1 >= max_iter) return jacobi_set_error(JACOBI_ECUDA, "internal: small-n solve ended without a stop decision");
+    k0 = k1 + 1;
+  }
+}
+
 static int solve_impl(jacobi_plan* p, const double* b, const double* x0, bool dev, int64_t max_iter, double tol,
                       double* x_out, int64_t* iters_out, double* hist) {
   if (!p || !b || !x0 || !x_out || !iters_out || max_iter < 0 || std::isnan(tol) || tol < 0)
@@ -418,6 +443,9 @@ static int solve_impl(jacobi_plan* p, const double* b, const double* x0, bool de
   if (rc == 2) {  // max_iter == 0: X^0 (reading R14)
     fin.status = JACOBI_MAX_ITER;
     fin.iters = 0;
+  } else if (p->cluster_C && p->nblocks == 1 && !p->comm) {
+    rc = solve_cluster(p, max_iter, &fin);
+    if (rc) return rc;
   } else {
     rc = solve_run(p, max_iter, &fin);
     if (rc) return rc;

@@ -385,3 +385,28 @@ def test_dist_plan_single_rank_matches_plain_plan(jb):
     with pytest.raises(jb.JacobiError) as e:
         jb.Plan(Z, dist=(jb.nccl_unique_id(), 0, 1))
     assert e.value.status == jb.EZERODIAG and "i = 5" in str(e.value)
+
+
+# ------------------------------------------------------------------ NEXT-3: small-n cluster-resident solver
+@pytest.mark.parametrize("n,f32", [(1, False), (2, False), (37, False), (256, False), (300, True), (600, False)])
+def test_small_n_cluster_path_bitwise(jb, n, f32, monkeypatch):
+    """The one-launch cluster solver (A in shared memory, x through DSMEM) must reproduce the sweep
+    kernels bit for bit: iterates, histories, stop iterations, both norms, and > 4096-sweep runs."""
+    A, b, _ = dominant(n, 5 + n, scale=1.02 if n > 1 else None, f32=f32)
+    x0 = np.random.default_rng(n).uniform(-1, 1, n)
+    runs = [(25, 0.0, "max"), (3000, 1e-12, "max"), (3000, 1e-12, "l2"), (4200, 0.0, "max")]
+    res = {}
+    for small in ("1", "0"):
+        monkeypatch.setenv("JACOBI_SMALL_N", small)
+        with jb.Plan(A) as p:
+            assert (p.info.cluster_ctas > 0) == (small == "1"), p.info.cluster_ctas
+            for mi, tol, norm in runs:
+                p.set_norm(norm)
+                res[(small, mi, tol, norm)] = p.solve(b, x0, mi, tol, history=True)
+    for mi, tol, norm in runs:
+        r1, r0 = res[("1", mi, tol, norm)], res[("0", mi, tol, norm)]
+        assert (r1.status, r1.iters) == (r0.status, r0.iters), (mi, tol, norm)
+        assert np.array_equal(r1.x, r0.x) and np.array_equal(r1.hist, r0.hist), (mi, tol, norm)
+    st_o, x_o, it_o = oracle.jacobi(A, b, x0, 3000, 1e-12)
+    r = res[("1", 3000, 1e-12, "max")]
+    assert (r.status, r.iters) == (st_o, it_o) and rel_linf(r.x, x_o) <= TOL64
