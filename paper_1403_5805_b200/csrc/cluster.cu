@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
   __shared__ unsigned long long s_wmax[kCT / 32];
 
   State* st = a.st;
-  if (*(volatile int32_t*)&st->done) return;  // uniform for the whole cluster
+  if (*(volatile int32_t*)&st->done || st->nonfinite) return;  // uniform for the whole cluster
   const double tol = st->tol;
   const int64_t max_iter = st->max_iter;
   double* hist = st->hist;

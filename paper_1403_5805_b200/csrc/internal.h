@@ -18,6 +18,8 @@ struct State {
   int32_t done;       // stop decided
   int32_t status;     // JACOBI_CONVERGED / JACOBI_MAX_ITER once done
   int64_t iters;      // sweeps performed once done
+  int32_t nonfinite;  // b or x0 held NaN/Inf (set by k_prepare): every sweep is a no-op, solve -> ENONFINITE
+  int32_t pad_;
 };
 
 // Everything a sweep kernel needs; fixed for the life of a plan (captured into CUDA graphs).
@@ -49,7 +51,9 @@ cudaError_t launch_setup_diag(int dtype, const void* A, int64_t lda, int64_t m, 
                               double* diag, unsigned long long* zero_min, cudaStream_t s);
 cudaError_t launch_scan_nonfinite_A(int dtype, const void* A, int64_t lda, int64_t m, int64_t n,
                                     int* flag, cudaStream_t s);
-cudaError_t launch_scan_nonfinite_vec(const double* v, int64_t len, int* flag, cudaStream_t s);
+cudaError_t launch_prepare(State* st, int64_t max_iter, double tol, double* hist, unsigned long long* dslot,
+                           unsigned* cnt, int64_t ncnt, const double* b, int64_t m, const double* x0, int64_t n,
+                           cudaStream_t s);
 cudaError_t launch_copy_pitched(int dtype, const void* src, int64_t src_ld, void* dst, int64_t dst_ld,
                                 int64_t rows, int64_t n, cudaStream_t s);
 int num_variants();

@@ -319,36 +319,22 @@ static int ensure_graph(jacobi_plan* p) {
   return 0;
 }
 
-// Copies inputs in, checks them, and resets the device stop state.  Returns 0, a negative status,
-// or 2 when max_iter == 0 (nothing to run).
+// Copies inputs in and resets the device stop state: two copies, one memset and k_prepare (which
+// also scans b and x0 for NaN/Inf).  No host round trip: ENONFINITE is read with the stop state.
 static int solve_prepare(jacobi_plan* p, const double* b, const double* x0, bool dev, int64_t max_iter, double tol,
                          double* hist_dev) {
   const cudaMemcpyKind kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   JCUDA(cudaMemcpyAsync(p->b, b, (size_t)p->m * 8, kind, p->stream));
   JCUDA(cudaMemcpyAsync(p->x[0], x0, (size_t)p->n * 8, kind, p->stream));
-  JCUDA(cudaMemsetAsync(p->flag_dev, 0, 4, p->stream));
-  JCUDA(jacobi::launch_scan_nonfinite_vec(p->b, p->m, p->flag_dev, p->stream));
-  JCUDA(jacobi::launch_scan_nonfinite_vec(p->x[0], p->n, p->flag_dev, p->stream));
-  if (p->comm) JNCCL(ncclAllReduce(p->flag_dev, p->flag_dev, 1, ncclInt32, ncclMax, p->comm, p->stream));
-  jacobi::State s0{};
-  s0.kbase = 0;
-  s0.max_iter = max_iter;
-  s0.tol = tol;
-  s0.hist = hist_dev;
-  s0.done = 0;
-  s0.status = 0;
-  s0.iters = 0;
-  p->st_host[0] = s0;
-  JCUDA(cudaMemcpyAsync(p->st, &p->st_host[0], sizeof(jacobi::State), cudaMemcpyHostToDevice, p->stream));
-  JCUDA(cudaMemsetAsync(p->dslot, 0, 4 * 8, p->stream));
-  JCUDA(cudaMemsetAsync(p->cnt, 0, (size_t)p->m * 4, p->stream));
-  int nf = 0;
-  JCUDA(cudaMemcpyAsync(&p->st_host[1].status, p->flag_dev, 4, cudaMemcpyDeviceToHost, p->stream));
-  JCUDA(cudaStreamSynchronize(p->stream));
-  nf = p->st_host[1].status;
-  if (nf) return jacobi_set_error(JACOBI_ENONFINITE, "b or x0 contains NaN or Inf");
-  return max_iter == 0 ? 2 : 0;
+  JCUDA(cudaMemsetAsync(p->st, 0, sizeof(jacobi::State), p->stream));
+  JCUDA(jacobi::launch_prepare(p->st, max_iter, tol, hist_dev, p->dslot, p->cnt, p->m, p->b, p->m, p->x[0], p->n,
+                               p->stream));
+  if (p->comm)
+    JNCCL(ncclAllReduce(&p->st->nonfinite, &p->st->nonfinite, 1, ncclInt32, ncclMax, p->comm, p->stream));
+  return 0;
 }
+
+static int nonfinite_error() { return jacobi_set_error(JACOBI_ENONFINITE, "b or x0 contains NaN or Inf"); }
 
 // Runs graph batches until the device decides to stop.  Fills *fin with the final state.
 static int solve_run(jacobi_plan* p, int64_t max_iter, jacobi::State* fin) {
@@ -381,6 +367,10 @@ static int solve_run(jacobi_plan* p, int64_t max_iter, jacobi::State* fin) {
       if (ar != ncclSuccess && ar != ncclInProgress) { rc = jacobi_set_error(JACOBI_ENCCL, ncclGetErrorString(ar)); break; }
     }
     ++waited;
+    if (p->st_host[slot].nonfinite) {
+      rc = nonfinite_error();
+      break;
+    }
     if (p->st_host[slot].done) {
       *fin = p->st_host[slot];
       done = true;
@@ -408,6 +398,7 @@ static int solve_cluster(jacobi_plan* p, int64_t max_iter, jacobi::State* fin) {
     JCUDA(cudaMemcpyAsync(&p->st_host[0], p->st, sizeof(jacobi::State), cudaMemcpyDeviceToHost, p->stream));
     JCUDA(cudaStreamSynchronize(p->stream));
     p->sweeps_launched += 1;
+    if (p->st_host[0].nonfinite) return nonfinite_error();
     if (p->st_host[0].done) {
       *fin = p->st_host[0];
       return 0;
@@ -440,7 +431,10 @@ static int solve_impl(jacobi_plan* p, const double* b, const double* x0, bool de
   int rc = solve_prepare(p, b, x0, dev, max_iter, tol, hist_dev);
   if (rc < 0) return rc;
   jacobi::State fin{};
-  if (rc == 2) {  // max_iter == 0: X^0 (reading R14)
+  if (max_iter == 0) {  // X^0 (reading R14), once the inputs are known to be finite
+    JCUDA(cudaMemcpyAsync(&p->st_host[0], p->st, sizeof(jacobi::State), cudaMemcpyDeviceToHost, p->stream));
+    JCUDA(cudaStreamSynchronize(p->stream));
+    if (p->st_host[0].nonfinite) return nonfinite_error();
     fin.status = JACOBI_MAX_ITER;
     fin.iters = 0;
   } else if (p->cluster_C && p->nblocks == 1 && !p->comm) {
@@ -477,6 +471,9 @@ extern "C" int jacobi_plan_time_sweeps(jacobi_plan* p, const double* d_b, const 
   JCUDA(cudaSetDevice(p->device));
   int rc = solve_prepare(p, d_b, d_x0, true, sweeps, 0.0, nullptr);
   if (rc < 0) return rc;
+  JCUDA(cudaMemcpyAsync(&p->st_host[0], p->st, sizeof(jacobi::State), cudaMemcpyDeviceToHost, p->stream));
+  JCUDA(cudaStreamSynchronize(p->stream));
+  if (p->st_host[0].nonfinite) return nonfinite_error();
   cudaEvent_t e0, e1;
   JCUDA(cudaEventCreate(&e0));
   JCUDA(cudaEventCreate(&e1));

@@ -59,7 +59,7 @@ __device__ __forceinline__ void ld_x(const double* p, double (&v)[E]) {
 // Every CTA evaluates the same inputs and reaches the same decision; only the leader writes.
 __device__ __forceinline__ bool sweep_prologue(const SweepArgs& a, int j, bool leader) {
   State* st = a.st;
-  if (*(volatile int32_t*)&st->done) return false;
+  if (*(volatile int32_t*)&st->done || st->nonfinite) return false;
   const int64_t k = st->kbase + j + 1;
   if (k >= 2) {
     const double d = __longlong_as_double((long long)a.dslot[(k - 1) & 3]);
@@ -363,7 +363,7 @@ __global__ void k_l2_final(const double* __restrict__ blk, int64_t nblk, unsigne
 // After a graph batch of K sweeps: settle the stop decision for the batch's last sweep (same rule
 // as the prologue) and advance the sweep counter.
 __global__ void k_advance(State* st, const unsigned long long* dslot, int K) {
-  if (st->done) return;
+  if (st->done || st->nonfinite) return;
   const int64_t k = st->kbase + K + 1;  // the sweep that would come next
   const double d = __longlong_as_double((long long)dslot[(k - 1) & 3]);
   if (st->hist) st->hist[k - 2] = d;
@@ -401,11 +401,24 @@ __global__ void k_scan_A(const T* __restrict__ A, int64_t lda, int64_t m, int64_
   if (__any_sync(kFull, bad) && lane == 0) *flag = 1;
 }
 
-__global__ void k_scan_vec(const double* __restrict__ v, int64_t len, int* flag) {
+// Solve start (one launch, no host round trip): stop-state parameters, distance slots and tile
+// counters cleared, and the non-finite scan of b and x0 (PAPER.md:59 inputs; ENONFINITE is reported
+// when the host reads the final state).  The state was zeroed by a memset just before.
+__global__ void k_prepare(State* st, int64_t max_iter, double tol, double* hist, unsigned long long* dslot,
+                          unsigned* cnt, int64_t ncnt, const double* __restrict__ b, int64_t m,
+                          const double* __restrict__ x0, int64_t n) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+  if (tid == 0) {
+    st->max_iter = max_iter;
+    st->tol = tol;
+    st->hist = hist;
+  }
+  if (tid < 4) dslot[tid] = 0ull;
+  for (int64_t i = tid; i < ncnt; i += stride) cnt[i] = 0u;
   bool bad = false;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
-    bad |= nonfinite(v[i]);
-  if (bad) *flag = 1;
+  for (int64_t i = tid; i < m; i += stride) bad |= nonfinite(b[i]);
+  for (int64_t i = tid; i < n; i += stride) bad |= nonfinite(x0[i]);
+  if (bad) st->nonfinite = 1;
 }
 
 template <typename T>
@@ -547,9 +560,11 @@ cudaError_t launch_scan_nonfinite_A(int dtype, const void* A, int64_t lda, int64
   return cudaGetLastError();
 }
 
-cudaError_t launch_scan_nonfinite_vec(const double* v, int64_t len, int* flag, cudaStream_t s) {
-  const int grid = (int)std::min<int64_t>((len + 255) / 256, 1024);
-  k_scan_vec<<<grid, 256, 0, s>>>(v, len, flag);
+cudaError_t launch_prepare(State* st, int64_t max_iter, double tol, double* hist, unsigned long long* dslot,
+                           unsigned* cnt, int64_t ncnt, const double* b, int64_t m, const double* x0, int64_t n,
+                           cudaStream_t s) {
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((std::max(n, ncnt) + 255) / 256, 592));
+  k_prepare<<<grid, 256, 0, s>>>(st, max_iter, tol, hist, dslot, cnt, ncnt, b, m, x0, n);
   return cudaGetLastError();
 }
 
