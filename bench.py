@@ -238,7 +238,7 @@ def main():
         for _ in range(args.steps):
             step()
             li = plan.info
-            launches += li.sweeps_launched + li.sweeps_launched // K + 2  # sweeps + k_advance + 2 scans
+            launches += li.sweeps_launched + li.sweeps_launched // K + 1  # sweeps + k_advance + k_prepare
         e1.record(stream)
         torch.cuda.synchronize()
         if world > 1:

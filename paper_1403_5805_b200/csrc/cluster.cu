@@ -23,8 +23,9 @@ namespace jacobi {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kCT = 256;  // threads per CTA
+constexpr int kCT = 512;  // threads per CTA (16 warps: one row per warp for n = 256, C = 16)
 constexpr int kMaxC = 16;
+static_assert(kCT >= kL2Block, "the in-kernel L2 tree uses one thread per row of a block");
 
 template <typename T> struct EOf;
 template <> struct EOf<double> { static constexpr int E = 4; };
@@ -159,7 +160,7 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
       const double* sqk = sq + par * L.n256;
       const int nblk = L.n256 / kL2Block;
       for (int q = 0; q < nblk; ++q) {
-        red[tid] = sqk[q * kL2Block + tid];  // rows >= n hold 0.0
+        if (tid < kL2Block) red[tid] = sqk[q * kL2Block + tid];  // rows >= n hold 0.0
         __syncthreads();
         for (int off = kL2Block / 2; off > 0; off >>= 1) {
           if (tid < off) red[tid] = __dadd_rn(red[tid], red[tid + off]);
@@ -173,9 +174,13 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) t = __dadd_rn(t, __shfl_xor_sync(kFull, t, off));
       d = __dsqrt_rn(t);
-    } else {
-      unsigned long long m = 0ull;
-      for (int q = 0; q < C; ++q) m = dsl[par * kMaxC + q] > m ? dsl[par * kMaxC + q] : m;
+    } else {  // max of the C slots: one load per lane, then a shuffle max
+      unsigned long long m = lane < C ? dsl[par * kMaxC + lane] : 0ull;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(kFull, m, off);
+        m = o > m ? o : m;
+      }
       d = __longlong_as_double((long long)m);
     }
     if (rank == 0 && tid == 0 && hist) hist[k - 1] = d;
