@@ -8,10 +8,12 @@
 //      columns; lane l owns columns c0 + (32 s + l)·E + e, one DFMA chain, shfl_xor butterfly, chunk
 //      sums ascending; diagonal and j >= n skipped — PAPER.md:55), so every bit equals the sweep
 //      kernels' result;
-//   2. stores x_i^(k) into every CTA's copy of x (DSMEM stores, lanes 0..C-1 one peer each) and its
-//      max |dx| bits (or, for the Euclidean rule, dx^2) into every CTA's slot;
-//   3. one cluster barrier; then every CTA evaluates the same stop test: max of the
-//      C slots, or the fixed 256-row tree + strided warp sum of k_l2_partials / k_l2_final.
+//   2. pushes x_i^(k) into every CTA's copy of x (st.async DSMEM stores, lanes 0..C-1 one peer each),
+//      and its max |dx| bits (or, for the Euclidean rule, dx^2) into every CTA's slots; each store
+//      completes transaction bytes on the receiver's mbarrier, so there is no fence and no cluster
+//      barrier per sweep (ncu showed ERRBAR + barrier at ~30 % of the samples with plain stores);
+//   3. once its mbarrier phase completes, every CTA evaluates the same stop test:
+//      max of the C slots, or the fixed 256-row tree + strided warp sum of k_l2_partials/k_l2_final.
 // A launch runs at most kMaxSweepsPerLaunch sweeps and writes x and the stop state back, so long
 // runs stay interruptible; the next launch resumes from global x.
 #include "internal.h"
@@ -54,6 +56,32 @@ __host__ __device__ inline Layout layout(int n, int C, int esz) {
   return L;
 }
 
+// DSMEM push with completion on the receiver's mbarrier (no fence, no cluster barrier per sweep).
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ unsigned mapa(unsigned laddr, int rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(laddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_b64(unsigned raddr, unsigned long long v, unsigned rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr), "l"(v),
+               "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init_local(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n W_%=: mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W_%=;\n}" ::"r"(smem_addr(b)),
+      "r"(parity)
+      : "memory");
+}
+
 struct ClusterArgs {
   const void* A;
   int64_t lda;
@@ -82,6 +110,7 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
   double* red = reinterpret_cast<double*>(sm + L.red_off);
   double* blk = reinterpret_cast<double*>(sm + L.blk_off);
   __shared__ unsigned long long s_wmax[kCT / 32];
+  __shared__ __align__(8) uint64_t s_full[2];  // per parity: x^(k), the C maxima (and dx^2) have landed
 
   State* st = a.st;
   if (*(volatile int32_t*)&st->done || st->nonfinite) return;  // uniform for the whole cluster
@@ -101,7 +130,15 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
   const double* xg = p0 ? a.x1buf : a.x0buf;
   for (int i = tid; i < L.xlen; i += kCT) xs[p0 * L.xlen + i] = i < n ? xg[i] : 0.0;
   for (int i = tid; i < 2 * L.n256; i += kCT) sq[i] = 0.0;
-  cl.sync();
+  if (tid == 0) {
+    mbar_init_local(&s_full[0], 1);
+    mbar_init_local(&s_full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  cl.sync();  // every CTA's barriers and buffers are ready before the first remote store
+  // bytes that land in each CTA per sweep: all n values of x^(k), C maxima, and n dx^2 for L2
+  const unsigned tx_bytes = (unsigned)(8 * n + 8 * C + (a.norm == JACOBI_NORM_L2 ? 8 * n : 0));
+  unsigned phase[2] = {0u, 0u};
 
   const int nsteps = a.chunk / (32 * E);
   int stop = 0;  // 1 converged, 2 iteration limit
@@ -109,6 +146,7 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
   for (; k <= k1; ++k) {
     const int par = (int)(k & 1);
     const double* xo = xs + (1 - par) * L.xlen;
+    if (tid == 0) mbar_expect(&s_full[par], tx_bytes);
     unsigned long long dmax = 0ull;
     for (int r = warp; r < nr; r += kCT / 32) {
       const int grow = r_begin + r;
@@ -133,13 +171,13 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
       }
       const double xnew = __ddiv_rn(__dsub_rn(a.b[grow], s), a.diag[grow]);
       const double dx = __dsub_rn(xnew, xo[grow]);
-      if (lane < C) {
-        double* px = cl.map_shared_rank(xs + par * L.xlen, lane);
-        px[grow] = xnew;
-        if (a.norm == JACOBI_NORM_L2) {
-          double* ps = cl.map_shared_rank(sq + par * L.n256, lane);
-          ps[grow] = __dmul_rn(dx, dx);
-        }
+      if (lane < C) {  // lane q pushes x_i^(k) (and dx^2) into CTA q
+        const unsigned rbar = mapa(smem_addr(&s_full[par]), lane);
+        st_async_b64(mapa(smem_addr(xs + par * L.xlen + grow), lane), (unsigned long long)__double_as_longlong(xnew),
+                     rbar);
+        if (a.norm == JACOBI_NORM_L2)
+          st_async_b64(mapa(smem_addr(sq + par * L.n256 + grow), lane),
+                       (unsigned long long)__double_as_longlong(__dmul_rn(dx, dx)), rbar);
       }
       const unsigned long long bits = (unsigned long long)__double_as_longlong(dx) & 0x7fffffffffffffffull;
       dmax = bits > dmax ? bits : dmax;
@@ -150,10 +188,10 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
       unsigned long long m = 0ull;
 #pragma unroll
       for (int w = 0; w < kCT / 32; ++w) m = s_wmax[w] > m ? s_wmax[w] : m;
-      unsigned long long* pd = cl.map_shared_rank(dsl + par * kMaxC, tid);
-      pd[rank] = m;
+      st_async_b64(mapa(smem_addr(dsl + par * kMaxC + rank), tid), m, mapa(smem_addr(&s_full[par]), tid));
     }
-    cl.sync();  // x^(k), the maxima and dx^2 of every row are visible in every CTA
+    mbar_wait_cluster(&s_full[par], phase[par]);  // x^(k), the maxima and dx^2 of every row have landed
+    phase[par] ^= 1u;
 
     double d;
     if (a.norm == JACOBI_NORM_L2) {  // identical arithmetic to k_l2_partials + k_l2_final
