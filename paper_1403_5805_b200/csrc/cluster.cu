@@ -74,9 +74,11 @@ __device__ __forceinline__ void mbar_init_local(uint64_t* b, unsigned count) {
 __device__ __forceinline__ void mbar_expect(uint64_t* b, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
 }
+// Default (.acquire.cta) semantics, as for TMA-multicast data: the st.async bytes are visible once
+// the phase completes; a .cluster-scope acquire would add an L1 invalidate (CCTL.IVALL) per sweep.
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, unsigned parity) {
   asm volatile(
-      "{\n .reg .pred p;\n W_%=: mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "{\n .reg .pred p;\n W_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra W_%=;\n}" ::"r"(smem_addr(b)),
       "r"(parity)
       : "memory");
