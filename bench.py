@@ -269,34 +269,52 @@ def main():
     del dA, db
     torch.cuda.empty_cache()
 
-    # ---- e2e through the public C-ABI with host buffers (pinned), copies inside the timed region
+    # ---- e2e through the public C-ABI with host buffers (pinned), copies inside the timed region.
+    # N = 1: the one-shot jacobi_solve (north-star signature).  N > 1: per step every rank creates a
+    # distributed plan from its host row block (H2D inside), solves from host b / x0 and reads x back.
     e2e = None
-    if not args.no_e2e and world == 1 and args.e2e_steps > 0:
-        hA = torch.empty((n, n), dtype=dt, pin_memory=True)
-        g.host_rows(cfg, 0, n, out=hA.numpy())
-        hb = torch.empty(n, dtype=torch.float64, pin_memory=True)
-        hb.numpy()[:] = g.host_diag_b(cfg, 0, n)[1]
+    if not args.no_e2e and args.e2e_steps > 0:
+        import ctypes
+        hA = torch.empty((m, n), dtype=dt, pin_memory=True)
+        g.host_rows(cfg, row0, row0 + m, out=hA.numpy())
+        hb = torch.empty(m, dtype=torch.float64, pin_memory=True)
+        hb.numpy()[:] = g.host_diag_b(cfg, row0, row0 + m)[1]
         hx0 = torch.zeros(n, dtype=torch.float64, pin_memory=True)
         hx = torch.empty(n, dtype=torch.float64, pin_memory=True)
         solve_fn = jb._lib.jacobi_solve_f32a if cfg.a_dtype == g.F32 else jb._lib.jacobi_solve
-        import ctypes
         it = ctypes.c_int64()
 
         def e2e_step():
-            st = solve_fn(n, hA.data_ptr(), hb.data_ptr(), hx0.data_ptr(), sweeps, tol, hx.data_ptr(), ctypes.byref(it))
-            assert st == jb.MAX_ITER and it.value == sweeps, (st, jb.last_error())
+            if world == 1:
+                st = solve_fn(n, hA.data_ptr(), hb.data_ptr(), hx0.data_ptr(), sweeps, tol, hx.data_ptr(),
+                              ctypes.byref(it))
+                assert st == jb.MAX_ITER and it.value == sweeps, (st, jb.last_error())
+            else:
+                from paper_1403_5805_b200.dist import dist_plan
+                with dist_plan(hA.numpy(), n) as p:
+                    r = p.solve(hb.numpy(), hx0.numpy(), sweeps, tol)
+                    assert r.status == jb.MAX_ITER and r.iters == sweeps
 
         e2e_step()  # warm-up
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             e2e_step()
         torch.cuda.synchronize()
         el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
         e2e = {"value": args.e2e_steps * sweeps / el, "unit": "it/s",
-               "h2d_bytes_per_step": int(hA.numel() * hA.element_size() + 2 * 8 * n),
-               "d2h_bytes_per_step": int(8 * n + 48), "steps": args.e2e_steps,
-               "api": "jacobi_solve (C-ABI, host pinned buffers; plan setup + H2D + sweeps + D2H per step)"}
+               "h2d_bytes_per_step": int(world * (hA.numel() * hA.element_size() + 8 * m + 8 * n)),
+               "d2h_bytes_per_step": int(world * (8 * n + 48)), "steps": args.e2e_steps,
+               "api": ("jacobi_solve (C-ABI one-shot, host pinned buffers: plan setup + H2D + sweeps + D2H per step)"
+                       if world == 1 else
+                       "jacobi_dist_plan_create + jacobi_plan_solve per step on every rank (host row block, H2D, "
+                       "NCCL comm init, sweeps, D2H); wall time, max over ranks")}
         del hA
 
     cpu = None
@@ -318,7 +336,7 @@ def main():
             "effective_gbs_per_gpu": achieved, "effective_gbs_aggregate": achieved * world,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(args.workload),
-                         "peak_source": peak_src, "kernel": f"k_sweep<{'double' if dt == torch.float64 else 'float'},R={info.rows_per_warp}>",
+                         "peak_source": peak_src, "kernel": f"{jb.VARIANT_NAMES[info.variant]} ({'fp64' if dt == torch.float64 else 'fp32'} A)",
                          "bytes_per_launch": bytes_sweep, "avg_launch_ms": sweep_ms,
                          "kernel_only_ms": kernel_ms, "kernel_only_gbs": bytes_sweep / (kernel_ms * 1e-3) / 1e9,
                          "read_ceiling_gbs": ceiling,

@@ -33,6 +33,12 @@ EXPORTS = ("jacobi_solve", "jacobi_solve_f32a", "jacobi_plan_create", "jacobi_pl
            "jacobi_version")
 
 
+# Sweep kernel variants compiled into libjacobi.so (csrc/sweep.cu kVariants; all bitwise identical).
+VARIANT_NAMES = ("k_sweep R4 U2", "k_sweep R8 U1", "k_sweep R2 U4", "k_sweep R4 U1", "k_sweep R4 U2 256t",
+                 "k_sweep R2 U1 1024t", "k_sweep_cta R8 U1", "k_sweep_cta R4 U1", "k_sweep_cta R8 U1 256t",
+                 "k_sweep_cta R4 U2", "k_sweep_cta R2 U4")
+
+
 class JacobiError(RuntimeError):
     def __init__(self, status, msg):
         super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
