@@ -457,21 +457,22 @@ __global__ void k_fill(double* buf, int64_t n) {
 // chosen from measurements (profiles/), others stay selectable with JACOBI_SWEEP_VARIANT for tuning.
 struct Variant {
   int R, threads, cta;  // cta = 1: k_sweep_cta (needs nchunks >= threads/32 and its partial slots)
+  int u64, u32;         // steps in flight (fp64 / fp32 instance): the chunk must be a multiple of 32*E*U
   void (*f64)(const SweepArgs, const int);
   void (*f32)(const SweepArgs, const int);
 };
 const Variant kVariants[] = {
-    {4, 512, 0, k_sweep<double, 4, 2, 512>, k_sweep<float, 4, 1, 512>},
-    {8, 512, 0, k_sweep<double, 8, 1, 512>, k_sweep<float, 8, 1, 512>},
-    {2, 512, 0, k_sweep<double, 2, 4, 512>, k_sweep<float, 2, 2, 512>},
-    {4, 512, 0, k_sweep<double, 4, 1, 512>, k_sweep<float, 4, 2, 512>},
-    {4, 256, 0, k_sweep<double, 4, 2, 256>, k_sweep<float, 4, 1, 256>},
-    {2, 1024, 0, k_sweep<double, 2, 1, 1024>, k_sweep<float, 2, 1, 1024>},
-    {8, 512, 1, k_sweep_cta<double, 8, 16>, k_sweep_cta<float, 8, 16>},
-    {4, 512, 1, k_sweep_cta<double, 4, 16>, k_sweep_cta<float, 4, 16>},
-    {8, 256, 1, k_sweep_cta<double, 8, 8>, k_sweep_cta<float, 4, 8>},
-    {4, 512, 1, k_sweep_cta<double, 4, 16, 2>, k_sweep_cta<float, 4, 16, 2>},
-    {2, 512, 1, k_sweep_cta<double, 2, 16, 4>, k_sweep_cta<float, 2, 16, 2>},
+    {4, 512, 0, 2, 1, k_sweep<double, 4, 2, 512>, k_sweep<float, 4, 1, 512>},
+    {8, 512, 0, 1, 1, k_sweep<double, 8, 1, 512>, k_sweep<float, 8, 1, 512>},
+    {2, 512, 0, 4, 2, k_sweep<double, 2, 4, 512>, k_sweep<float, 2, 2, 512>},
+    {4, 512, 0, 1, 2, k_sweep<double, 4, 1, 512>, k_sweep<float, 4, 2, 512>},
+    {4, 256, 0, 2, 1, k_sweep<double, 4, 2, 256>, k_sweep<float, 4, 1, 256>},
+    {2, 1024, 0, 1, 1, k_sweep<double, 2, 1, 1024>, k_sweep<float, 2, 1, 1024>},
+    {8, 512, 1, 1, 1, k_sweep_cta<double, 8, 16>, k_sweep_cta<float, 8, 16>},
+    {4, 512, 1, 1, 1, k_sweep_cta<double, 4, 16>, k_sweep_cta<float, 4, 16>},
+    {8, 256, 1, 1, 1, k_sweep_cta<double, 8, 8>, k_sweep_cta<float, 4, 8>},
+    {4, 512, 1, 2, 2, k_sweep_cta<double, 4, 16, 2>, k_sweep_cta<float, 4, 16, 2>},
+    {2, 512, 1, 4, 2, k_sweep_cta<double, 2, 16, 4>, k_sweep_cta<float, 2, 16, 2>},
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
@@ -486,6 +487,8 @@ size_t variant_smem(int v, int nchunks, int /*dtype*/, int /*chunk*/) {
 }
 bool variant_fits(int v, int nchunks, int dtype, int chunk) {
   const Variant& V = kVariants[v];
+  const int step_cols = 32 * (dtype == JACOBI_F32 ? 8 : 4) * (dtype == JACOBI_F32 ? V.u32 : V.u64);
+  if (chunk % step_cols != 0) return false;
   return !V.cta || (nchunks >= V.threads / 32 && variant_smem(v, nchunks, dtype, chunk) <= 48 * 1024);
 }
 int variant_rows_dt(int v, int /*dtype*/) { return kVariants[v].R; }
@@ -496,17 +499,17 @@ int variant_rows_dt(int v, int /*dtype*/) { return kVariants[v].R; }
 int default_variant(int dtype, int nchunks, int chunk) {
   const int big = dtype == JACOBI_F32 ? 7 : 9;
   if (variant_fits(big, nchunks, dtype, chunk)) return big;
-  return dtype == JACOBI_F32 ? 0 : 1;
+  return dtype == JACOBI_F32 ? 0 : 1;  // U = 1: fits every chunk
 }
 int variant_rows(int v) { return kVariants[v].R; }
 int variant_threads(int v) { return kVariants[v].threads; }
 
 int chunk_for(int64_t n, int dtype) {
   // 8 KB of row data per chunk (1024 fp64 / 2048 fp32 columns) when n has >= 16 such chunks, halved
-  // down to 512 columns otherwise.  A function of (n, dtype) only, so every rank count and every
-  // kernel variant sums each row in the same order.
+  // down to 256 columns otherwise (c2, n = 4096: 16 chunks of 256).  A function of (n, dtype) only,
+  // so every rank count and every kernel variant sums each row in the same order.
   int c = dtype == JACOBI_F32 ? 2048 : 1024;
-  while (c > 512 && (int64_t)c * 16 > n) c /= 2;
+  while (c > 256 && (int64_t)c * 16 > n) c /= 2;
   return c;
 }
 
