@@ -135,6 +135,20 @@ int jacobi_dist_plan_create(jacobi_plan** out, const void* uid128, int rank, int
                             int dtype, const void* A_rows, int64_t lda, int a_on_device,
                             void* cuda_stream);
 
+/* Column-wise distribution (§3.2; NEXT-4 comparison scheme): rank r passes the
+ * n x m column slab A_cols (rows 0..n-1, columns [r*m, (r+1)*m), lda >= m).  Each sweep computes the
+ * slab's partial row sums for all n rows from the rank's own x slice, a reduce-scatter (sum, the
+ * "MPI_Allreduce ... MPI_SUM" of PAPER.md:100 restricted to the rows each rank finalizes) gives rank
+ * r the sums of rows [r*m, (r+1)*m), and the epilogue updates that slice — the only part of x the
+ * rank needs next sweep, so x is allgathered once, at the end.  The rank-sum order is NCCL's, so
+ * results are NOT bitwise independent of P (they are within the parity tolerance). */
+int jacobi_dist_plan_create_colwise(jacobi_plan** out, const void* uid128, int rank, int nranks, int64_t n,
+                                    int dtype, const void* A_cols, int64_t lda, int a_on_device,
+                                    void* cuda_stream);
+/* Test hook: emulate a P-slab column-wise sweep on one GPU (P | n): P slab launches write row sums,
+ * and the epilogue adds the P partials in slab order.  Exercises the slab kernels with col0 > 0. */
+int jacobi_plan_set_col_blocks(jacobi_plan* plan, int nblocks);
+
 /* ------------------------------------------------------------------ measurement */
 /* Read-only HBM ceiling: streams `nbytes` of device memory with the sweep kernel's load flavour
  * (256-bit, L1::no_allocate) and returns the best GB/s of `reps` timed passes. */

@@ -29,7 +29,8 @@ STATUS_NAMES = {0: "CONVERGED", 1: "MAX_ITER", -1: "EINVAL", -2: "EZERODIAG", -3
 EXPORTS = ("jacobi_solve", "jacobi_solve_f32a", "jacobi_plan_create", "jacobi_plan_solve",
            "jacobi_plan_solve_device", "jacobi_plan_destroy", "jacobi_plan_set_row_blocks",
            "jacobi_plan_set_batch", "jacobi_plan_set_norm", "jacobi_plan_info", "jacobi_plan_time_sweeps", "jacobi_partition",
-           "jacobi_nccl_unique_id", "jacobi_dist_plan_create", "jacobi_bwprobe", "jacobi_last_error",
+           "jacobi_nccl_unique_id", "jacobi_dist_plan_create", "jacobi_dist_plan_create_colwise",
+           "jacobi_plan_set_col_blocks", "jacobi_bwprobe", "jacobi_last_error",
            "jacobi_version")
 
 
@@ -76,6 +77,8 @@ def _load():
         "jacobi_partition": ([i64, i32, i32, P(i64), P(i64)], i32),
         "jacobi_nccl_unique_id": ([vp], i32),
         "jacobi_dist_plan_create": ([P(vp), vp, i32, i32, i64, i32, vp, i64, i32, vp], i32),
+        "jacobi_dist_plan_create_colwise": ([P(vp), vp, i32, i32, i64, i32, vp, i64, i32, vp], i32),
+        "jacobi_plan_set_col_blocks": ([vp, i32], i32),
         "jacobi_bwprobe": ([i64, i32, P(dbl)], i32),
         "jacobi_last_error": ([], ctypes.c_char_p),
         "jacobi_version": ([], i32),
@@ -152,9 +155,10 @@ class Plan:
     """A resident system (``jacobi_plan_create`` / ``jacobi_dist_plan_create``).
 
     A: numpy array (host; copied) or torch CUDA tensor (device; borrowed, must outlive the plan).
-    For a distributed plan pass ``dist=(uid_bytes, rank, nranks)`` and A = this rank's row block."""
+    For a distributed plan pass ``dist=(uid_bytes, rank, nranks)`` and A = this rank's row block
+    (``layout="rows"``, §3.1) or its n x m column slab (``layout="cols"``, §3.2)."""
 
-    def __init__(self, A, n=None, lda=None, stream=None, dist=None):
+    def __init__(self, A, n=None, lda=None, stream=None, dist=None, layout="rows"):
         on_dev = _is_torch_cuda(A)
         if on_dev:
             dt = str(A.dtype)
@@ -181,8 +185,9 @@ class Plan:
         else:
             uid, rank, nranks = dist
             ub = ctypes.create_string_buffer(bytes(uid), 128)
-            _check(_lib.jacobi_dist_plan_create(ctypes.byref(h), ub, int(rank), int(nranks), self.n, self.dtype,
-                                                ctypes.c_void_p(ptr), lda, int(on_dev), s))
+            create = {"rows": _lib.jacobi_dist_plan_create, "cols": _lib.jacobi_dist_plan_create_colwise}[layout]
+            _check(create(ctypes.byref(h), ub, int(rank), int(nranks), self.n, self.dtype, ctypes.c_void_p(ptr), lda,
+                          int(on_dev), s))
         self._h = h
 
     def close(self):
@@ -210,6 +215,9 @@ class Plan:
 
     def set_row_blocks(self, nblocks):
         _check(_lib.jacobi_plan_set_row_blocks(self._h, int(nblocks)))
+
+    def set_col_blocks(self, nblocks):
+        _check(_lib.jacobi_plan_set_col_blocks(self._h, int(nblocks)))
 
     def set_norm(self, norm):
         """'max' (north_star, default) or 'l2' (the paper's Euclidean distance)."""

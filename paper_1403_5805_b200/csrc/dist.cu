@@ -29,19 +29,27 @@ extern "C" int jacobi_nccl_unique_id(void* out128) {
   return 0;
 }
 
-extern "C" int jacobi_dist_plan_create(jacobi_plan** out, const void* uid128, int rank, int nranks, int64_t n,
-                                       int dtype, const void* A_rows, int64_t lda, int a_on_device,
-                                       void* cuda_stream) {
-  if (!out || !uid128 || !A_rows || n < 1 || lda < n || nranks < 1 || rank < 0 || rank >= nranks ||
+static int dist_create(jacobi_plan** out, const void* uid128, int rank, int nranks, int64_t n, int dtype,
+                       const void* A_block, int64_t lda, int a_on_device, void* cuda_stream, bool colwise) {
+  const char* fn = colwise ? "jacobi_dist_plan_create_colwise" : "jacobi_dist_plan_create";
+  if (!out || !uid128 || !A_block || n < 1 || nranks < 1 || rank < 0 || rank >= nranks ||
       (dtype != JACOBI_F64 && dtype != JACOBI_F32))
-    return jacobi_set_error(JACOBI_EINVAL, "jacobi_dist_plan_create: bad argument");
+    return jacobi_set_error(JACOBI_EINVAL, std::string(fn) + ": bad argument");
   int64_t row0 = 0, m = 0;
   int rc = jacobi_partition(n, nranks, rank, &row0, &m);
   if (rc) return rc;
+  if (lda < (colwise ? m : n)) return jacobi_set_error(JACOBI_EINVAL, std::string(fn) + ": lda too small");
   jacobi_plan* p = new jacobi_plan();
   p->rank = rank;
   p->nranks = nranks;
-  rc = plan_init_common(p, n, m, row0, dtype, A_rows, lda, a_on_device, cuda_stream);
+  p->colwise = colwise;
+  rc = colwise ? plan_init_common(p, n, m, row0, dtype, A_block, n, m, lda, a_on_device, cuda_stream)
+               : plan_init_common(p, n, m, row0, dtype, A_block, m, n, lda, a_on_device, cuda_stream);
+  if (rc == 0 && colwise) {
+    cudaError_t e = cudaMalloc(&p->rsum, (size_t)n * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&p->rs_own, (size_t)m * 8);
+    if (e != cudaSuccess) rc = jacobi_set_error(JACOBI_ENOMEM, std::string("column-wise buffers: ") + cudaGetErrorString(e));
+  }
   if (rc == 0) {
     ncclUniqueId id;
     std::memcpy(&id, uid128, sizeof(id));
@@ -65,4 +73,16 @@ extern "C" int jacobi_dist_plan_create(jacobi_plan** out, const void* uid128, in
   }
   *out = p;
   return 0;
+}
+
+extern "C" int jacobi_dist_plan_create(jacobi_plan** out, const void* uid128, int rank, int nranks, int64_t n,
+                                       int dtype, const void* A_rows, int64_t lda, int a_on_device,
+                                       void* cuda_stream) {
+  return dist_create(out, uid128, rank, nranks, n, dtype, A_rows, lda, a_on_device, cuda_stream, false);
+}
+
+extern "C" int jacobi_dist_plan_create_colwise(jacobi_plan** out, const void* uid128, int rank, int nranks,
+                                               int64_t n, int dtype, const void* A_cols, int64_t lda,
+                                               int a_on_device, void* cuda_stream) {
+  return dist_create(out, uid128, rank, nranks, n, dtype, A_cols, lda, a_on_device, cuda_stream, true);
 }

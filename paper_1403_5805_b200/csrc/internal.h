@@ -37,6 +37,9 @@ struct SweepArgs {
   unsigned* cnt;            // per row-tile arrival counters (reset by the finalizing warp)
   unsigned long long* dslot;// 4-slot ring of max|dx| bit patterns; sweep k uses slot k & 3
   State* st;
+  int64_t col0, cend;       // column range of A held here: [0, n) row-wise; a slab column-wise (NEXT-4)
+  double* rsum;             // non-null: write the row sums over [col0, cend) to rsum[row] (column-wise
+                            // partial products) instead of applying the epilogue
   double* sq;               // norm == L2: (x_i^(k) - x_i^(k-1))^2 of the launch's rows
   int norm;                 // JACOBI_NORM_MAX / JACOBI_NORM_L2
   int chunk;                // columns per work item (multiple of 512, depends on n only)
@@ -65,6 +68,11 @@ int variant_rows(int variant);
 int variant_threads(int variant);
 int sweep_grid(int dtype, int variant, int num_sms, int nchunks, int chunk);
 int chunk_for(int64_t n, int dtype);
+// Column-wise epilogue (NEXT-4): s_i = sum over nb partial blocks (ascending), then x_i^(k), |dx|.
+cudaError_t launch_colsum_epilogue(const double* rsum, int nb, int64_t stride, int64_t rows, int64_t row0,
+                                   const double* b, const double* diag, double* x0buf, double* x1buf,
+                                   unsigned long long* dslot, double* sq, int norm, State* st, int j,
+                                   cudaStream_t s);
 // cluster.cu (NEXT-3 small-n solver)
 int cluster_plan(int64_t n, int dtype, size_t* smem);
 cudaError_t launch_solve_cluster(int dtype, int C, size_t smem, const void* A, int64_t lda, int64_t n, int chunk,
@@ -82,9 +90,15 @@ double bwprobe(int64_t nbytes, int reps);
 // The opaque plan of jacobi.h.
 struct jacobi_plan {
   int64_t n = 0, lda = 0, m = 0, row0 = 0;
+  int64_t a_rows = 0, a_cols = 0;  // stored block of A: m x n (row-wise) or n x m (column slab)
   int dtype = JACOBI_F64, rank = 0, nranks = 1;
   int device = 0, num_sms = 0, grid = 0;
   int nblocks = 1;               // P12(a) row-block emulation
+  bool colwise = false;          // NEXT-4: this rank holds the n x m column slab [row0, row0 + m)
+  int colblocks = 1;             // 1-GPU emulation of a P-slab column-wise sweep (test hook)
+  double* rsum = nullptr;        // column-wise row sums: colblocks x n (emulation) or n (distributed)
+  double* rs_own = nullptr;      // distributed column-wise: reduce-scatter output (m)
+  int gemv_variant = 0, gemv_grid = 0;  // kernel for the emulated column slabs
   int variant = 0;               // sweep kernel variant (R, U, threads); default per dtype, JACOBI_SWEEP_VARIANT overrides
   int batch = 32;                // sweeps per graph batch
   int norm = JACOBI_NORM_MAX;    // distance of the stop test
@@ -113,7 +127,7 @@ struct jacobi_plan {
   unsigned long long* zmin_dev = nullptr;
   ncclComm_t comm = nullptr;     // distributed plans only
   cudaGraphExec_t graph = nullptr;
-  int graph_batch = 0, graph_nblocks = 0, graph_norm = -1;
+  int graph_batch = 0, graph_nblocks = 0, graph_norm = -1, graph_colblocks = 0;
   int64_t sweeps_launched = 0;
   int chunk = 0;
 };
@@ -127,6 +141,11 @@ int jacobi_set_error(int code, const std::string& msg);
       return jacobi_set_error(_e == cudaErrorMemoryAllocation ? JACOBI_ENOMEM : JACOBI_ECUDA,   \
                               std::string(#call) + ": " + cudaGetErrorString(_e));              \
   } while (0)
+#define JRC(call)                                                                               \
+  do {                                                                                          \
+    int _rc = (call);                                                                           \
+    if (_rc) return _rc;                                                                        \
+  } while (0)
 #define JNCCL(call)                                                                             \
   do {                                                                                          \
     ncclResult_t _r = (call);                                                                   \
@@ -136,5 +155,5 @@ int jacobi_set_error(int code, const std::string& msg);
 
 // Shared by plan.cu / dist.cu
 int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dtype, const void* A,
-                     int64_t lda, int a_on_device, void* stream);
+                     int64_t a_rows, int64_t a_cols, int64_t lda, int a_on_device, void* stream);
 int plan_validate_A(jacobi_plan* p, unsigned long long* zero_row, int* nonfinite);

@@ -39,9 +39,9 @@ static int plan_free(jacobi_plan* p) {
   if (p->graph) chk(cudaGraphExecDestroy(p->graph), "cudaGraphExecDestroy");
   if (p->comm) ncclCommDestroy(p->comm);
   void* dev[] = {p->dA_owned, p->diag, p->b, p->x[0], p->x[1], p->part, p->cnt, p->dslot, p->st,
-                 p->hist_dev, p->flag_dev, p->zmin_dev, p->sq, p->blk, p->blk_all};
+                 p->hist_dev, p->flag_dev, p->zmin_dev, p->sq, p->blk, p->blk_all, p->rsum, p->rs_own};
   const char* names[] = {"A", "diag", "b", "x0", "x1", "part", "cnt", "dslot", "state", "hist", "flag", "zmin",
-                         "sq", "blk", "blk_all"};
+                         "sq", "blk", "blk_all", "rsum", "rs_own"};
   for (size_t i = 0; i < sizeof(dev) / sizeof(dev[0]); ++i)
     if (dev[i]) chk(cudaFree(dev[i]), names[i]);
   if (p->st_host) chk(cudaFreeHost(p->st_host), "cudaFreeHost(state)");
@@ -64,13 +64,30 @@ static int check_last(const char* what) {
     if (_rc) return _rc;             \
   } while (0)
 
-int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dtype, const void* A, int64_t lda,
-                     int a_on_device, void* stream) {
+// Sweep-kernel variant for a GEMV over `ncols` columns (default from measurements; the
+// JACOBI_SWEEP_VARIANT override is honoured when the variant can tile the chunking).
+static void choose_variant(const jacobi_plan* p, int64_t ncols, int* variant, int* grid) {
+  const int nch = (int)((ncols + p->chunk - 1) / p->chunk);
+  int v = jacobi::default_variant(p->dtype, nch, p->chunk);
+  if (const char* e = getenv("JACOBI_SWEEP_VARIANT")) {  // tuning override (all variants: same bits)
+    const int vi = atoi(e);
+    if (vi >= 0 && vi < jacobi::num_variants() && jacobi::variant_fits(vi, nch, p->dtype, p->chunk)) v = vi;
+  }
+  *variant = v;
+  *grid = jacobi::sweep_grid(p->dtype, v, p->num_sms, nch, p->chunk);
+}
+
+// Common plan setup.  The stored block of A is a_rows x a_cols (row-major, lda): the m x n row block
+// (row-wise) or the n x m column slab [row0, row0 + m) (column-wise, NEXT-4).
+int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dtype, const void* A, int64_t a_rows,
+                     int64_t a_cols, int64_t lda, int a_on_device, void* stream) {
   JLAST("pending CUDA error before plan creation");
   p->n = n;
   p->m = m;
   p->row0 = row0;
   p->dtype = dtype;
+  p->a_rows = a_rows;
+  p->a_cols = a_cols;
   JCUDA(cudaGetDevice(&p->device));
   JCUDA(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, p->device));
   int major = 0;
@@ -83,43 +100,37 @@ int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dty
     p->own_stream = true;
   }
   const int64_t elt = dtype == JACOBI_F32 ? 4 : 8;
-  const int64_t lda_dev = round_up(n, 8);
+  const int64_t lda_dev = round_up(a_cols, 8);
   if (a_on_device && ((uintptr_t)A % 32 == 0) && lda % 8 == 0) {
     p->dA = A;
     p->lda = lda;
     p->a_borrowed = true;
   } else {
-    JCUDA(cudaMalloc(&p->dA_owned, (size_t)(m * lda_dev * elt)));
+    JCUDA(cudaMalloc(&p->dA_owned, (size_t)(a_rows * lda_dev * elt)));
     p->lda = lda_dev;
     p->dA = p->dA_owned;
     if (a_on_device) {
-      JCUDA(jacobi::launch_copy_pitched(dtype, A, lda, p->dA_owned, lda_dev, m, n, p->stream));
+      JCUDA(jacobi::launch_copy_pitched(dtype, A, lda, p->dA_owned, lda_dev, a_rows, a_cols, p->stream));
     } else if (lda == lda_dev) {
-      JCUDA(cudaMemcpyAsync(p->dA_owned, A, (size_t)(m * lda * elt), cudaMemcpyHostToDevice, p->stream));
+      JCUDA(cudaMemcpyAsync(p->dA_owned, A, (size_t)(a_rows * lda * elt), cudaMemcpyHostToDevice, p->stream));
     } else {
-      JCUDA(cudaMemsetAsync(p->dA_owned, 0, (size_t)(m * lda_dev * elt), p->stream));
-      JCUDA(cudaMemcpy2DAsync(p->dA_owned, (size_t)(lda_dev * elt), A, (size_t)(lda * elt), (size_t)(n * elt),
-                              (size_t)m, cudaMemcpyHostToDevice, p->stream));
+      JCUDA(cudaMemsetAsync(p->dA_owned, 0, (size_t)(a_rows * lda_dev * elt), p->stream));
+      JCUDA(cudaMemcpy2DAsync(p->dA_owned, (size_t)(lda_dev * elt), A, (size_t)(lda * elt), (size_t)(a_cols * elt),
+                              (size_t)a_rows, cudaMemcpyHostToDevice, p->stream));
     }
   }
-  p->chunk = jacobi::chunk_for(n, dtype);
-  const int nch = (int)((n + p->chunk - 1) / p->chunk);
-  p->variant = jacobi::default_variant(dtype, nch, p->chunk);
-  if (const char* v = getenv("JACOBI_SWEEP_VARIANT")) {  // tuning override (all variants: same bits)
-    int vi = atoi(v);
-    if (vi >= 0 && vi < jacobi::num_variants() && jacobi::variant_fits(vi, nch, dtype, p->chunk)) p->variant = vi;
-  }
   JLAST("A upload");
-  p->grid = jacobi::sweep_grid(dtype, p->variant, p->num_sms, nch, p->chunk);
+  p->chunk = jacobi::chunk_for(n, dtype);
+  choose_variant(p, a_cols, &p->variant, &p->grid);
   JLAST("sweep kernel occupancy query");
   p->x_len = round_up(n, 256) + 256;
-  const int64_t nchunks = (n + p->chunk - 1) / p->chunk;
+  const int64_t nchunks = (a_cols + p->chunk - 1) / p->chunk;
   JCUDA(cudaMalloc(&p->diag, (size_t)m * 8));
   JCUDA(cudaMalloc(&p->b, (size_t)m * 8));
   JCUDA(cudaMalloc(&p->x[0], (size_t)p->x_len * 8));
   JCUDA(cudaMalloc(&p->x[1], (size_t)p->x_len * 8));
-  JCUDA(cudaMalloc(&p->part, (size_t)(nchunks * m) * 8));
-  JCUDA(cudaMalloc(&p->cnt, (size_t)m * 4));
+  JCUDA(cudaMalloc(&p->part, (size_t)(nchunks * a_rows) * 8));
+  JCUDA(cudaMalloc(&p->cnt, (size_t)a_rows * 4));
   p->nblk = (m + jacobi::kL2Block - 1) / jacobi::kL2Block;
   JCUDA(cudaMalloc(&p->sq, (size_t)m * 8));
   JCUDA(cudaMalloc(&p->blk, (size_t)p->nblk * 8));
@@ -130,7 +141,7 @@ int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dty
   JCUDA(cudaMallocHost(&p->st_host, kLookahead * sizeof(jacobi::State)));
   JCUDA(cudaMemsetAsync(p->x[0], 0, (size_t)p->x_len * 8, p->stream));
   JCUDA(cudaMemsetAsync(p->x[1], 0, (size_t)p->x_len * 8, p->stream));
-  JCUDA(cudaMemsetAsync(p->cnt, 0, (size_t)m * 4, p->stream));
+  JCUDA(cudaMemsetAsync(p->cnt, 0, (size_t)a_rows * 4, p->stream));
   JLAST("plan buffers");
   return 0;
 }
@@ -139,8 +150,11 @@ int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dty
 int plan_validate_A(jacobi_plan* p, unsigned long long* zero_row, int* nonfinite) {
   JCUDA(cudaMemsetAsync(p->zmin_dev, 0xff, 8, p->stream));
   JCUDA(cudaMemsetAsync(p->flag_dev, 0, 4, p->stream));
-  JCUDA(jacobi::launch_setup_diag(p->dtype, p->dA, p->lda, p->m, p->row0, p->diag, p->zmin_dev, p->stream));
-  JCUDA(jacobi::launch_scan_nonfinite_A(p->dtype, p->dA, p->lda, p->m, p->n, p->flag_dev, p->stream));
+  // a_ii of the owned rows: row block -> A[r][row0 + r]; column slab -> A[row0 + r][r].
+  const size_t esz = p->dtype == JACOBI_F32 ? 4 : 8;
+  const void* dbase = p->colwise ? (const char*)p->dA + (size_t)(p->row0 * p->lda - p->row0) * esz : p->dA;
+  JCUDA(jacobi::launch_setup_diag(p->dtype, dbase, p->lda, p->m, p->row0, p->diag, p->zmin_dev, p->stream));
+  JCUDA(jacobi::launch_scan_nonfinite_A(p->dtype, p->dA, p->lda, p->a_rows, p->a_cols, p->flag_dev, p->stream));
   if (p->comm) {
     JNCCL(ncclAllReduce(p->zmin_dev, p->zmin_dev, 1, ncclUint64, ncclMin, p->comm, p->stream));
     JNCCL(ncclAllReduce(p->flag_dev, p->flag_dev, 1, ncclInt32, ncclMax, p->comm, p->stream));
@@ -164,7 +178,7 @@ extern "C" int jacobi_plan_create(jacobi_plan** out, int64_t n, int dtype, const
   if (!out || !A || n < 1 || lda < n || (dtype != JACOBI_F64 && dtype != JACOBI_F32))
     return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_create: bad argument (out/A NULL, n < 1, lda < n or dtype)");
   jacobi_plan* p = new jacobi_plan();
-  int rc = plan_init_common(p, n, n, 0, dtype, A, lda, a_on_device, cuda_stream);
+  int rc = plan_init_common(p, n, n, 0, dtype, A, n, n, lda, a_on_device, cuda_stream);
   if (rc == 0) {
     const char* e = getenv("JACOBI_SMALL_N");
     if (!(e && e[0] == '0')) p->cluster_C = jacobi::cluster_plan(n, dtype, &p->cluster_smem);
@@ -194,6 +208,20 @@ extern "C" int jacobi_plan_set_row_blocks(jacobi_plan* p, int nblocks) {
   if (!p || nblocks < 1 || p->m % nblocks != 0 || p->comm)
     return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_set_row_blocks: nblocks must divide the rows of a 1-GPU plan");
   p->nblocks = nblocks;
+  return 0;
+}
+
+extern "C" int jacobi_plan_set_col_blocks(jacobi_plan* p, int nblocks) {
+  if (!p || nblocks < 1 || p->n % nblocks != 0 || p->comm || p->colwise)
+    return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_set_col_blocks: nblocks must divide n of a 1-GPU plan");
+  if (nblocks > 1) {
+    cudaFree(p->rsum);
+    p->rsum = nullptr;
+    JCUDA(cudaMalloc(&p->rsum, (size_t)(nblocks * p->n) * 8));
+    choose_variant(p, p->n / nblocks, &p->gemv_variant, &p->gemv_grid);
+    JLAST("column-block setup");
+  }
+  p->colblocks = nblocks;
   return 0;
 }
 
@@ -233,7 +261,7 @@ extern "C" int jacobi_plan_info(const jacobi_plan* p, jacobi_plan_info_t* info) 
   info->bytes_per_sweep = (double)p->m * (double)p->n * sA + 8.0 * (double)p->n + 16.0 * (double)p->m;
   info->variant = p->variant;
   info->num_variants = jacobi::num_variants();
-  info->cluster_ctas = (p->cluster_C && p->nblocks == 1 && !p->comm) ? p->cluster_C : 0;
+  info->cluster_ctas = (p->cluster_C && p->nblocks == 1 && p->colblocks == 1 && !p->comm) ? p->cluster_C : 0;
   return 0;
 }
 
@@ -254,6 +282,9 @@ static jacobi::SweepArgs sweep_args(const jacobi_plan* p, int blk) {
   a.cnt = p->cnt;
   a.dslot = p->dslot;
   a.st = p->st;
+  a.col0 = 0;
+  a.cend = p->n;
+  a.rsum = nullptr;
   a.sq = p->sq + blk * mb;
   a.norm = p->norm;
   a.chunk = p->chunk;
@@ -263,12 +294,54 @@ static jacobi::SweepArgs sweep_args(const jacobi_plan* p, int blk) {
   return a;
 }
 
-// Enqueue sweep j of a batch (all row blocks) plus, for distributed plans, the exchange
-// (SURVEY.md §8(a) a6): in-place allgather of the new x slice and max-allreduce of d_k's bits.
+// The sweep kernels of sweep j: row blocks (row-wise; P12a emulation when nblocks > 1), or column
+// slabs writing row sums (column-wise NEXT-4: this rank's slab, or the 1-GPU P-slab emulation).
+static int launch_gemv(jacobi_plan* p, int j) {
+  if (!p->colwise && p->colblocks == 1) {
+    for (int blk = 0; blk < p->nblocks; ++blk)
+      JCUDA(jacobi::launch_sweep(p->dtype, p->variant, sweep_args(p, blk), j, p->grid, p->stream));
+    return 0;
+  }
+  const int nb = p->colwise ? 1 : p->colblocks;
+  const int64_t w = p->colwise ? p->m : p->n / nb;  // slab width
+  const size_t esz = p->dtype == JACOBI_F32 ? 4 : 8;
+  const int v = p->colwise ? p->variant : p->gemv_variant;
+  const int grid = p->colwise ? p->grid : p->gemv_grid;
+  for (int q = 0; q < nb; ++q) {
+    jacobi::SweepArgs a = sweep_args(p, 0);
+    a.col0 = p->colwise ? p->row0 : q * w;
+    a.cend = a.col0 + w;
+    // pointer to column col0 of row 0 of the stored block (kernels index A by global column)
+    a.A = p->colwise ? p->dA : (const char*)p->dA + (size_t)(q * w) * esz;
+    a.m = p->n;  // every row of the system
+    a.row0 = 0;
+    a.rsum = p->rsum + (size_t)q * p->n;
+    a.nchunks = (int)((w + p->chunk - 1) / p->chunk);
+    const int R = jacobi::variant_rows_dt(v, p->dtype);
+    a.tiles = (int)((p->n + R - 1) / R);
+    JCUDA(jacobi::launch_sweep(p->dtype, v, a, j, grid, p->stream));
+  }
+  return 0;
+}
+
+// Enqueue sweep j of a batch plus, for distributed plans, the exchange:
+// row-wise: in-place allgather of the new x slice and max-allreduce of d_k's bits; column-wise:
+// reduce-scatter (sum) of the row sums, the epilogue on the owned rows, and the max-allreduce.
 static int enqueue_sweep(jacobi_plan* p, int j) {
-  for (int blk = 0; blk < p->nblocks; ++blk)
-    JCUDA(jacobi::launch_sweep(p->dtype, p->variant, sweep_args(p, blk), j, p->grid, p->stream));
-  if (p->comm) {
+  JRC(launch_gemv(p, j));
+  if (p->colwise) {
+    JNCCL(ncclReduceScatter(p->rsum, p->rs_own, (size_t)p->m, ncclDouble, ncclSum, p->comm, p->stream));
+    JCUDA(jacobi::launch_colsum_epilogue(p->rs_own, 1, p->m, p->m, p->row0, p->b, p->diag, p->x[0], p->x[1],
+                                         p->dslot, p->sq, p->norm, p->st, j, p->stream));
+  } else if (p->colblocks > 1) {
+    JCUDA(jacobi::launch_colsum_epilogue(p->rsum, p->colblocks, p->n, p->n, 0, p->b, p->diag, p->x[0], p->x[1],
+                                         p->dslot, p->sq, p->norm, p->st, j, p->stream));
+  }
+  if (p->comm && p->colwise) {
+    if (p->norm == JACOBI_NORM_MAX)
+      JNCCL(ncclAllReduce(p->dslot + ((j + 1) & 3), p->dslot + ((j + 1) & 3), 1, ncclUint64, ncclMax, p->comm,
+                          p->stream));
+  } else if (p->comm) {
     // k = kbase + j + 1 with kbase a multiple of the batch size (a multiple of 4): parity is static.
     double* xk = p->x[(j + 1) & 1];
     JNCCL(ncclAllGather(xk + p->row0, xk, (size_t)p->m, ncclDouble, p->comm, p->stream));
@@ -291,7 +364,9 @@ static int enqueue_sweep(jacobi_plan* p, int j) {
 }
 
 static int ensure_graph(jacobi_plan* p) {
-  if (p->graph && p->graph_batch == p->batch && p->graph_nblocks == p->nblocks && p->graph_norm == p->norm) return 0;
+  if (p->graph && p->graph_batch == p->batch && p->graph_nblocks == p->nblocks && p->graph_norm == p->norm &&
+      p->graph_colblocks == p->colblocks)
+    return 0;
   if (p->graph) {
     cudaGraphExecDestroy(p->graph);
     p->graph = nullptr;
@@ -316,6 +391,7 @@ static int ensure_graph(jacobi_plan* p) {
   p->graph_batch = p->batch;
   p->graph_nblocks = p->nblocks;
   p->graph_norm = p->norm;
+  p->graph_colblocks = p->colblocks;
   return 0;
 }
 
@@ -437,12 +513,16 @@ static int solve_impl(jacobi_plan* p, const double* b, const double* x0, bool de
     if (p->st_host[0].nonfinite) return nonfinite_error();
     fin.status = JACOBI_MAX_ITER;
     fin.iters = 0;
-  } else if (p->cluster_C && p->nblocks == 1 && !p->comm) {
+  } else if (p->cluster_C && p->nblocks == 1 && p->colblocks == 1 && !p->comm) {
     rc = solve_cluster(p, max_iter, &fin);
     if (rc) return rc;
   } else {
     rc = solve_run(p, max_iter, &fin);
     if (rc) return rc;
+  }
+  if (p->colwise && fin.iters > 0) {  // column-wise ranks hold only their slice: assemble x^(iters)
+    double* xf = p->x[fin.iters & 1];
+    JNCCL(ncclAllGather(xf + p->row0, xf, (size_t)p->m, ncclDouble, p->comm, p->stream));
   }
   const cudaMemcpyKind kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
   JCUDA(cudaMemcpyAsync(x_out, p->x[fin.iters & 1], (size_t)p->n * 8, kind, p->stream));
@@ -479,16 +559,24 @@ extern "C" int jacobi_plan_time_sweeps(jacobi_plan* p, const double* d_b, const 
   JCUDA(cudaEventCreate(&e1));
   for (int j = 0; j < sweeps && rc == 0; ++j) {
     cudaEventRecord(e0, p->stream);
-    for (int blk = 0; blk < p->nblocks; ++blk) {
-      cudaError_t e = jacobi::launch_sweep(p->dtype, p->variant, sweep_args(p, blk), j, p->grid, p->stream);
-      if (e != cudaSuccess) rc = jacobi_set_error(JACOBI_ECUDA, cudaGetErrorString(e));
-    }
+    rc = launch_gemv(p, j);  // the sweep kernel(s) alone are timed
     cudaEventRecord(e1, p->stream);
-    if (rc == 0 && p->comm) rc = [&]() -> int {
-      double* xk = p->x[(j + 1) & 1];
-      JNCCL(ncclAllGather(xk + p->row0, xk, (size_t)p->m, ncclDouble, p->comm, p->stream));
-      JNCCL(ncclAllReduce(p->dslot + ((j + 1) & 3), p->dslot + ((j + 1) & 3), 1, ncclUint64, ncclMax, p->comm,
-                          p->stream));
+    if (rc == 0) rc = [&]() -> int {  // the rest of the sweep (exchange, column-wise epilogue)
+      if (p->colwise) {
+        JNCCL(ncclReduceScatter(p->rsum, p->rs_own, (size_t)p->m, ncclDouble, ncclSum, p->comm, p->stream));
+        JCUDA(jacobi::launch_colsum_epilogue(p->rs_own, 1, p->m, p->m, p->row0, p->b, p->diag, p->x[0], p->x[1],
+                                             p->dslot, p->sq, JACOBI_NORM_MAX, p->st, j, p->stream));
+      } else if (p->colblocks > 1) {
+        JCUDA(jacobi::launch_colsum_epilogue(p->rsum, p->colblocks, p->n, p->n, 0, p->b, p->diag, p->x[0],
+                                             p->x[1], p->dslot, p->sq, JACOBI_NORM_MAX, p->st, j, p->stream));
+      }
+      if (p->comm && !p->colwise) {
+        double* xk = p->x[(j + 1) & 1];
+        JNCCL(ncclAllGather(xk + p->row0, xk, (size_t)p->m, ncclDouble, p->comm, p->stream));
+      }
+      if (p->comm)
+        JNCCL(ncclAllReduce(p->dslot + ((j + 1) & 3), p->dslot + ((j + 1) & 3), 1, ncclUint64, ncclMax, p->comm,
+                            p->stream));
       return 0;
     }();
     cudaError_t se = cudaEventSynchronize(e1);

@@ -161,17 +161,17 @@ __global__ void __launch_bounds__(NT, (NT < 512 ? 512 / NT : 1)) k_sweep(const S
     const int tile = (int)(it % a.tiles);
     const int c = (int)(it / a.tiles);
     const int64_t r0 = (int64_t)tile * R;
-    const int64_t c0 = (int64_t)c * a.chunk;
-    const int64_t c1 = min(c0 + (int64_t)a.chunk, a.n);
+    const int64_t c0 = a.col0 + (int64_t)c * a.chunk;
+    const int64_t c1 = min(c0 + (int64_t)a.chunk, a.cend);
     const int64_t g0 = a.row0 + r0;  // global index of the tile's first row
-    const T* rowp[R];
+    const T* rowp[R];  // indexed by global column
 #pragma unroll
-    for (int r = 0; r < R; ++r) rowp[r] = A + min(r0 + r, a.m - 1) * a.lda;
+    for (int r = 0; r < R; ++r) rowp[r] = A + min(r0 + r, a.m - 1) * a.lda - a.col0;
     double acc[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[r] = 0.0;
 
-    accumulate_chunk<T, R, U>(rowp, R, xo, c0, c1, a.chunk, a.n, g0, lane, acc);
+    accumulate_chunk<T, R, U>(rowp, R, xo, c0, c1, a.chunk, a.cend, g0, lane, acc);
     // Butterfly: every lane ends with the same, order-fixed row sums.
 #pragma unroll
     for (int r = 0; r < R; ++r)
@@ -198,12 +198,16 @@ __global__ void __launch_bounds__(NT, (NT < 512 ? 512 / NT : 1)) k_sweep(const S
       const int64_t row = r0 + lane;
       double s = __ldcg(a.part + row);
       for (int cc = 1; cc < a.nchunks; ++cc) s += __ldcg(a.part + (int64_t)cc * a.m + row);
-      const double xnew = __ddiv_rn(__dsub_rn(a.b[row], s), a.diag[row]);
-      const int64_t gi = a.row0 + row;
-      const double dx = __dsub_rn(xnew, xo[gi]);
-      xn[gi] = xnew;
-      dbits = (unsigned long long)__double_as_longlong(dx) & 0x7fffffffffffffffull;
-      if (a.norm == JACOBI_NORM_L2) a.sq[row] = __dmul_rn(dx, dx);
+      if (a.rsum) {  // column-wise partial product of this slab (epilogue after the reduction)
+        a.rsum[row] = s;
+      } else {
+        const double xnew = __ddiv_rn(__dsub_rn(a.b[row], s), a.diag[row]);
+        const int64_t gi = a.row0 + row;
+        const double dx = __dsub_rn(xnew, xo[gi]);
+        xn[gi] = xnew;
+        dbits = (unsigned long long)__double_as_longlong(dx) & 0x7fffffffffffffffull;
+        if (a.norm == JACOBI_NORM_L2) a.sq[row] = __dmul_rn(dx, dx);
+      }
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -279,6 +283,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
       double s = sp[0];
       for (int c = 1; c < nch; ++c) s += sp[(size_t)c * R];
       const int64_t row = r0 + lane;
+      if (a.rsum) {  // column-wise partial product of this slab (epilogue after the reduction)
+        a.rsum[row] = s;
+        goto tile_done;
+      }
+      {
       const double xnew = __ddiv_rn(__dsub_rn(a.b[row], s), a.diag[row]);
       const int64_t gi = a.row0 + row;
       const double dx = __dsub_rn(xnew, xo[gi]);
@@ -286,7 +295,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
       const unsigned long long bits = (unsigned long long)__double_as_longlong(dx) & 0x7fffffffffffffffull;
       dmax = bits > dmax ? bits : dmax;
       if (a.norm == JACOBI_NORM_L2) a.sq[row] = __dmul_rn(dx, dx);
+      }
     }
+  tile_done:
     __syncwarp();
     if (lane == 0) mbar_arrive(&s_empty[q]);
   };
@@ -298,15 +309,15 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
     if (t >= kSlots) mbar_wait(&s_empty[q], (unsigned)(((t / kSlots) - 1) & 1));
     const T* rowp[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) rowp[r] = A + (r0 + min(r, nv - 1)) * a.lda;
+    for (int r = 0; r < R; ++r) rowp[r] = A + (r0 + min(r, nv - 1)) * a.lda - a.col0;  // global columns
     const int64_t g0 = a.row0 + r0;
     for (int c = w; c < nch; c += NW) {
       double acc[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) acc[r] = 0.0;
-      const int64_t c0 = (int64_t)c * a.chunk;
-      const int64_t c1 = min(c0 + (int64_t)a.chunk, a.n);
-      accumulate_chunk<T, R, U, XL>(rowp, nv, xo, c0, c1, a.chunk, a.n, g0, lane, acc);
+      const int64_t c0 = a.col0 + (int64_t)c * a.chunk;
+      const int64_t c1 = min(c0 + (int64_t)a.chunk, a.cend);
+      accumulate_chunk<T, R, U, XL>(rowp, nv, xo, c0, c1, a.chunk, a.cend, g0, lane, acc);
 #pragma unroll
       for (int r = 0; r < R; ++r)
 #pragma unroll
@@ -358,6 +369,37 @@ __global__ void k_l2_final(const double* __restrict__ blk, int64_t nblk, unsigne
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) s = __dadd_rn(s, __shfl_xor_sync(kFull, s, off));
   if (threadIdx.x == 0) dslot[k & 3] = (unsigned long long)__double_as_longlong(__dsqrt_rn(s));
+}
+
+// Column-wise epilogue (NEXT-4, "partial values ... added together and subtracted by the
+// value of the corresponding cell of the B vector"): s_i = sum of the nb slab partials in ascending
+// slab order, then x_i^(k) = (b_i - s_i)/a_ii and |dx| for the rows [row0, row0 + rows).
+__global__ void k_colsum_epilogue(const double* __restrict__ rsum, int nb, int64_t stride, int64_t rows,
+                                  int64_t row0, const double* __restrict__ b, const double* __restrict__ diag,
+                                  double* x0buf, double* x1buf, unsigned long long* dslot, double* sq, int norm,
+                                  State* st, int j) {
+  if (*(volatile int32_t*)&st->done || st->nonfinite) return;
+  const int64_t k = st->kbase + j + 1;
+  const double* xo = (k & 1) ? x0buf : x1buf;
+  double* xn = (k & 1) ? x1buf : x0buf;
+  unsigned long long dmax = 0ull;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    double s = rsum[r];
+    for (int q = 1; q < nb; ++q) s += rsum[(int64_t)q * stride + r];
+    const double xnew = __ddiv_rn(__dsub_rn(b[r], s), diag[r]);
+    const int64_t gi = row0 + r;
+    const double dx = __dsub_rn(xnew, xo[gi]);
+    xn[gi] = xnew;
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(dx) & 0x7fffffffffffffffull;
+    dmax = bits > dmax ? bits : dmax;
+    if (norm == JACOBI_NORM_L2) sq[r] = __dmul_rn(dx, dx);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const unsigned long long o = __shfl_xor_sync(kFull, dmax, off);
+    dmax = o > dmax ? o : dmax;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(&dslot[k & 3], dmax);
 }
 
 // After a graph batch of K sweeps: settle the stop decision for the batch's last sweep (same rule
@@ -539,6 +581,15 @@ cudaError_t launch_l2_partials(const double* sq, int64_t m, double* blk, const S
 cudaError_t launch_l2_final(const double* blk, int64_t nblk, unsigned long long* dslot, State* st, int j,
                             cudaStream_t s) {
   k_l2_final<<<1, 32, 0, s>>>(blk, nblk, dslot, st, j);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_colsum_epilogue(const double* rsum, int nb, int64_t stride, int64_t rows, int64_t row0,
+                                   const double* b, const double* diag, double* x0buf, double* x1buf,
+                                   unsigned long long* dslot, double* sq, int norm, State* st, int j,
+                                   cudaStream_t s) {
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((rows + 255) / 256, 592));
+  k_colsum_epilogue<<<grid, 256, 0, s>>>(rsum, nb, stride, rows, row0, b, diag, x0buf, x1buf, dslot, sq, norm, st, j);
   return cudaGetLastError();
 }
 

@@ -410,3 +410,36 @@ def test_small_n_cluster_path_bitwise(jb, n, f32, monkeypatch):
     st_o, x_o, it_o = oracle.jacobi(A, b, x0, 3000, 1e-12)
     r = res[("1", 3000, 1e-12, "max")]
     assert (r.status, r.iters) == (st_o, it_o) and rel_linf(r.x, x_o) <= TOL64
+
+
+# ------------------------------------------------------------------ NEXT-4: column-wise distribution (§3.2)
+def test_colwise_emulated_slabs_and_single_rank(jb):
+    """Column slabs: row sums of each n x m slab from that slab's x slice, summed over
+    slabs, then the epilogue.  1-GPU emulation with P slabs vs the oracle (tolerance: the slab sums
+    re-associate the chunk sums), and the NCCL column-wise plan with one rank (bitwise = row-wise)."""
+    import torch
+    for n, scale, f32 in ((4096, 1.05, False), (3000, 1.02, False), (8192, 1.2, True)):
+        A, b, _ = dominant(n, 91 + n, scale=scale, f32=f32)
+        st_o, x_o, it_o, h_o = oracle.jacobi(A, b, None, 3000, 1e-10, nthreads=16, history=True)
+        with jb.Plan(A) as p:
+            ref = p.solve(b, None, 3000, 1e-10, history=True)
+            for P in (2, 4, 8):
+                if n % P:
+                    continue
+                p.set_col_blocks(P)
+                r = p.solve(b, None, 3000, 1e-10, history=True)
+                assert (r.status, r.iters) == (st_o, it_o), (n, P)
+                assert rel_linf(r.x, x_o) <= TOL64
+                np.testing.assert_allclose(r.hist, h_o, rtol=1e-9, atol=1e-14)
+                p.set_norm("l2")
+                rl = p.solve(b, None, 3000, 1e-10)
+                p.set_norm("max")
+                assert rl.iters >= r.iters and rel_linf(rl.x, x_o) <= 1e-9
+            p.set_col_blocks(1)
+            r1 = p.solve(b, None, 3000, 1e-10, history=True)
+            assert np.array_equal(r1.x, ref.x) and np.array_equal(r1.hist, ref.hist)
+        dA = torch.from_numpy(A).cuda()
+        with jb.Plan(dA, n=n, dist=(jb.nccl_unique_id(), 0, 1), layout="cols") as p:
+            rc = p.solve(b, None, 3000, 1e-10, history=True)
+            assert (rc.status, rc.iters) == (ref.status, ref.iters)
+            assert np.array_equal(rc.x, ref.x) and np.array_equal(rc.hist, ref.hist)
