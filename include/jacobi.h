@@ -141,11 +141,12 @@ int jacobi_dist_plan_create(jacobi_plan** out, const void* uid128, int rank, int
  * "MPI_Allreduce ... MPI_SUM" of PAPER.md:100 restricted to the rows each rank finalizes) gives rank
  * r the sums of rows [r*m, (r+1)*m), and the epilogue updates that slice — the only part of x the
  * rank needs next sweep, so x is allgathered once, at the end.  The rank-sum order is NCCL's, so
- * results are NOT bitwise independent of P (they are within the parity tolerance). */
+ * results are NOT bitwise independent of P (they are within the parity tolerance).  For nranks > 1,
+ * m = n / nranks must be a multiple of 8 (32-byte aligned slab columns), else JACOBI_EINVAL. */
 int jacobi_dist_plan_create_colwise(jacobi_plan** out, const void* uid128, int rank, int nranks, int64_t n,
                                     int dtype, const void* A_cols, int64_t lda, int a_on_device,
                                     void* cuda_stream);
-/* Test hook: emulate a P-slab column-wise sweep on one GPU (P | n): P slab launches write row sums,
+/* Test hook: emulate a P-slab column-wise sweep on one GPU (P | n, n/P a multiple of 8 when P > 1): P slab launches write row sums,
  * and the epilogue adds the P partials in slab order.  Exercises the slab kernels with col0 > 0. */
 int jacobi_plan_set_col_blocks(jacobi_plan* plan, int nblocks);
 

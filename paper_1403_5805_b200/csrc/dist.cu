@@ -39,6 +39,8 @@ static int dist_create(jacobi_plan** out, const void* uid128, int rank, int nran
   int rc = jacobi_partition(n, nranks, rank, &row0, &m);
   if (rc) return rc;
   if (lda < (colwise ? m : n)) return jacobi_set_error(JACOBI_EINVAL, std::string(fn) + ": lda too small");
+  if (colwise && nranks > 1 && m % 8 != 0)
+    return jacobi_set_error(JACOBI_EINVAL, std::string(fn) + ": n / nranks must be a multiple of 8 (slab alignment)");
   jacobi_plan* p = new jacobi_plan();
   p->rank = rank;
   p->nranks = nranks;

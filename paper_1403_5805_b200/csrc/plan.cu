@@ -212,8 +212,10 @@ extern "C" int jacobi_plan_set_row_blocks(jacobi_plan* p, int nblocks) {
 }
 
 extern "C" int jacobi_plan_set_col_blocks(jacobi_plan* p, int nblocks) {
-  if (!p || nblocks < 1 || p->n % nblocks != 0 || p->comm || p->colwise)
-    return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_set_col_blocks: nblocks must divide n of a 1-GPU plan");
+  if (!p || nblocks < 1 || p->n % nblocks != 0 || p->comm || p->colwise ||
+      (nblocks > 1 && (p->n / nblocks) % 8 != 0))
+    return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_set_col_blocks: nblocks must divide n of a 1-GPU plan "
+                                           "into slabs of a multiple of 8 columns (32-byte aligned loads)");
   if (nblocks > 1) {
     cudaFree(p->rsum);
     p->rsum = nullptr;

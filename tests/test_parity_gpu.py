@@ -418,14 +418,14 @@ def test_colwise_emulated_slabs_and_single_rank(jb):
     slabs, then the epilogue.  1-GPU emulation with P slabs vs the oracle (tolerance: the slab sums
     re-associate the chunk sums), and the NCCL column-wise plan with one rank (bitwise = row-wise)."""
     import torch
-    for n, scale, f32 in ((4096, 1.05, False), (3000, 1.02, False), (8192, 1.2, True)):
+    for n, scale, f32, Ps in ((4096, 1.05, False, (2, 4, 8)), (3000, 1.02, False, (3, 5)), (8192, 1.2, True, (2, 8))):
         A, b, _ = dominant(n, 91 + n, scale=scale, f32=f32)
         st_o, x_o, it_o, h_o = oracle.jacobi(A, b, None, 3000, 1e-10, nthreads=16, history=True)
         with jb.Plan(A) as p:
             ref = p.solve(b, None, 3000, 1e-10, history=True)
-            for P in (2, 4, 8):
-                if n % P:
-                    continue
+            with pytest.raises(jb.JacobiError):
+                p.set_col_blocks(7)  # 7 does not divide n into 8-aligned slabs
+            for P in Ps:
                 p.set_col_blocks(P)
                 r = p.solve(b, None, 3000, 1e-10, history=True)
                 assert (r.status, r.iters) == (st_o, it_o), (n, P)
