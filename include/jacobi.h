@@ -150,6 +150,21 @@ int jacobi_dist_plan_create_colwise(jacobi_plan** out, const void* uid128, int r
  * and the epilogue adds the P partials in slab order.  Exercises the slab kernels with col0 > 0. */
 int jacobi_plan_set_col_blocks(jacobi_plan* plan, int nblocks);
 
+/* Fused exchange (the non-blocking overlap of PAPER.md:82 and the one-sided
+ * put/get of PAPER.md:118-148): instead of NCCL collectives after each sweep, the sweep kernel's
+ * epilogue stores every new x_i into every rank's x buffer over NVLink, folds max|dx| into every rank's
+ * distance slot with remote atomics, and after a system-scope fence each CTA bumps every rank's
+ * arrival counter; the next sweep's prologue waits for its own counter (acquire).  Max norm only.
+ *   jacobi_plan_ipc_export: 256 bytes of CUDA IPC handles of this rank's x buffers, slots, counters.
+ *   jacobi_plan_ipc_attach: all ranks' 256-byte blocks (rank order) -> peer mappings; enables the mode.
+ * Both are called on every rank of a row-wise distributed plan (the caller gathers the handles). */
+int jacobi_plan_ipc_export(jacobi_plan* plan, void* out256);
+int jacobi_plan_ipc_attach(jacobi_plan* plan, const void* all_handles);
+/* Test hook: the fused exchange with P ranks emulated on one GPU (P | n, P <= 8): per-rank x copies,
+ * slots and counters; the ranks' sweep kernels run as P sequential launches, so no launch ever waits
+ * on a concurrently running one.  Results equal the plain plan bit for bit. */
+int jacobi_plan_set_p2p_emulation(jacobi_plan* plan, int P);
+
 /* ------------------------------------------------------------------ measurement */
 /* Read-only HBM ceiling: streams `nbytes` of device memory with the sweep kernel's load flavour
  * (256-bit, L1::no_allocate) and returns the best GB/s of `reps` timed passes. */

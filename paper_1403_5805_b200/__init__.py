@@ -30,7 +30,8 @@ EXPORTS = ("jacobi_solve", "jacobi_solve_f32a", "jacobi_plan_create", "jacobi_pl
            "jacobi_plan_solve_device", "jacobi_plan_destroy", "jacobi_plan_set_row_blocks",
            "jacobi_plan_set_batch", "jacobi_plan_set_norm", "jacobi_plan_info", "jacobi_plan_time_sweeps", "jacobi_partition",
            "jacobi_nccl_unique_id", "jacobi_dist_plan_create", "jacobi_dist_plan_create_colwise",
-           "jacobi_plan_set_col_blocks", "jacobi_bwprobe", "jacobi_last_error",
+           "jacobi_plan_set_col_blocks", "jacobi_plan_ipc_export", "jacobi_plan_ipc_attach",
+           "jacobi_plan_set_p2p_emulation", "jacobi_bwprobe", "jacobi_last_error",
            "jacobi_version")
 
 
@@ -79,6 +80,9 @@ def _load():
         "jacobi_dist_plan_create": ([P(vp), vp, i32, i32, i64, i32, vp, i64, i32, vp], i32),
         "jacobi_dist_plan_create_colwise": ([P(vp), vp, i32, i32, i64, i32, vp, i64, i32, vp], i32),
         "jacobi_plan_set_col_blocks": ([vp, i32], i32),
+        "jacobi_plan_ipc_export": ([vp, vp], i32),
+        "jacobi_plan_ipc_attach": ([vp, vp], i32),
+        "jacobi_plan_set_p2p_emulation": ([vp, i32], i32),
         "jacobi_bwprobe": ([i64, i32, P(dbl)], i32),
         "jacobi_last_error": ([], ctypes.c_char_p),
         "jacobi_version": ([], i32),
@@ -215,6 +219,18 @@ class Plan:
 
     def set_row_blocks(self, nblocks):
         _check(_lib.jacobi_plan_set_row_blocks(self._h, int(nblocks)))
+
+    def set_p2p_emulation(self, nranks):
+        _check(_lib.jacobi_plan_set_p2p_emulation(self._h, int(nranks)))
+
+    def ipc_export(self) -> bytes:
+        buf = ctypes.create_string_buffer(256)
+        _check(_lib.jacobi_plan_ipc_export(self._h, buf))
+        return buf.raw
+
+    def ipc_attach(self, all_handles: bytes):
+        buf = ctypes.create_string_buffer(bytes(all_handles), len(all_handles))
+        _check(_lib.jacobi_plan_ipc_attach(self._h, buf))
 
     def set_col_blocks(self, nblocks):
         _check(_lib.jacobi_plan_set_col_blocks(self._h, int(nblocks)))

@@ -4,6 +4,7 @@
 #include <nccl.h>
 #include <stdint.h>
 #include <string>
+#include <vector>
 #include "jacobi.h"
 
 namespace jacobi {
@@ -20,6 +21,18 @@ struct State {
   int64_t iters;      // sweeps performed once done
   int32_t nonfinite;  // b or x0 held NaN/Inf (set by k_prepare): every sweep is a no-op, solve -> ENONFINITE
   int32_t pad_;
+};
+
+// NEXT-1 fused exchange: every rank's x buffers, distance slots and arrival counters (peer-mapped
+// pointers over NVLink, or copies on one GPU when P ranks are emulated).  Device-resident.
+enum { kMaxPeers = 8 };
+struct PeerArgs {
+  int P, rank;
+  unsigned long long total_ctas;             // sweep-kernel CTAs over all ranks (arrivals per sweep)
+  double* x0[kMaxPeers];
+  double* x1[kMaxPeers];
+  unsigned long long* dslot[kMaxPeers];
+  unsigned long long* flags[kMaxPeers];      // [2] arrival counters per parity of k
 };
 
 // Everything a sweep kernel needs; fixed for the life of a plan (captured into CUDA graphs).
@@ -41,6 +54,7 @@ struct SweepArgs {
   double* rsum;             // non-null: write the row sums over [col0, cend) to rsum[row] (column-wise
                             // partial products) instead of applying the epilogue
   double* sq;               // norm == L2: (x_i^(k) - x_i^(k-1))^2 of the launch's rows
+  const PeerArgs* peers;    // non-null: fused exchange (NEXT-1) — CTA kernel only
   int norm;                 // JACOBI_NORM_MAX / JACOBI_NORM_L2
   int chunk;                // columns per work item (multiple of 512, depends on n only)
   int nchunks;              // ceil(n / chunk)
@@ -56,7 +70,7 @@ cudaError_t launch_scan_nonfinite_A(int dtype, const void* A, int64_t lda, int64
                                     int* flag, cudaStream_t s);
 cudaError_t launch_prepare(State* st, int64_t max_iter, double tol, double* hist, unsigned long long* dslot,
                            unsigned* cnt, int64_t ncnt, const double* b, int64_t m, const double* x0, int64_t n,
-                           cudaStream_t s);
+                           unsigned long long* flags, cudaStream_t s);
 cudaError_t launch_copy_pitched(int dtype, const void* src, int64_t src_ld, void* dst, int64_t dst_ld,
                                 int64_t rows, int64_t n, cudaStream_t s);
 int num_variants();
@@ -99,6 +113,15 @@ struct jacobi_plan {
   double* rsum = nullptr;        // column-wise row sums: colblocks x n (emulation) or n (distributed)
   double* rs_own = nullptr;      // distributed column-wise: reduce-scatter output (m)
   int gemv_variant = 0, gemv_grid = 0;  // kernel for the emulated column slabs
+  // NEXT-1 fused exchange
+  int p2p = 0;                   // 0 off; >= 1: number of ranks (peer-mapped, or emulated on one GPU)
+  bool p2p_emul = false;         // P ranks emulated on this GPU (sequential row-block launches)
+  jacobi::PeerArgs* peers_dev = nullptr;  // one PeerArgs per (virtual) rank
+  unsigned long long* flags = nullptr;    // own arrival counters [2]
+  double* ex_x = nullptr;        // emulation: x copies of virtual ranks 1..P-1 (2 buffers each)
+  unsigned long long* ex_dslot = nullptr;
+  unsigned long long* ex_flags = nullptr;
+  std::vector<void*> ipc_open;   // opened peer mappings (closed at destroy)
   int variant = 0;               // sweep kernel variant (R, U, threads); default per dtype, JACOBI_SWEEP_VARIANT overrides
   int batch = 32;                // sweeps per graph batch
   int norm = JACOBI_NORM_MAX;    // distance of the stop test

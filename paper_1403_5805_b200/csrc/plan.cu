@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 namespace {
 thread_local std::string g_err;
@@ -39,9 +40,11 @@ static int plan_free(jacobi_plan* p) {
   if (p->graph) chk(cudaGraphExecDestroy(p->graph), "cudaGraphExecDestroy");
   if (p->comm) ncclCommDestroy(p->comm);
   void* dev[] = {p->dA_owned, p->diag, p->b, p->x[0], p->x[1], p->part, p->cnt, p->dslot, p->st,
-                 p->hist_dev, p->flag_dev, p->zmin_dev, p->sq, p->blk, p->blk_all, p->rsum, p->rs_own};
+                 p->hist_dev, p->flag_dev, p->zmin_dev, p->sq, p->blk, p->blk_all, p->rsum, p->rs_own,
+                 p->flags, p->ex_x, p->ex_dslot, p->ex_flags, p->peers_dev};
   const char* names[] = {"A", "diag", "b", "x0", "x1", "part", "cnt", "dslot", "state", "hist", "flag", "zmin",
-                         "sq", "blk", "blk_all", "rsum", "rs_own"};
+                         "sq", "blk", "blk_all", "rsum", "rs_own", "flags", "ex_x", "ex_dslot", "ex_flags", "peers"};
+  for (void* q : p->ipc_open) chk(cudaIpcCloseMemHandle(q), "cudaIpcCloseMemHandle");
   for (size_t i = 0; i < sizeof(dev) / sizeof(dev[0]); ++i)
     if (dev[i]) chk(cudaFree(dev[i]), names[i]);
   if (p->st_host) chk(cudaFreeHost(p->st_host), "cudaFreeHost(state)");
@@ -135,6 +138,8 @@ int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dty
   JCUDA(cudaMalloc(&p->sq, (size_t)m * 8));
   JCUDA(cudaMalloc(&p->blk, (size_t)p->nblk * 8));
   JCUDA(cudaMalloc(&p->dslot, 4 * 8));
+  JCUDA(cudaMalloc(&p->flags, 2 * 8));
+  JCUDA(cudaMemsetAsync(p->flags, 0, 2 * 8, p->stream));
   JCUDA(cudaMalloc(&p->st, sizeof(jacobi::State)));
   JCUDA(cudaMalloc(&p->flag_dev, 16));
   JCUDA(cudaMalloc(&p->zmin_dev, 8));
@@ -205,14 +210,14 @@ extern "C" void jacobi_plan_destroy(jacobi_plan* p) {
 }
 
 extern "C" int jacobi_plan_set_row_blocks(jacobi_plan* p, int nblocks) {
-  if (!p || nblocks < 1 || p->m % nblocks != 0 || p->comm)
+  if (!p || nblocks < 1 || p->m % nblocks != 0 || p->comm || p->p2p)
     return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_set_row_blocks: nblocks must divide the rows of a 1-GPU plan");
   p->nblocks = nblocks;
   return 0;
 }
 
 extern "C" int jacobi_plan_set_col_blocks(jacobi_plan* p, int nblocks) {
-  if (!p || nblocks < 1 || p->n % nblocks != 0 || p->comm || p->colwise ||
+  if (!p || nblocks < 1 || p->n % nblocks != 0 || p->comm || p->colwise || p->p2p ||
       (nblocks > 1 && (p->n / nblocks) % 8 != 0))
     return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_set_col_blocks: nblocks must divide n of a 1-GPU plan "
                                            "into slabs of a multiple of 8 columns (32-byte aligned loads)");
@@ -227,9 +232,109 @@ extern "C" int jacobi_plan_set_col_blocks(jacobi_plan* p, int nblocks) {
   return 0;
 }
 
+// NEXT-1 helpers --------------------------------------------------------------------------------
+static int p2p_pick_variant(jacobi_plan* p) {
+  if (jacobi::variant_is_cta(p->variant)) return 0;
+  const int nch = (int)((p->n + p->chunk - 1) / p->chunk);
+  for (int v : {9, 7, 6}) {
+    if (jacobi::variant_fits(v, nch, p->dtype, p->chunk)) {
+      p->variant = v;
+      p->grid = jacobi::sweep_grid(p->dtype, v, p->num_sms, nch, p->chunk);
+      return check_last("fused-exchange variant");
+    }
+  }
+  return jacobi_set_error(JACOBI_EINVAL, "fused exchange needs the CTA sweep kernel (n with >= 16 chunks)");
+}
+
+extern "C" int jacobi_plan_set_p2p_emulation(jacobi_plan* p, int P) {
+  if (!p || P < 1 || P > jacobi::kMaxPeers || p->comm || p->colwise || p->colblocks > 1 || p->m % P != 0 ||
+      p->norm != JACOBI_NORM_MAX || p->p2p)
+    return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_set_p2p_emulation: 1-GPU max-norm plan, P in [1, 8] dividing n, once");
+  JRC(p2p_pick_variant(p));
+  if (P > 1) {
+    JCUDA(cudaMalloc(&p->ex_x, (size_t)(P - 1) * 2 * p->x_len * 8));
+    JCUDA(cudaMemsetAsync(p->ex_x, 0, (size_t)(P - 1) * 2 * p->x_len * 8, p->stream));
+    JCUDA(cudaMalloc(&p->ex_dslot, (size_t)(P - 1) * 4 * 8));
+    JCUDA(cudaMalloc(&p->ex_flags, (size_t)(P - 1) * 2 * 8));
+  }
+  std::vector<jacobi::PeerArgs> pa(P);
+  for (int r = 0; r < P; ++r) {
+    jacobi::PeerArgs& a = pa[r];
+    std::memset(&a, 0, sizeof(a));
+    a.P = P;
+    a.rank = r;
+    a.total_ctas = (unsigned long long)P * p->grid;
+    for (int q = 0; q < P; ++q) {
+      a.x0[q] = q == 0 ? p->x[0] : p->ex_x + (size_t)(q - 1) * 2 * p->x_len;
+      a.x1[q] = q == 0 ? p->x[1] : a.x0[q] + p->x_len;
+      a.dslot[q] = q == 0 ? p->dslot : p->ex_dslot + (size_t)(q - 1) * 4;
+      a.flags[q] = q == 0 ? p->flags : p->ex_flags + (size_t)(q - 1) * 2;
+    }
+  }
+  JCUDA(cudaMalloc(&p->peers_dev, sizeof(jacobi::PeerArgs) * P));
+  JCUDA(cudaMemcpyAsync(p->peers_dev, pa.data(), sizeof(jacobi::PeerArgs) * P, cudaMemcpyHostToDevice, p->stream));
+  JCUDA(cudaStreamSynchronize(p->stream));
+  p->p2p = P;
+  p->p2p_emul = true;
+  p->nblocks = P;
+  return 0;
+}
+
+extern "C" int jacobi_plan_ipc_export(jacobi_plan* p, void* out256) {
+  if (!p || !out256 || !p->comm || p->colwise)
+    return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_ipc_export: row-wise distributed plan and a 256-byte buffer");
+  cudaIpcMemHandle_t h[4];
+  JCUDA(cudaIpcGetMemHandle(&h[0], p->x[0]));
+  JCUDA(cudaIpcGetMemHandle(&h[1], p->x[1]));
+  JCUDA(cudaIpcGetMemHandle(&h[2], p->dslot));
+  JCUDA(cudaIpcGetMemHandle(&h[3], p->flags));
+  static_assert(sizeof(h) == 256, "4 IPC handles");
+  std::memcpy(out256, h, sizeof(h));
+  return 0;
+}
+
+extern "C" int jacobi_plan_ipc_attach(jacobi_plan* p, const void* all_handles) {
+  if (!p || !all_handles || !p->comm || p->colwise || p->nranks > jacobi::kMaxPeers || p->norm != JACOBI_NORM_MAX ||
+      p->p2p)
+    return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_ipc_attach: row-wise max-norm distributed plan, <= 8 ranks, once");
+  JRC(p2p_pick_variant(p));
+  jacobi::PeerArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.P = p->nranks;
+  a.rank = p->rank;
+  a.total_ctas = (unsigned long long)p->nranks * p->grid;  // same device type on every rank
+  const cudaIpcMemHandle_t* h = static_cast<const cudaIpcMemHandle_t*>(all_handles);
+  for (int q = 0; q < p->nranks; ++q) {
+    if (q == p->rank) {
+      a.x0[q] = p->x[0];
+      a.x1[q] = p->x[1];
+      a.dslot[q] = p->dslot;
+      a.flags[q] = p->flags;
+      continue;
+    }
+    void* ptr[4];
+    for (int i = 0; i < 4; ++i) JCUDA(cudaIpcOpenMemHandle(&ptr[i], h[q * 4 + i], cudaIpcMemLazyEnablePeerAccess));
+    a.x0[q] = static_cast<double*>(ptr[0]);
+    a.x1[q] = static_cast<double*>(ptr[1]);
+    a.dslot[q] = static_cast<unsigned long long*>(ptr[2]);
+    a.flags[q] = static_cast<unsigned long long*>(ptr[3]);
+    p->ipc_open.push_back(ptr[0]);
+    p->ipc_open.push_back(ptr[1]);
+    p->ipc_open.push_back(ptr[2]);
+    p->ipc_open.push_back(ptr[3]);
+  }
+  JCUDA(cudaMalloc(&p->peers_dev, sizeof(a)));
+  JCUDA(cudaMemcpyAsync(p->peers_dev, &a, sizeof(a), cudaMemcpyHostToDevice, p->stream));
+  JCUDA(cudaStreamSynchronize(p->stream));
+  p->p2p = p->nranks;
+  return 0;
+}
+
 extern "C" int jacobi_plan_set_norm(jacobi_plan* p, int norm) {
   if (!p || (norm != JACOBI_NORM_MAX && norm != JACOBI_NORM_L2))
     return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_set_norm: norm must be JACOBI_NORM_MAX or JACOBI_NORM_L2");
+  if (norm == JACOBI_NORM_L2 && p->p2p)
+    return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_set_norm: the fused exchange supports the max norm only");
   if (norm == JACOBI_NORM_L2 && p->comm && !p->blk_all) {
     JCUDA(cudaMalloc(&p->blk_all, (size_t)(p->nblk * p->nranks) * 8));
   }
@@ -263,7 +368,8 @@ extern "C" int jacobi_plan_info(const jacobi_plan* p, jacobi_plan_info_t* info) 
   info->bytes_per_sweep = (double)p->m * (double)p->n * sA + 8.0 * (double)p->n + 16.0 * (double)p->m;
   info->variant = p->variant;
   info->num_variants = jacobi::num_variants();
-  info->cluster_ctas = (p->cluster_C && p->nblocks == 1 && p->colblocks == 1 && !p->comm) ? p->cluster_C : 0;
+  info->cluster_ctas =
+      (p->cluster_C && p->nblocks == 1 && p->colblocks == 1 && !p->comm && !p->p2p) ? p->cluster_C : 0;
   return 0;
 }
 
@@ -287,6 +393,7 @@ static jacobi::SweepArgs sweep_args(const jacobi_plan* p, int blk) {
   a.col0 = 0;
   a.cend = p->n;
   a.rsum = nullptr;
+  a.peers = nullptr;
   a.sq = p->sq + blk * mb;
   a.norm = p->norm;
   a.chunk = p->chunk;
@@ -299,6 +406,20 @@ static jacobi::SweepArgs sweep_args(const jacobi_plan* p, int blk) {
 // The sweep kernels of sweep j: row blocks (row-wise; P12a emulation when nblocks > 1), or column
 // slabs writing row sums (column-wise NEXT-4: this rank's slab, or the 1-GPU P-slab emulation).
 static int launch_gemv(jacobi_plan* p, int j) {
+  if (p->p2p) {  // NEXT-1 fused exchange: (virtual) rank r's launch reads and signals its own copies
+    const int nr = p->p2p_emul ? p->p2p : 1;
+    for (int r = 0; r < nr; ++r) {
+      jacobi::SweepArgs a = sweep_args(p, p->p2p_emul ? r : 0);
+      a.peers = p->peers_dev + r;
+      if (p->p2p_emul && r > 0) {
+        a.x0buf = p->ex_x + (size_t)(r - 1) * 2 * p->x_len;
+        a.x1buf = a.x0buf + p->x_len;
+        a.dslot = p->ex_dslot + (size_t)(r - 1) * 4;
+      }
+      JCUDA(jacobi::launch_sweep(p->dtype, p->variant, a, j, p->grid, p->stream));
+    }
+    return 0;
+  }
   if (!p->colwise && p->colblocks == 1) {
     for (int blk = 0; blk < p->nblocks; ++blk)
       JCUDA(jacobi::launch_sweep(p->dtype, p->variant, sweep_args(p, blk), j, p->grid, p->stream));
@@ -331,6 +452,7 @@ static int launch_gemv(jacobi_plan* p, int j) {
 // reduce-scatter (sum) of the row sums, the epilogue on the owned rows, and the max-allreduce.
 static int enqueue_sweep(jacobi_plan* p, int j) {
   JRC(launch_gemv(p, j));
+  if (p->p2p) return 0;  // the exchange happened inside the sweep kernel
   if (p->colwise) {
     JNCCL(ncclReduceScatter(p->rsum, p->rs_own, (size_t)p->m, ncclDouble, ncclSum, p->comm, p->stream));
     JCUDA(jacobi::launch_colsum_epilogue(p->rs_own, 1, p->m, p->m, p->row0, p->b, p->diag, p->x[0], p->x[1],
@@ -405,8 +527,15 @@ static int solve_prepare(jacobi_plan* p, const double* b, const double* x0, bool
   JCUDA(cudaMemcpyAsync(p->b, b, (size_t)p->m * 8, kind, p->stream));
   JCUDA(cudaMemcpyAsync(p->x[0], x0, (size_t)p->n * 8, kind, p->stream));
   JCUDA(cudaMemsetAsync(p->st, 0, sizeof(jacobi::State), p->stream));
-  JCUDA(jacobi::launch_prepare(p->st, max_iter, tol, hist_dev, p->dslot, p->cnt, p->m, p->b, p->m, p->x[0], p->n,
-                               p->stream));
+  JCUDA(jacobi::launch_prepare(p->st, max_iter, tol, hist_dev, p->dslot, p->cnt, p->a_rows, p->b, p->m, p->x[0],
+                               p->n, p->p2p ? p->flags : nullptr, p->stream));
+  if (p->p2p_emul) {  // virtual ranks 1..P-1: their x^(0), slots and counters
+    for (int r = 1; r < p->p2p; ++r)
+      JCUDA(cudaMemcpyAsync(p->ex_x + (size_t)(r - 1) * 2 * p->x_len, p->x[0], (size_t)p->n * 8,
+                            cudaMemcpyDeviceToDevice, p->stream));
+    JCUDA(cudaMemsetAsync(p->ex_dslot, 0, (size_t)(p->p2p - 1) * 4 * 8, p->stream));
+    JCUDA(cudaMemsetAsync(p->ex_flags, 0, (size_t)(p->p2p - 1) * 2 * 8, p->stream));
+  }
   if (p->comm)
     JNCCL(ncclAllReduce(&p->st->nonfinite, &p->st->nonfinite, 1, ncclInt32, ncclMax, p->comm, p->stream));
   return 0;
@@ -515,7 +644,7 @@ static int solve_impl(jacobi_plan* p, const double* b, const double* x0, bool de
     if (p->st_host[0].nonfinite) return nonfinite_error();
     fin.status = JACOBI_MAX_ITER;
     fin.iters = 0;
-  } else if (p->cluster_C && p->nblocks == 1 && p->colblocks == 1 && !p->comm) {
+  } else if (p->cluster_C && p->nblocks == 1 && p->colblocks == 1 && !p->comm && !p->p2p) {
     rc = solve_cluster(p, max_iter, &fin);
     if (rc) return rc;
   } else {
@@ -564,6 +693,7 @@ extern "C" int jacobi_plan_time_sweeps(jacobi_plan* p, const double* d_b, const 
     rc = launch_gemv(p, j);  // the sweep kernel(s) alone are timed
     cudaEventRecord(e1, p->stream);
     if (rc == 0) rc = [&]() -> int {  // the rest of the sweep (exchange, column-wise epilogue)
+      if (p->p2p) return 0;           // fused exchange: nothing outside the kernel
       if (p->colwise) {
         JNCCL(ncclReduceScatter(p->rsum, p->rs_own, (size_t)p->m, ncclDouble, ncclSum, p->comm, p->stream));
         JCUDA(jacobi::launch_colsum_epilogue(p->rs_own, 1, p->m, p->m, p->row0, p->b, p->diag, p->x[0], p->x[1],

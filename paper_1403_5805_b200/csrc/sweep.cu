@@ -57,10 +57,24 @@ __device__ __forceinline__ void ld_x(const double* p, double (&v)[E]) {
 
 // Prologue of sweep k (PAPER.md:64-66 evaluated on the device): decides whether sweep k runs.
 // Every CTA evaluates the same inputs and reaches the same decision; only the leader writes.
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ bool sweep_prologue(const SweepArgs& a, int j, bool leader) {
   State* st = a.st;
   if (*(volatile int32_t*)&st->done || st->nonfinite) return false;
   const int64_t k = st->kbase + j + 1;
+  if (k >= 2 && a.peers) {
+    // NEXT-1: wait until every CTA of every rank has pushed its x^(k-1) rows and max|dx| bits here.
+    const PeerArgs* pe = a.peers;
+    const unsigned long long kp = (unsigned long long)(k - 1);
+    const unsigned long long target = ((kp + (kp & 1)) / 2) * pe->total_ctas;  // sweeps of this parity
+    const unsigned long long* f = pe->flags[pe->rank] + (kp & 1);
+    while (ld_acquire_sys(f) < target) __nanosleep(64);
+  }
   if (k >= 2) {
     const double d = __longlong_as_double((long long)a.dslot[(k - 1) & 3]);
     if (leader && st->hist) st->hist[k - 2] = d;
@@ -285,19 +299,21 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
       const int64_t row = r0 + lane;
       if (a.rsum) {  // column-wise partial product of this slab (epilogue after the reduction)
         a.rsum[row] = s;
-        goto tile_done;
-      }
-      {
-      const double xnew = __ddiv_rn(__dsub_rn(a.b[row], s), a.diag[row]);
-      const int64_t gi = a.row0 + row;
-      const double dx = __dsub_rn(xnew, xo[gi]);
-      xn[gi] = xnew;
-      const unsigned long long bits = (unsigned long long)__double_as_longlong(dx) & 0x7fffffffffffffffull;
-      dmax = bits > dmax ? bits : dmax;
-      if (a.norm == JACOBI_NORM_L2) a.sq[row] = __dmul_rn(dx, dx);
+      } else {
+        const double xnew = __ddiv_rn(__dsub_rn(a.b[row], s), a.diag[row]);
+        const int64_t gi = a.row0 + row;
+        const double dx = __dsub_rn(xnew, xo[gi]);
+        if (a.peers) {  // NEXT-1: push x_i^(k) into every rank's x^(k) buffer (NVLink stores)
+          const PeerArgs* pe = a.peers;
+          for (int p = 0; p < pe->P; ++p) ((k & 1) ? pe->x1[p] : pe->x0[p])[gi] = xnew;
+        } else {
+          xn[gi] = xnew;
+        }
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(dx) & 0x7fffffffffffffffull;
+        dmax = bits > dmax ? bits : dmax;
+        if (a.norm == JACOBI_NORM_L2) a.sq[row] = __dmul_rn(dx, dx);
       }
     }
-  tile_done:
     __syncwarp();
     if (lane == 0) mbar_arrive(&s_empty[q]);
   };
@@ -338,7 +354,19 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
     const unsigned long long o = __shfl_xor_sync(kFull, dmax, off);
     dmax = o > dmax ? o : dmax;
   }
-  if (lane == 0) atomicMax(&a.dslot[k & 3], dmax);
+  if (!a.peers) {
+    if (lane == 0) atomicMax(&a.dslot[k & 3], dmax);
+    return;
+  }
+  // NEXT-1: max|dx| bits into every rank's slot, then (after a system fence) one arrival per CTA on
+  // every rank's counter for this parity; the next sweep's prologue waits for all of them.
+  const PeerArgs* pe = a.peers;
+  if (lane == 0)
+    for (int p = 0; p < pe->P; ++p) atomicMax(pe->dslot[p] + (k & 3), dmax);
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int p = 0; p < pe->P; ++p) atomicAdd(pe->flags[p] + (k & 1), 1ull);
 }
 
 
@@ -448,7 +476,7 @@ __global__ void k_scan_A(const T* __restrict__ A, int64_t lda, int64_t m, int64_
 // when the host reads the final state).  The state was zeroed by a memset just before.
 __global__ void k_prepare(State* st, int64_t max_iter, double tol, double* hist, unsigned long long* dslot,
                           unsigned* cnt, int64_t ncnt, const double* __restrict__ b, int64_t m,
-                          const double* __restrict__ x0, int64_t n) {
+                          const double* __restrict__ x0, int64_t n, unsigned long long* flags) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
   if (tid == 0) {
     st->max_iter = max_iter;
@@ -456,6 +484,7 @@ __global__ void k_prepare(State* st, int64_t max_iter, double tol, double* hist,
     st->hist = hist;
   }
   if (tid < 4) dslot[tid] = 0ull;
+  if (flags && tid < 2) flags[tid] = 0ull;
   for (int64_t i = tid; i < ncnt; i += stride) cnt[i] = 0u;
   bool bad = false;
   for (int64_t i = tid; i < m; i += stride) bad |= nonfinite(b[i]);
@@ -616,9 +645,9 @@ cudaError_t launch_scan_nonfinite_A(int dtype, const void* A, int64_t lda, int64
 
 cudaError_t launch_prepare(State* st, int64_t max_iter, double tol, double* hist, unsigned long long* dslot,
                            unsigned* cnt, int64_t ncnt, const double* b, int64_t m, const double* x0, int64_t n,
-                           cudaStream_t s) {
+                           unsigned long long* flags, cudaStream_t s) {
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((std::max(n, ncnt) + 255) / 256, 592));
-  k_prepare<<<grid, 256, 0, s>>>(st, max_iter, tol, hist, dslot, cnt, ncnt, b, m, x0, n);
+  k_prepare<<<grid, 256, 0, s>>>(st, max_iter, tol, hist, dslot, cnt, ncnt, b, m, x0, n, flags);
   return cudaGetLastError();
 }
 

@@ -19,9 +19,20 @@ def bootstrap(n: int):
     return obj[0], rank, world, row0, rows
 
 
-def dist_plan(A_rows, n: int, stream=None) -> Plan:
-    """Distributed plan over this rank's row block A_rows (torch CUDA tensor, borrowed, or numpy)."""
+def dist_plan(A_block, n: int, stream=None, layout: str = "rows", p2p: bool = False) -> Plan:
+    """Distributed plan over this rank's block (torch CUDA tensor, borrowed, or numpy): its row block
+    (layout="rows", §3.1) or its n x m column slab (layout="cols", §3.2).  p2p=True switches
+    a row-wise plan to the fused NVLink exchange (NEXT-1): the CUDA IPC handles of every rank's x
+    buffers, slots and counters are all-gathered through torch.distributed and mapped."""
+    import torch.distributed as dist
     uid, rank, world, row0, rows = bootstrap(n)
-    if A_rows.shape[0] != rows:
-        raise ValueError(f"rank {rank} must pass rows [{row0}, {row0 + rows}) ({rows} rows), got {A_rows.shape[0]}")
-    return Plan(A_rows, n=n, stream=stream, dist=(uid, rank, world))
+    want = rows if layout == "rows" else n
+    if A_block.shape[0] != want:
+        raise ValueError(f"rank {rank}: expected {want} rows in its {layout} block, got {A_block.shape[0]}")
+    plan = Plan(A_block, n=n, stream=stream, dist=(uid, rank, world), layout=layout)
+    if p2p:
+        mine = plan.ipc_export()
+        allh = [None] * world
+        dist.all_gather_object(allh, mine)
+        plan.ipc_attach(b"".join(allh))
+    return plan

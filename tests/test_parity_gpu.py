@@ -443,3 +443,38 @@ def test_colwise_emulated_slabs_and_single_rank(jb):
             rc = p.solve(b, None, 3000, 1e-10, history=True)
             assert (rc.status, rc.iters) == (ref.status, ref.iters)
             assert np.array_equal(rc.x, ref.x) and np.array_equal(rc.hist, ref.hist)
+
+
+# ------------------------------------------------------------------ NEXT-1: fused NVLink exchange (emulated ranks)
+def test_fused_exchange_emulated_ranks_bitwise(jb):
+    """P ranks emulated on one GPU (per-rank x copies, slots and arrival counters; the ranks' sweep
+    kernels push x_i^(k) into every copy, fold max|dx| into every slot with atomics and bump every
+    counter; the next sweep waits on its own counter).  Must equal the plain plan bit for bit."""
+    import torch
+    for n, scale in ((8192, 1.05), (16384, 1.02)):
+        A, b, _ = dominant(n, 111 + n, scale=scale)
+        x0 = np.random.default_rng(n).uniform(-1, 1, n)
+        with jb.Plan(A) as p:
+            ref = p.solve(b, x0, 40, 0.0, history=True)
+            ref2 = p.solve(b, x0, 3000, 1e-11, history=True)
+        for P in (1, 2, 4, 8):
+            with jb.Plan(A) as p:
+                p.set_p2p_emulation(P)
+                for K in (4, 32):
+                    p.set_batch(K)
+                    r = p.solve(b, x0, 40, 0.0, history=True)
+                    assert r.iters == 40 and np.array_equal(r.x, ref.x) and np.array_equal(r.hist, ref.hist), (n, P, K)
+                    r2 = p.solve(b, x0, 3000, 1e-11, history=True)
+                    assert (r2.status, r2.iters) == (ref2.status, ref2.iters) and np.array_equal(r2.x, ref2.x), (n, P)
+                with pytest.raises(jb.JacobiError):
+                    p.set_norm("l2")  # max norm only
+    # the real IPC path with a single rank (own handles only)
+    A, b, _ = dominant(8192, 5, scale=1.05)
+    with jb.Plan(A) as p0:
+        ref = p0.solve(b, None, 3000, 1e-11, history=True)
+    dA = torch.from_numpy(A).cuda()
+    with jb.Plan(dA, n=8192, dist=(jb.nccl_unique_id(), 0, 1)) as p:
+        p.ipc_attach(p.ipc_export())
+        r = p.solve(b, None, 3000, 1e-11, history=True)
+        assert (r.status, r.iters) == (ref.status, ref.iters) and np.array_equal(r.x, ref.x)
+        assert np.array_equal(r.hist, ref.hist)
