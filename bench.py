@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU oracle sample budget per run")
+    ap.add_argument("--exchange", choices=["nccl", "p2p", "cols"], default="nccl",
+                    help="N > 1: NCCL row-wise (default), fused NVLink push (NEXT-1), or column-wise (NEXT-4)")
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
     return ap.parse_args()
 
@@ -207,15 +209,29 @@ def main():
     row0, m = jb.partition(n, world, rank)
 
     # ---- resident inputs (device twin of the generator; identical bits to the host generator)
-    dA = torch.empty((m, n), dtype=dt, device="cuda")
+    cols = world > 1 and args.exchange == "cols"
     db = torch.empty(m, dtype=torch.float64, device="cuda")
-    g.device_rows(cfg, row0, row0 + m, dA.data_ptr(), n, db.data_ptr(), sh)
+    if cols:  # column slab [row0, row0 + m) of all n rows: generate all rows, keep the slab
+        dA = torch.empty((n, m), dtype=dt, device="cuda")
+        tmp = torch.empty((4096, n), dtype=dt, device="cuda")
+        tb = torch.empty(4096, dtype=torch.float64, device="cuda")
+        for r in range(0, n, 4096):
+            g.device_rows(cfg, r, min(n, r + 4096), tmp.data_ptr(), n, tb.data_ptr(), sh)
+            dA[r:r + 4096].copy_(tmp[: min(4096, n - r), row0:row0 + m])
+            if row0 <= r < row0 + m or r <= row0 < r + 4096:
+                lo, hi = max(r, row0), min(r + 4096, row0 + m)
+                if lo < hi:
+                    db[lo - row0:hi - row0].copy_(tb[lo - r:hi - r])
+        del tmp, tb
+    else:
+        dA = torch.empty((m, n), dtype=dt, device="cuda")
+        g.device_rows(cfg, row0, row0 + m, dA.data_ptr(), n, db.data_ptr(), sh)
     dx0 = torch.zeros(n, dtype=torch.float64, device="cuda")
     dxo = torch.empty(n, dtype=torch.float64, device="cuda")
     torch.cuda.synchronize()
     if world > 1:
         from paper_1403_5805_b200.dist import dist_plan
-        plan = dist_plan(dA, n, stream=sh)
+        plan = dist_plan(dA, n, stream=sh, layout="cols" if cols else "rows", p2p=args.exchange == "p2p")
     else:
         plan = jb.Plan(dA, n=n, stream=sh)
     K = 20 if sweeps % 20 == 0 else 4
@@ -329,7 +345,9 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded counter-based generator, BASELINE.json recipe; device twin)",
             "config": {"workload": desc, "n": n, "sweeps_per_step": sweeps, "tol": tol,
-                       "parallelism": f"row-block x{world}" + (" + NCCL allgather/allreduce" if world > 1 else ""),
+                       "parallelism": (f"row-block x{world}" if not cols else f"column-slab x{world}") + (
+                           {"nccl": " + NCCL allgather/allreduce", "p2p": " + fused NVLink push exchange (NEXT-1)",
+                            "cols": " + NCCL reduce-scatter/allreduce (NEXT-4)"}[args.exchange] if world > 1 else ""),
                        "l2": "A per GPU >> 126 MB L2; each sweep streams A from HBM (no flush needed)",
                        "graph_batch": K, "chunk_cols": info.chunk_cols, "rows_per_warp": info.rows_per_warp,
                        "grid": f"{info.grid_ctas}x{info.threads_per_cta}"},
