@@ -76,6 +76,8 @@ cudaError_t launch_copy_pitched(int dtype, const void* src, int64_t src_ld, void
 int num_variants();
 int default_variant(int dtype, int nchunks, int chunk);
 bool variant_is_cta(int variant);
+bool variant_is_push(int variant);
+int push_variant();
 bool variant_fits(int variant, int nchunks, int dtype, int chunk);
 int variant_rows_dt(int variant, int dtype);
 int variant_rows(int variant);

@@ -74,7 +74,9 @@ static void choose_variant(const jacobi_plan* p, int64_t ncols, int* variant, in
   int v = jacobi::default_variant(p->dtype, nch, p->chunk);
   if (const char* e = getenv("JACOBI_SWEEP_VARIANT")) {  // tuning override (all variants: same bits)
     const int vi = atoi(e);
-    if (vi >= 0 && vi < jacobi::num_variants() && jacobi::variant_fits(vi, nch, p->dtype, p->chunk)) v = vi;
+    if (vi >= 0 && vi < jacobi::num_variants() && !jacobi::variant_is_push(vi) &&
+        jacobi::variant_fits(vi, nch, p->dtype, p->chunk))
+      v = vi;
   }
   *variant = v;
   *grid = jacobi::sweep_grid(p->dtype, v, p->num_sms, nch, p->chunk);
@@ -234,16 +236,13 @@ extern "C" int jacobi_plan_set_col_blocks(jacobi_plan* p, int nblocks) {
 
 // NEXT-1 helpers --------------------------------------------------------------------------------
 static int p2p_pick_variant(jacobi_plan* p) {
-  if (jacobi::variant_is_cta(p->variant)) return 0;
   const int nch = (int)((p->n + p->chunk - 1) / p->chunk);
-  for (int v : {9, 7, 6}) {
-    if (jacobi::variant_fits(v, nch, p->dtype, p->chunk)) {
-      p->variant = v;
-      p->grid = jacobi::sweep_grid(p->dtype, v, p->num_sms, nch, p->chunk);
-      return check_last("fused-exchange variant");
-    }
-  }
-  return jacobi_set_error(JACOBI_EINVAL, "fused exchange needs the CTA sweep kernel (n with >= 16 chunks)");
+  const int v = jacobi::push_variant();
+  if (!jacobi::variant_fits(v, nch, p->dtype, p->chunk))
+    return jacobi_set_error(JACOBI_EINVAL, "fused exchange needs the CTA sweep kernel (n with >= 16 chunks)");
+  p->variant = v;
+  p->grid = jacobi::sweep_grid(p->dtype, v, p->num_sms, nch, p->chunk);
+  return check_last("fused-exchange variant");
 }
 
 extern "C" int jacobi_plan_set_p2p_emulation(jacobi_plan* p, int P) {

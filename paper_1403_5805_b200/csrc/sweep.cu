@@ -260,7 +260,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
 
 constexpr int kSlots = 4;
 
-template <typename T, int R, int NW, int U = 1, int XL = 0>
+template <typename T, int R, int NW, int U = 1, int XL = 0, bool PUSH = false>
 __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, const int j) {
   extern __shared__ __align__(16) double s_part[];  // [kSlots][nchunks][R]
   __shared__ __align__(8) uint64_t s_full[kSlots], s_empty[kSlots];
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
         const double xnew = __ddiv_rn(__dsub_rn(a.b[row], s), a.diag[row]);
         const int64_t gi = a.row0 + row;
         const double dx = __dsub_rn(xnew, xo[gi]);
-        if (a.peers) {  // NEXT-1: push x_i^(k) into every rank's x^(k) buffer (NVLink stores)
+        if constexpr (PUSH) {  // NEXT-1: push x_i^(k) into every rank's x^(k) buffer (NVLink stores)
           const PeerArgs* pe = a.peers;
           for (int p = 0; p < pe->P; ++p) ((k & 1) ? pe->x1[p] : pe->x0[p])[gi] = xnew;
         } else {
@@ -354,19 +354,19 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
     const unsigned long long o = __shfl_xor_sync(kFull, dmax, off);
     dmax = o > dmax ? o : dmax;
   }
-  if (!a.peers) {
+  if constexpr (!PUSH) {
     if (lane == 0) atomicMax(&a.dslot[k & 3], dmax);
-    return;
+  } else {
+    // NEXT-1: max|dx| bits into every rank's slot, then (after a system fence) one arrival per CTA on
+    // every rank's counter for this parity; the next sweep's prologue waits for all of them.
+    const PeerArgs* pe = a.peers;
+    if (lane == 0)
+      for (int p = 0; p < pe->P; ++p) atomicMax(pe->dslot[p] + (k & 3), dmax);
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int p = 0; p < pe->P; ++p) atomicAdd(pe->flags[p] + (k & 1), 1ull);
   }
-  // NEXT-1: max|dx| bits into every rank's slot, then (after a system fence) one arrival per CTA on
-  // every rank's counter for this parity; the next sweep's prologue waits for all of them.
-  const PeerArgs* pe = a.peers;
-  if (lane == 0)
-    for (int p = 0; p < pe->P; ++p) atomicMax(pe->dslot[p] + (k & 3), dmax);
-  __threadfence_system();
-  __syncthreads();
-  if (threadIdx.x == 0)
-    for (int p = 0; p < pe->P; ++p) atomicAdd(pe->flags[p] + (k & 1), 1ull);
 }
 
 
@@ -544,6 +544,9 @@ const Variant kVariants[] = {
     {8, 256, 1, 1, 1, k_sweep_cta<double, 8, 8>, k_sweep_cta<float, 4, 8>},
     {4, 512, 1, 2, 2, k_sweep_cta<double, 4, 16, 2>, k_sweep_cta<float, 4, 16, 2>},
     {2, 512, 1, 4, 2, k_sweep_cta<double, 2, 16, 4>, k_sweep_cta<float, 2, 16, 2>},
+    // fused-exchange (NEXT-1) instances of the defaults; selected only by jacobi_plan_ipc_attach /
+    // jacobi_plan_set_p2p_emulation (they need SweepArgs.peers)
+    {4, 512, 2, 2, 1, k_sweep_cta<double, 4, 16, 2, 0, true>, k_sweep_cta<float, 4, 16, 1, 0, true>},
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
@@ -551,10 +554,11 @@ constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 int num_variants() { return kNumVariants; }
 bool variant_is_cta(int v) { return kVariants[v].cta != 0; }
+int push_variant() { return 11; }
 // Shared memory of a variant: the CTA kernel's partial slots.
 size_t variant_smem(int v, int nchunks, int /*dtype*/, int /*chunk*/) {
   const Variant& V = kVariants[v];
-  return V.cta ? (size_t)kSlots * nchunks * V.R * 8 : 0;
+  return V.cta ? (size_t)kSlots * nchunks * V.R * 8 : 0;  // cta = 1 or 2 (fused exchange)
 }
 bool variant_fits(int v, int nchunks, int dtype, int chunk) {
   const Variant& V = kVariants[v];
@@ -562,6 +566,7 @@ bool variant_fits(int v, int nchunks, int dtype, int chunk) {
   if (chunk % step_cols != 0) return false;
   return !V.cta || (nchunks >= V.threads / 32 && variant_smem(v, nchunks, dtype, chunk) <= 48 * 1024);
 }
+bool variant_is_push(int v) { return kVariants[v].cta == 2; }
 int variant_rows_dt(int v, int /*dtype*/) { return kVariants[v].R; }
 // Defaults from B200 measurements (profiles/variants5_r01_*.jsonl, sustained 100-sweep graph solves):
 // the CTA-cooperative kernel when n has at least 16 chunks — fp64 R=4 with 2 steps in flight (c4:
