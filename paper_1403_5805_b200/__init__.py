@@ -38,7 +38,7 @@ EXPORTS = ("jacobi_solve", "jacobi_solve_f32a", "jacobi_plan_create", "jacobi_pl
 # Sweep kernel variants compiled into libjacobi.so (csrc/sweep.cu kVariants; all bitwise identical).
 VARIANT_NAMES = ("k_sweep R4 U2", "k_sweep R8 U1", "k_sweep R2 U4", "k_sweep R4 U1", "k_sweep R4 U2 256t",
                  "k_sweep R2 U1 1024t", "k_sweep_cta R8 U1", "k_sweep_cta R4 U1", "k_sweep_cta R8 U1 256t",
-                 "k_sweep_cta R4 U2", "k_sweep_cta R2 U4", "k_sweep_cta R4 U2 fused-exchange")
+                 "k_sweep_cta R4 U2", "k_sweep_cta R2 U4", "k_sweep_cta R4 U1 fused-exchange")
 
 
 class JacobiError(RuntimeError):

@@ -546,7 +546,7 @@ const Variant kVariants[] = {
     {2, 512, 1, 4, 2, k_sweep_cta<double, 2, 16, 4>, k_sweep_cta<float, 2, 16, 2>},
     // fused-exchange (NEXT-1) instances of the defaults; selected only by jacobi_plan_ipc_attach /
     // jacobi_plan_set_p2p_emulation (they need SweepArgs.peers)
-    {4, 512, 2, 2, 1, k_sweep_cta<double, 4, 16, 2, 0, true>, k_sweep_cta<float, 4, 16, 1, 0, true>},
+    {4, 512, 2, 1, 1, k_sweep_cta<double, 4, 16, 1, 0, true>, k_sweep_cta<float, 4, 16, 1, 0, true>},
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
@@ -568,12 +568,13 @@ bool variant_fits(int v, int nchunks, int dtype, int chunk) {
 }
 bool variant_is_push(int v) { return kVariants[v].cta == 2; }
 int variant_rows_dt(int v, int /*dtype*/) { return kVariants[v].R; }
-// Defaults from B200 measurements (profiles/variants5_r01_*.jsonl, sustained 100-sweep graph solves):
-// the CTA-cooperative kernel when n has at least 16 chunks — fp64 R=4 with 2 steps in flight (c4:
-// 7178 GB/s sustained, 7232 burst), fp32 R=4 (c5: 6734 burst) — else the item kernel R=8,U=1 (fp64)
-// or R=4,U=1 (fp32).
+// Defaults from B200 measurements (profiles/variants*_r01_*.jsonl, sustained 100-sweep graph solves):
+// the CTA-cooperative kernel R=4 when n has at least 16 chunks (c4 fp64: 7257 GB/s burst, 7153
+// sustained; c5 fp32: 6734 burst), else the item kernel R=8,U=1 (fp64) or R=4,U=1 (fp32).  The U=2
+// instance (variant 9) measured 7275/7186 before the column-range generalisation and 7063/7033 after
+// (it sits at the 128-register cap, so its schedule is fragile); U=1 kept its speed.
 int default_variant(int dtype, int nchunks, int chunk) {
-  const int big = dtype == JACOBI_F32 ? 7 : 9;
+  const int big = 7;
   if (variant_fits(big, nchunks, dtype, chunk)) return big;
   return dtype == JACOBI_F32 ? 0 : 1;  // U = 1: fits every chunk
 }
