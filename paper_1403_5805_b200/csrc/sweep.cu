@@ -333,7 +333,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
       for (int r = 0; r < R; ++r) acc[r] = 0.0;
       const int64_t c0 = a.col0 + (int64_t)c * a.chunk;
       const int64_t c1 = min(c0 + (int64_t)a.chunk, a.cend);
-      accumulate_chunk<T, R, U, XL>(rowp, nv, xo, c0, c1, a.chunk, a.cend, g0, lane, acc);
+      // Full tiles take the constant-row-count instance: with a run-time row count nvcc wraps each
+      // row's load (and, for fp32, its converts) in a branch and keeps one A load in flight per warp
+      // (c5 fell to 3.97 TB/s); with nv = R the loads are unconditional and software-pipelined.
+      if (nv == R) accumulate_chunk<T, R, U, XL>(rowp, R, xo, c0, c1, a.chunk, a.cend, g0, lane, acc);
+      else accumulate_chunk<T, R, U, XL>(rowp, nv, xo, c0, c1, a.chunk, a.cend, g0, lane, acc);
 #pragma unroll
       for (int r = 0; r < R; ++r)
 #pragma unroll
