@@ -37,7 +37,10 @@
  *     number of ranks / row blocks (the per-row summation order depends only on column indices).
  *   - Threading: a plan is used by one host thread at a time; distinct plans are independent.
  *   - Streams: cuda_stream (a cudaStream_t, may be NULL) is the stream every kernel, copy and NCCL
- *     call of the plan is issued on; NULL makes the plan create its own non-blocking stream.
+ *     call of the plan is issued on; NULL makes the plan create its own stream, a blocking one
+ *     (ordered with the legacy default stream, where device inputs written on stream 0 — torch's
+ *     default stream — are complete before the plan reads them).  Device inputs written on any
+ *     other stream must be complete, or ordered before the call on cuda_stream, by the caller.
  *     Functions return after the work they enqueue has completed (they synchronize that stream).
  */
 #ifndef JACOBI_H

@@ -59,6 +59,7 @@ struct SweepArgs {
   int chunk;                // columns per work item (multiple of 512, depends on n only)
   int nchunks;              // ceil(n / chunk)
   int tiles;                // ceil(m / R)
+  int l2_keep_pm;           // per-mille of the rows loaded with L2 evict_last (variants with POL)
 };
 
 // Launchers (sweep.cu).  Return cudaGetLastError() of the launch.
@@ -74,7 +75,8 @@ cudaError_t launch_prepare(State* st, int64_t max_iter, double tol, double* hist
 cudaError_t launch_copy_pitched(int dtype, const void* src, int64_t src_ld, void* dst, int64_t dst_ld,
                                 int64_t rows, int64_t n, cudaStream_t s);
 int num_variants();
-int default_variant(int dtype, int nchunks, int chunk);
+int default_variant(int dtype, int nchunks, int chunk, bool l2_keep);
+bool variant_uses_l2_keep(int variant);
 bool variant_is_cta(int variant);
 bool variant_is_push(int variant);
 int push_variant();
@@ -126,6 +128,7 @@ struct jacobi_plan {
   std::vector<void*> ipc_open;   // opened peer mappings (closed at destroy)
   int variant = 0;               // sweep kernel variant (R, U, threads); default per dtype, JACOBI_SWEEP_VARIANT overrides
   int batch = 32;                // sweeps per graph batch
+  int l2_keep_pm = 0;            // per-mille of A rows kept L2-resident (evict_last) by the POL variants
   int norm = JACOBI_NORM_MAX;    // distance of the stop test
   int cluster_C = 0;             // > 0: small-n solves run in one cluster launch (cluster.cu)
   size_t cluster_smem = 0;

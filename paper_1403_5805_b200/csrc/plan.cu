@@ -71,7 +71,7 @@ static int check_last(const char* what) {
 // JACOBI_SWEEP_VARIANT override is honoured when the variant can tile the chunking).
 static void choose_variant(const jacobi_plan* p, int64_t ncols, int* variant, int* grid) {
   const int nch = (int)((ncols + p->chunk - 1) / p->chunk);
-  int v = jacobi::default_variant(p->dtype, nch, p->chunk);
+  int v = jacobi::default_variant(p->dtype, nch, p->chunk, p->l2_keep_pm > 0);
   if (const char* e = getenv("JACOBI_SWEEP_VARIANT")) {  // tuning override (all variants: same bits)
     const int vi = atoi(e);
     if (vi >= 0 && vi < jacobi::num_variants() && !jacobi::variant_is_push(vi) &&
@@ -101,7 +101,9 @@ int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dty
   if (stream) {
     p->stream = (cudaStream_t)stream;
   } else {
-    JCUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    // A blocking stream: ordered with the legacy default stream, so device buffers the caller filled
+    // there (e.g. torch's default stream, handle 0) are complete before the plan reads them.
+    JCUDA(cudaStreamCreateWithFlags(&p->stream, cudaStreamDefault));
     p->own_stream = true;
   }
   const int64_t elt = dtype == JACOBI_F32 ? 4 : 8;
@@ -126,6 +128,16 @@ int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dty
   }
   JLAST("A upload");
   p->chunk = jacobi::chunk_for(n, dtype);
+  // L2-resident share of A (sweep variants with POL): when the stored block is at most 4x the L2,
+  // keep ~59 % of the L2 (74 MB of 126 MB: the measured optimum at c2) of it across sweeps with
+  // evict_last loads and stream the rest with evict_first.  JACOBI_L2_KEEP (per mille) overrides.
+  {
+    int l2 = 0;
+    JCUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, p->device));
+    const double a_bytes = (double)a_rows * (double)a_cols * (dtype == JACOBI_F32 ? 4.0 : 8.0);
+    if (l2 > 0 && a_bytes <= 4.0 * l2) p->l2_keep_pm = (int)std::min(1000.0, 1000.0 * 0.59 * l2 / a_bytes);
+    if (const char* e = getenv("JACOBI_L2_KEEP")) p->l2_keep_pm = std::max(0, std::min(1000, atoi(e)));
+  }
   choose_variant(p, a_cols, &p->variant, &p->grid);
   JLAST("sweep kernel occupancy query");
   p->x_len = round_up(n, 256) + 256;
@@ -399,6 +411,7 @@ static jacobi::SweepArgs sweep_args(const jacobi_plan* p, int blk) {
   a.nchunks = (int)((p->n + p->chunk - 1) / p->chunk);
   const int R = jacobi::variant_rows_dt(p->variant, p->dtype);
   a.tiles = (int)((mb + R - 1) / R);
+  a.l2_keep_pm = p->l2_keep_pm;
   return a;
 }
 

@@ -40,6 +40,28 @@ __device__ __forceinline__ void ld_a(const float* p, float (&v)[8]) {
       : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
       : "l"(p));
 }
+// Same loads with an L2 eviction-priority policy (createpolicy): used to keep part of A resident in
+// L2 across sweeps when A is about the L2 size (c2: 134 MB vs 126 MB of L2).
+__device__ __forceinline__ void ld_a(const double* p, double (&v)[4], uint64_t pol) {
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+      : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ void ld_a(const float* p, float (&v)[8], uint64_t pol) {
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+      : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ uint64_t l2_policy(bool keep) {
+  uint64_t pol;
+  if (keep) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  else asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+template <bool POL, typename T, int E>
+__device__ __forceinline__ void ld_a_p(const T* p, T (&v)[E], uint64_t pol) {
+  if constexpr (POL) ld_a(p, v, pol);
+  else ld_a(p, v);
+}
 // x^(k-1) is read-only during the sweep (it lives in the other ping-pong buffer): L1-cached loads.
 template <int XL>
 __device__ __forceinline__ void ld_x4(const double* p, double* v) {
@@ -95,11 +117,12 @@ __device__ __forceinline__ bool sweep_prologue(const SweepArgs& a, int j, bool l
 // variant shares: lane l owns columns c0 + (32*s + l)*E + e, accumulated in ascending s then e with
 // one DFMA chain per row; j == i (the diagonal) and j >= n are skipped.  Rows r >= nv
 // are not loaded (their sums are unused).
-template <typename T, int R, int U, int XL = 0>
+template <typename T, int R, int U, int XL = 0, bool POL = false>
 __device__ __forceinline__ void accumulate_chunk(const T* const (&rowp)[R], const int nv,
                                                  const double* __restrict__ xo, const int64_t c0,
                                                  const int64_t c1, const int chunk, const int64_t n,
-                                                 const int64_t g0, const int lane, double (&acc)[R]) {
+                                                 const int64_t g0, const int lane, double (&acc)[R],
+                                                 const uint64_t pol = 0) {
   constexpr int E = VecOf<T>::E;
   constexpr int S = 32 * E;  // columns per warp step
   const int nsteps = chunk / S;
@@ -111,10 +134,10 @@ __device__ __forceinline__ void accumulate_chunk(const T* const (&rowp)[R], cons
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t col = c0 + (int64_t)((s + u) * 32 + lane) * E;
-        ld_x<E>(xo + col, xv[u]);
+        ld_x<E, XL>(xo + col, xv[u]);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          if (r < nv) ld_a(rowp[r] + col, av[u][r]);
+          if (r < nv) ld_a_p<POL>(rowp[r] + col, av[u][r], pol);
           else {
 #pragma unroll
             for (int e = 0; e < E; ++e) av[u][r][e] = T(0);
@@ -138,7 +161,7 @@ __device__ __forceinline__ void accumulate_chunk(const T* const (&rowp)[R], cons
         ld_x<E, XL>(xo + col, xv);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          if (r < nv) ld_a(rowp[r] + col, av[r]);
+          if (r < nv) ld_a_p<POL>(rowp[r] + col, av[r], pol);
           else {
 #pragma unroll
             for (int e = 0; e < E; ++e) av[r][e] = T(0);
@@ -260,7 +283,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
 
 constexpr int kSlots = 4;
 
-template <typename T, int R, int NW, int U = 1, int XL = 0, bool PUSH = false>
+template <typename T, int R, int NW, int U = 1, int XL = 0, bool PUSH = false, bool POL = false>
 __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, const int j) {
   extern __shared__ __align__(16) double s_part[];  // [kSlots][nchunks][R]
   __shared__ __align__(8) uint64_t s_full[kSlots], s_empty[kSlots];
@@ -327,6 +350,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
 #pragma unroll
     for (int r = 0; r < R; ++r) rowp[r] = A + (r0 + min(r, nv - 1)) * a.lda - a.col0;  // global columns
     const int64_t g0 = a.row0 + r0;
+    uint64_t pol = 0;  // POL: the first l2_keep_pm/1000 of the CTA's rows stay in L2 (evict_last)
+    if constexpr (POL) pol = l2_policy((r0 - rb) * 1000 < (re - rb) * (int64_t)a.l2_keep_pm);
     for (int c = w; c < nch; c += NW) {
       double acc[R];
 #pragma unroll
@@ -336,8 +361,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
       // Full tiles take the constant-row-count instance: with a run-time row count nvcc wraps each
       // row's load (and, for fp32, its converts) in a branch and keeps one A load in flight per warp
       // (c5 fell to 3.97 TB/s); with nv = R the loads are unconditional and software-pipelined.
-      if (nv == R) accumulate_chunk<T, R, U, XL>(rowp, R, xo, c0, c1, a.chunk, a.cend, g0, lane, acc);
-      else accumulate_chunk<T, R, U, XL>(rowp, nv, xo, c0, c1, a.chunk, a.cend, g0, lane, acc);
+      if (nv == R) accumulate_chunk<T, R, U, XL, POL>(rowp, R, xo, c0, c1, a.chunk, a.cend, g0, lane, acc, pol);
+      else accumulate_chunk<T, R, U, XL, POL>(rowp, nv, xo, c0, c1, a.chunk, a.cend, g0, lane, acc, pol);
 #pragma unroll
       for (int r = 0; r < R; ++r)
 #pragma unroll
@@ -371,6 +396,104 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
     if (threadIdx.x == 0)
       for (int p = 0; p < pe->P; ++p) atomicAdd(pe->flags[p] + (k & 1), 1ull);
   }
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// k_sweep_panel: every warp owns whole rows.  CTA b of G owns rows [b*m/G, (b+1)*m/G); warp w of NW
+// owns an equal share of them (balanced to one row) and walks its tiles of R rows across all column
+// chunks in ascending order, adding each chunk's butterfly sum to the row's running sum — exactly the
+// canonical order (s = chunk_0; s += chunk_c for c = 1, 2, ...) — and applies the fused epilogue
+// itself.  No shared memory, no barriers, no cross-warp handoff.  Because the CTA's warps march
+// across the same column chunks at the same rate, each x^(k-1) chunk is fetched from L2 once per CTA
+// and served to the other warps from L1 (in k_sweep_cta every warp reads a different chunk, so x
+// streams from L2 once per tile: +25 % of the A bytes for fp64, +50 % for fp32 A).
+template <typename T, int R, int U, int XL, bool POL, int NV>
+__device__ __forceinline__ void panel_tile(const SweepArgs& a, const T* A, const double* __restrict__ xo,
+                                           const int64_t r0, const int lane, double (&s)[R], const uint64_t pol) {
+  const T* rowp[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) rowp[r] = A + (r0 + (r < NV ? r : NV - 1)) * a.lda - a.col0;
+  const int64_t g0 = a.row0 + r0;
+  for (int c = 0; c < a.nchunks; ++c) {
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+    const int64_t c0 = a.col0 + (int64_t)c * a.chunk;
+    const int64_t c1 = min(c0 + (int64_t)a.chunk, a.cend);
+    accumulate_chunk<T, R, U, XL, POL>(rowp, NV, xo, c0, c1, a.chunk, a.cend, g0, lane, acc, pol);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc[r] += __shfl_xor_sync(kFull, acc[r], off);
+      s[r] = c == 0 ? acc[r] : s[r] + acc[r];
+    }
+  }
+}
+
+// Row count nv in [1, R] as a compile-time constant (a run-time count serialises the loads, see
+// k_sweep_cta).
+template <typename T, int R, int U, int XL, bool POL, int NV = R>
+__device__ __forceinline__ void panel_tile_nv(const int nv, const SweepArgs& a, const T* A,
+                                              const double* __restrict__ xo, const int64_t r0, const int lane,
+                                              double (&s)[R], const uint64_t pol) {
+  if constexpr (NV == 1) {
+    panel_tile<T, R, U, XL, POL, 1>(a, A, xo, r0, lane, s, pol);
+  } else {
+    if (nv == NV) panel_tile<T, R, U, XL, POL, NV>(a, A, xo, r0, lane, s, pol);
+    else panel_tile_nv<T, R, U, XL, POL, NV - 1>(nv, a, A, xo, r0, lane, s, pol);
+  }
+}
+
+// POL: rows in the first l2_keep_pm/1000 of each warp's share are loaded with L2 evict_last (kept
+// resident across sweeps), the rest with evict_first.
+template <typename T, int R, int NW, int U = 1, int XL = 0, bool POL = false>
+__global__ void __launch_bounds__(NW * 32, 1) k_sweep_panel(const SweepArgs a, const int j) {
+  __shared__ int s_go;
+  if (threadIdx.x == 0) s_go = sweep_prologue(a, j, blockIdx.x == 0);
+  __syncthreads();
+  if (!s_go) return;
+
+  const int64_t k = a.st->kbase + j + 1;
+  const double* __restrict__ xo = (k & 1) ? a.x0buf : a.x1buf;  // x^(k-1)
+  double* __restrict__ xn = (k & 1) ? a.x1buf : a.x0buf;        // x^(k)
+  const T* __restrict__ A = static_cast<const T*>(a.A);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t rb = (int64_t)blockIdx.x * a.m / gridDim.x;
+  const int64_t re = (int64_t)(blockIdx.x + 1) * a.m / gridDim.x;
+  const int64_t wb = rb + (re - rb) * w / NW, we = rb + (re - rb) * (w + 1) / NW;
+  unsigned long long dmax = 0ull;
+  for (int64_t r0 = wb; r0 < we; r0 += R) {
+    const int nv = (int)min((int64_t)R, we - r0);
+    double s[R];
+    uint64_t pol = 0;
+    if constexpr (POL) pol = l2_policy((r0 - wb) * 1000 < (we - wb) * (int64_t)a.l2_keep_pm);
+    panel_tile_nv<T, R, U, XL, POL>(nv, a, A, xo, r0, lane, s, pol);
+    double mine = s[0];
+#pragma unroll
+    for (int r = 1; r < R; ++r)
+      if (lane == r) mine = s[r];
+    if (lane < nv) {
+      const int64_t row = r0 + lane;
+      if (a.rsum) {  // column-wise partial product of this slab (epilogue after the reduction)
+        a.rsum[row] = mine;
+      } else {
+        const double xnew = __ddiv_rn(__dsub_rn(a.b[row], mine), a.diag[row]);
+        const int64_t gi = a.row0 + row;
+        const double dx = __dsub_rn(xnew, xo[gi]);
+        xn[gi] = xnew;
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(dx) & 0x7fffffffffffffffull;
+        dmax = bits > dmax ? bits : dmax;
+        if (a.norm == JACOBI_NORM_L2) a.sq[row] = __dmul_rn(dx, dx);
+      }
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const unsigned long long o = __shfl_xor_sync(kFull, dmax, off);
+    dmax = o > dmax ? o : dmax;
+  }
+  if (lane == 0 && dmax) atomicMax(&a.dslot[k & 3], dmax);
 }
 
 
@@ -551,6 +674,14 @@ const Variant kVariants[] = {
     // fused-exchange (NEXT-1) instances of the defaults; selected only by jacobi_plan_ipc_attach /
     // jacobi_plan_set_p2p_emulation (they need SweepArgs.peers)
     {4, 512, 2, 1, 1, k_sweep_cta<double, 4, 16, 1, 0, true>, k_sweep_cta<float, 4, 16, 1, 0, true>},
+    // row-panel kernel (cta = 3): warps own whole rows, x chunks shared through L1
+    {4, 512, 3, 1, 1, k_sweep_panel<double, 4, 16>, k_sweep_panel<float, 4, 16>},
+    {4, 512, 3, 1, 1, k_sweep_panel<double, 4, 16, 1, 1>, k_sweep_panel<float, 4, 16, 1, 1>},
+    {8, 512, 3, 1, 1, k_sweep_panel<double, 8, 16>, k_sweep_panel<float, 8, 16>},
+    {4, 512, 3, 2, 1, k_sweep_panel<double, 4, 16, 2>, k_sweep_panel<float, 4, 16, 1, 1>},
+    // L2-resident share of A (SweepArgs.l2_keep_pm): 16 = CTA kernel, 17 = panel kernel
+    {4, 512, 1, 1, 1, k_sweep_cta<double, 4, 16, 1, 0, false, true>, k_sweep_cta<float, 4, 16, 1, 0, false, true>},
+    {4, 512, 3, 1, 1, k_sweep_panel<double, 4, 16, 1, 0, true>, k_sweep_panel<float, 4, 16, 1, 0, true>},
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
@@ -562,26 +693,31 @@ int push_variant() { return 11; }
 // Shared memory of a variant: the CTA kernel's partial slots.
 size_t variant_smem(int v, int nchunks, int /*dtype*/, int /*chunk*/) {
   const Variant& V = kVariants[v];
-  return V.cta ? (size_t)kSlots * nchunks * V.R * 8 : 0;  // cta = 1 or 2 (fused exchange)
+  return (V.cta == 1 || V.cta == 2) ? (size_t)kSlots * nchunks * V.R * 8 : 0;  // 2: fused exchange
 }
 bool variant_fits(int v, int nchunks, int dtype, int chunk) {
   const Variant& V = kVariants[v];
   const int step_cols = 32 * (dtype == JACOBI_F32 ? 8 : 4) * (dtype == JACOBI_F32 ? V.u32 : V.u64);
   if (chunk % step_cols != 0) return false;
-  return !V.cta || (nchunks >= V.threads / 32 && variant_smem(v, nchunks, dtype, chunk) <= 48 * 1024);
+  return !V.cta || V.cta == 3 || (nchunks >= V.threads / 32 && variant_smem(v, nchunks, dtype, chunk) <= 48 * 1024);
 }
 bool variant_is_push(int v) { return kVariants[v].cta == 2; }
 int variant_rows_dt(int v, int /*dtype*/) { return kVariants[v].R; }
-// Defaults from B200 measurements (profiles/variants*_r01_*.jsonl, sustained 100-sweep graph solves):
-// the CTA-cooperative kernel R=4 when n has at least 16 chunks (c4 fp64: 7257 GB/s burst, 7153
-// sustained; c5 fp32: 6734 burst), else the item kernel R=8,U=1 (fp64) or R=4,U=1 (fp32).  The U=2
-// instance (variant 9) measured 7275/7186 before the column-range generalisation and 7063/7033 after
-// (it sits at the 128-register cap, so its schedule is fragile); U=1 kept its speed.
-int default_variant(int dtype, int nchunks, int chunk) {
-  const int big = 7;
+// Defaults from B200 measurements (profiles/variants*_r01_*.jsonl; sustained = 100-sweep graph solves):
+// - fp64, n with >= 16 chunks: CTA-cooperative R=4 (c4: 7283 burst / 7175 sustained GB/s; the panel
+//   kernel ties at 7208 / 7187, U=2 instances sit at the 128-register cap and measured lower);
+//   with an L2-resident share of A (l2_keep_pm > 0, A within 4x the L2) its POL instance (c2:
+//   4976 -> 6051 effective GB/s at 55 % kept);
+// - fp32 A, >= 16 chunks: the row-panel kernel R=4 (c5: 7016 / 6771 vs 6983 / 6415 for the CTA kernel,
+//   which re-reads x from L2 once per tile: +50 % of the A bytes with fp32 A);
+// - fewer chunks: the item kernel R=8,U=1 (fp64) or R=4,U=1 (fp32).
+int default_variant(int dtype, int nchunks, int chunk, bool l2_keep) {
+  if (dtype == JACOBI_F32 && nchunks >= 16) return 12;
+  const int big = l2_keep ? 16 : 7;
   if (variant_fits(big, nchunks, dtype, chunk)) return big;
   return dtype == JACOBI_F32 ? 0 : 1;  // U = 1: fits every chunk
 }
+bool variant_uses_l2_keep(int v) { return v == 16 || v == 17; }
 int variant_rows(int v) { return kVariants[v].R; }
 int variant_threads(int v) { return kVariants[v].threads; }
 

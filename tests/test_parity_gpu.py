@@ -480,3 +480,23 @@ def test_fused_exchange_emulated_ranks_bitwise(jb):
         r = p.solve(b, None, 3000, 1e-11, history=True)
         assert (r.status, r.iters) == (ref.status, ref.iters) and np.array_equal(r.x, ref.x)
         assert np.array_equal(r.hist, ref.hist)
+
+
+# ------------------------------------------------------------------ stream ordering of borrowed inputs
+def test_null_stream_plan_sees_default_stream_writes(jb):
+    """A plan created with no stream reads a borrowed device A that the caller has just written on
+    torch's default (legacy) stream: its own stream is a blocking one, so the generator's writes
+    are complete before the setup kernels read a_ii (with a non-blocking stream this raced and
+    reported EZERODIAG on rows the generator had not reached yet)."""
+    import torch
+    cfg = g.GenConfig(16384, diag_mode=g.DIAG_SCALE, diag_scale=1.05)
+    for _ in range(3):
+        dA = torch.empty((cfg.n, cfg.n), dtype=torch.float64, device="cuda")
+        db = torch.empty(cfg.n, dtype=torch.float64, device="cuda")
+        g.device_rows(cfg, 0, cfg.n, dA.data_ptr(), cfg.n, db.data_ptr(), 0)  # legacy default stream
+        with jb.Plan(dA, n=cfg.n) as p:  # no stream, no synchronize in between
+            r = p.solve(db.cpu().numpy(), None, 1, 0.0)
+        d, bh = g.host_diag_b(cfg, 0, cfg.n)
+        assert np.array_equal(r.x, bh / d)  # P3: sweep 1 from x0 = 0 is b / diag bitwise
+        del dA, db
+        torch.cuda.empty_cache()
