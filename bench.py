@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--exchange", choices=["nccl", "p2p", "cols"], default="nccl",
                     help="N > 1: NCCL row-wise (default), fused NVLink push (NEXT-1), or column-wise (NEXT-4)")
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the per-config rates of the other BASELINE.json configs (N = 1 only)")
     return ap.parse_args()
 
 
@@ -165,6 +167,51 @@ def cpu_oracle_rate(wname, seconds, steps=None):
     return rate, cores, sample, el
 
 
+# ----------------------------------------------------------------------------- other configs (N = 1)
+OTHER_RUNS = (("c1", 200, 0.0), ("c1", 200, 1e-12), ("c2", 500, 0.0), ("c3", 5000, 1e-10), ("c3", 1000, 0.0),
+              ("c5", 2000, 1e-6), ("c5", 100, 0.0))
+
+
+def other_configs(jb, g, torch, stream):
+    """Rates of the other BASELINE.json configs on this GPU (informational; the headline is c4):
+    device-resident inputs, best of 3 solves after a warm-up, CUDA events on the plan's stream.
+    it/s = sweeps / time; GB/s = algorithmic bytes per sweep x it/s (c1/c2 sit in or near L2)."""
+    out = []
+    sh = stream.cuda_stream
+    for name in dict.fromkeys(r[0] for r in OTHER_RUNS):
+        cfg = g.CONFIGS[name]
+        n = cfg.n
+        dA = torch.empty((n, n), dtype=torch.float32 if cfg.a_dtype == g.F32 else torch.float64, device="cuda")
+        db = torch.empty(n, dtype=torch.float64, device="cuda")
+        g.device_rows(cfg, 0, n, dA.data_ptr(), n, db.data_ptr(), sh)
+        dx0 = torch.zeros(n, dtype=torch.float64, device="cuda")
+        dxo = torch.empty(n, dtype=torch.float64, device="cuda")
+        with jb.Plan(dA, n=n, stream=sh) as p:
+            inf = p.info
+            for _, max_iter, tol in (r for r in OTHER_RUNS if r[0] == name):
+                p.set_batch(20 if max_iter % 20 == 0 else 32)
+                r = p.solve_device(db, dx0, dxo, max_iter, tol)
+                best = None
+                for _ in range(3):
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    r = p.solve_device(db, dx0, dxo, max_iter, tol)
+                    e1.record(stream)
+                    e1.synchronize()
+                    ms = e0.elapsed_time(e1)
+                    best = ms if best is None else min(best, ms)
+                its = r.iters / (best * 1e-3)
+                out.append({"config": name, "n": n, "max_iter": max_iter, "tol": tol,
+                            "status": jb.STATUS_NAMES[r.status], "iters": r.iters, "it_per_s": round(its, 1),
+                            "us_per_sweep": round(1e3 * best / r.iters, 2),
+                            "effective_gbs": round(inf.bytes_per_sweep * its / 1e9, 1),
+                            "path": (f"cluster x{inf.cluster_ctas}" if inf.cluster_ctas else
+                                     f"graph: {jb.variant_name(inf.variant)}")})
+        del dA, db
+        torch.cuda.empty_cache()
+    return out
+
+
 # ----------------------------------------------------------------------------- main (GPU arm)
 def main():
     args = parse()
@@ -204,7 +251,10 @@ def main():
     cfg = g.CONFIGS[gname]
     n = cfg.n
     dt = torch.float32 if cfg.a_dtype == g.F32 else torch.float64
-    stream = torch.cuda.current_stream()
+    # A dedicated stream: the plan issues every kernel and collective on it and the CUDA events that
+    # time the step are recorded on it.
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     sh = stream.cuda_stream
     row0, m = jb.partition(n, world, rank)
 
@@ -333,6 +383,10 @@ def main():
                        "NCCL comm init, sweeps, D2H); wall time, max over ranks")}
         del hA
 
+    configs = None
+    if world == 1 and not args.no_configs:
+        configs = other_configs(jb, g, torch, stream)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, cores, sample, _ = cpu_oracle_rate(args.workload, args.cpu_seconds)
@@ -354,7 +408,7 @@ def main():
             "effective_gbs_per_gpu": achieved, "effective_gbs_aggregate": achieved * world,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(args.workload),
-                         "peak_source": peak_src, "kernel": f"{jb.VARIANT_NAMES[info.variant]} ({'fp64' if dt == torch.float64 else 'fp32'} A)",
+                         "peak_source": peak_src, "kernel": f"{jb.variant_name(info.variant)} ({'fp64' if dt == torch.float64 else 'fp32'} A)",
                          "bytes_per_launch": bytes_sweep, "avg_launch_ms": sweep_ms,
                          "kernel_only_ms": kernel_ms, "kernel_only_gbs": bytes_sweep / (kernel_ms * 1e-3) / 1e9,
                          "read_ceiling_gbs": ceiling,
@@ -364,6 +418,7 @@ def main():
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "other_configs": configs,
         }
         s = json.dumps(line)
         print(s, flush=True)

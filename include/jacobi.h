@@ -175,6 +175,9 @@ int jacobi_bwprobe(int64_t nbytes, int reps, double* best_gbs);
 
 const char* jacobi_last_error(void);
 int jacobi_version(void); /* 100 * major + minor */
+/* Name of a sweep-kernel variant ("k_sweep_cta R4 U1", ...; jacobi_plan_info_t.variant), or NULL
+ * when 0 <= variant < num_variants does not hold.  Static storage, never freed.  No CUDA call. */
+const char* jacobi_variant_name(int variant);
 
 #ifdef __cplusplus
 }

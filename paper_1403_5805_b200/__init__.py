@@ -32,13 +32,13 @@ EXPORTS = ("jacobi_solve", "jacobi_solve_f32a", "jacobi_plan_create", "jacobi_pl
            "jacobi_nccl_unique_id", "jacobi_dist_plan_create", "jacobi_dist_plan_create_colwise",
            "jacobi_plan_set_col_blocks", "jacobi_plan_ipc_export", "jacobi_plan_ipc_attach",
            "jacobi_plan_set_p2p_emulation", "jacobi_bwprobe", "jacobi_last_error",
-           "jacobi_version")
+           "jacobi_version", "jacobi_variant_name")
 
 
-# Sweep kernel variants compiled into libjacobi.so (csrc/sweep.cu kVariants; all bitwise identical).
-VARIANT_NAMES = ("k_sweep R4 U2", "k_sweep R8 U1", "k_sweep R2 U4", "k_sweep R4 U1", "k_sweep R4 U2 256t",
-                 "k_sweep R2 U1 1024t", "k_sweep_cta R8 U1", "k_sweep_cta R4 U1", "k_sweep_cta R8 U1 256t",
-                 "k_sweep_cta R4 U2", "k_sweep_cta R2 U4", "k_sweep_cta R4 U1 fused-exchange")
+def variant_name(v: int) -> str:
+    """Name of sweep-kernel variant v (csrc/sweep.cu kVariants; all bitwise identical)."""
+    nm = _lib.jacobi_variant_name(int(v))
+    return nm.decode() if nm else f"variant {v}"
 
 
 class JacobiError(RuntimeError):
@@ -86,6 +86,7 @@ def _load():
         "jacobi_bwprobe": ([i64, i32, P(dbl)], i32),
         "jacobi_last_error": ([], ctypes.c_char_p),
         "jacobi_version": ([], i32),
+        "jacobi_variant_name": ([i32], ctypes.c_char_p),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)

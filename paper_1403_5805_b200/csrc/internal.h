@@ -75,6 +75,7 @@ cudaError_t launch_prepare(State* st, int64_t max_iter, double tol, double* hist
 cudaError_t launch_copy_pitched(int dtype, const void* src, int64_t src_ld, void* dst, int64_t dst_ld,
                                 int64_t rows, int64_t n, cudaStream_t s);
 int num_variants();
+const char* variant_name(int variant);
 int default_variant(int dtype, int nchunks, int chunk, bool l2_keep);
 bool variant_uses_l2_keep(int variant);
 bool variant_is_cta(int variant);

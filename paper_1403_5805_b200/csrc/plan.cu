@@ -28,6 +28,7 @@ int jacobi_set_error(int code, const std::string& msg) {
 
 extern "C" const char* jacobi_last_error(void) { return g_err.c_str(); }
 extern "C" int jacobi_version(void) { return 100; }
+extern "C" const char* jacobi_variant_name(int variant) { return jacobi::variant_name(variant); }
 
 // Frees everything the plan owns.  Every release is checked; the first failure is reported through
 // jacobi_last_error (destroy itself cannot return a status) and the runtime's error state is cleared.

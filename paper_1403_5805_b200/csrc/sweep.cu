@@ -654,40 +654,42 @@ __global__ void k_fill(double* buf, int64_t n) {
 // produce identical bits (the summation order does not depend on R, U or the grid); the default is
 // chosen from measurements (profiles/), others stay selectable with JACOBI_SWEEP_VARIANT for tuning.
 struct Variant {
+  const char* name;
   int R, threads, cta;  // cta = 1: k_sweep_cta (needs nchunks >= threads/32 and its partial slots)
   int u64, u32;         // steps in flight (fp64 / fp32 instance): the chunk must be a multiple of 32*E*U
   void (*f64)(const SweepArgs, const int);
   void (*f32)(const SweepArgs, const int);
 };
 const Variant kVariants[] = {
-    {4, 512, 0, 2, 1, k_sweep<double, 4, 2, 512>, k_sweep<float, 4, 1, 512>},
-    {8, 512, 0, 1, 1, k_sweep<double, 8, 1, 512>, k_sweep<float, 8, 1, 512>},
-    {2, 512, 0, 4, 2, k_sweep<double, 2, 4, 512>, k_sweep<float, 2, 2, 512>},
-    {4, 512, 0, 1, 2, k_sweep<double, 4, 1, 512>, k_sweep<float, 4, 2, 512>},
-    {4, 256, 0, 2, 1, k_sweep<double, 4, 2, 256>, k_sweep<float, 4, 1, 256>},
-    {2, 1024, 0, 1, 1, k_sweep<double, 2, 1, 1024>, k_sweep<float, 2, 1, 1024>},
-    {8, 512, 1, 1, 1, k_sweep_cta<double, 8, 16>, k_sweep_cta<float, 8, 16>},
-    {4, 512, 1, 1, 1, k_sweep_cta<double, 4, 16>, k_sweep_cta<float, 4, 16>},
-    {8, 256, 1, 1, 1, k_sweep_cta<double, 8, 8>, k_sweep_cta<float, 4, 8>},
-    {4, 512, 1, 2, 2, k_sweep_cta<double, 4, 16, 2>, k_sweep_cta<float, 4, 16, 2>},
-    {2, 512, 1, 4, 2, k_sweep_cta<double, 2, 16, 4>, k_sweep_cta<float, 2, 16, 2>},
+    {"k_sweep R4 U2", 4, 512, 0, 2, 1, k_sweep<double, 4, 2, 512>, k_sweep<float, 4, 1, 512>},
+    {"k_sweep R8 U1", 8, 512, 0, 1, 1, k_sweep<double, 8, 1, 512>, k_sweep<float, 8, 1, 512>},
+    {"k_sweep R2 U4", 2, 512, 0, 4, 2, k_sweep<double, 2, 4, 512>, k_sweep<float, 2, 2, 512>},
+    {"k_sweep R4 U1", 4, 512, 0, 1, 2, k_sweep<double, 4, 1, 512>, k_sweep<float, 4, 2, 512>},
+    {"k_sweep R4 U2 256t", 4, 256, 0, 2, 1, k_sweep<double, 4, 2, 256>, k_sweep<float, 4, 1, 256>},
+    {"k_sweep R2 U1 1024t", 2, 1024, 0, 1, 1, k_sweep<double, 2, 1, 1024>, k_sweep<float, 2, 1, 1024>},
+    {"k_sweep_cta R8 U1", 8, 512, 1, 1, 1, k_sweep_cta<double, 8, 16>, k_sweep_cta<float, 8, 16>},
+    {"k_sweep_cta R4 U1", 4, 512, 1, 1, 1, k_sweep_cta<double, 4, 16>, k_sweep_cta<float, 4, 16>},
+    {"k_sweep_cta R8 U1 256t", 8, 256, 1, 1, 1, k_sweep_cta<double, 8, 8>, k_sweep_cta<float, 4, 8>},
+    {"k_sweep_cta R4 U2", 4, 512, 1, 2, 2, k_sweep_cta<double, 4, 16, 2>, k_sweep_cta<float, 4, 16, 2>},
+    {"k_sweep_cta R2 U4", 2, 512, 1, 4, 2, k_sweep_cta<double, 2, 16, 4>, k_sweep_cta<float, 2, 16, 2>},
     // fused-exchange (NEXT-1) instances of the defaults; selected only by jacobi_plan_ipc_attach /
     // jacobi_plan_set_p2p_emulation (they need SweepArgs.peers)
-    {4, 512, 2, 1, 1, k_sweep_cta<double, 4, 16, 1, 0, true>, k_sweep_cta<float, 4, 16, 1, 0, true>},
+    {"k_sweep_cta R4 U1 fused-exchange", 4, 512, 2, 1, 1, k_sweep_cta<double, 4, 16, 1, 0, true>, k_sweep_cta<float, 4, 16, 1, 0, true>},
     // row-panel kernel (cta = 3): warps own whole rows, x chunks shared through L1
-    {4, 512, 3, 1, 1, k_sweep_panel<double, 4, 16>, k_sweep_panel<float, 4, 16>},
-    {4, 512, 3, 1, 1, k_sweep_panel<double, 4, 16, 1, 1>, k_sweep_panel<float, 4, 16, 1, 1>},
-    {8, 512, 3, 1, 1, k_sweep_panel<double, 8, 16>, k_sweep_panel<float, 8, 16>},
-    {4, 512, 3, 2, 1, k_sweep_panel<double, 4, 16, 2>, k_sweep_panel<float, 4, 16, 1, 1>},
+    {"k_sweep_panel R4 U1", 4, 512, 3, 1, 1, k_sweep_panel<double, 4, 16>, k_sweep_panel<float, 4, 16>},
+    {"k_sweep_panel R4 U1 x-evict_last", 4, 512, 3, 1, 1, k_sweep_panel<double, 4, 16, 1, 1>, k_sweep_panel<float, 4, 16, 1, 1>},
+    {"k_sweep_panel R8 U1", 8, 512, 3, 1, 1, k_sweep_panel<double, 8, 16>, k_sweep_panel<float, 8, 16>},
+    {"k_sweep_panel R4 U2", 4, 512, 3, 2, 1, k_sweep_panel<double, 4, 16, 2>, k_sweep_panel<float, 4, 16, 1, 1>},
     // L2-resident share of A (SweepArgs.l2_keep_pm): 16 = CTA kernel, 17 = panel kernel
-    {4, 512, 1, 1, 1, k_sweep_cta<double, 4, 16, 1, 0, false, true>, k_sweep_cta<float, 4, 16, 1, 0, false, true>},
-    {4, 512, 3, 1, 1, k_sweep_panel<double, 4, 16, 1, 0, true>, k_sweep_panel<float, 4, 16, 1, 0, true>},
+    {"k_sweep_cta R4 U1 L2-keep", 4, 512, 1, 1, 1, k_sweep_cta<double, 4, 16, 1, 0, false, true>, k_sweep_cta<float, 4, 16, 1, 0, false, true>},
+    {"k_sweep_panel R4 U1 L2-keep", 4, 512, 3, 1, 1, k_sweep_panel<double, 4, 16, 1, 0, true>, k_sweep_panel<float, 4, 16, 1, 0, true>},
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 }  // namespace
 
 int num_variants() { return kNumVariants; }
+const char* variant_name(int v) { return v >= 0 && v < kNumVariants ? kVariants[v].name : nullptr; }
 bool variant_is_cta(int v) { return kVariants[v].cta != 0; }
 int push_variant() { return 11; }
 // Shared memory of a variant: the CTA kernel's partial slots.

@@ -10,6 +10,8 @@ import subprocess
 import sys
 
 rep, launches, tag, cmd = sys.argv[1:5]
+key = sys.argv[5] if len(sys.argv) > 5 else "c4"             # workload key in ncu_sweep_summary.json
+alg = float(sys.argv[6]) if len(sys.argv) > 6 else 34361311232  # algorithmic bytes per launch
 out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 r = list(csv.reader(out.splitlines()))
 h, u, v = r[0], r[1], r[2]
@@ -22,13 +24,13 @@ def num(k):
     return float(val.replace(",", "")) * scale.get(unit, 1)
 
 
-summ = {"c4": {
+summ = {key: {
     "kernel": d["Kernel Name"][0] if "Kernel Name" in d else "k_sweep",
     "source": f"{rep} (ncu --set full --clock-control none, {cmd})",
     "duration_ms": num("gpu__time_duration.sum") * 1e3,
     "dram_bytes_read": num("dram__bytes_read.sum"), "dram_bytes_write": num("dram__bytes_write.sum"),
     "dram_bytes_per_launch": num("dram__bytes_read.sum") + num("dram__bytes_write.sum"),
-    "algorithmic_bytes_per_launch": 34361311232,
+    "algorithmic_bytes_per_launch": alg,
     "dram_gbs": (num("dram__bytes_read.sum") + num("dram__bytes_write.sum")) / num("gpu__time_duration.sum") / 1e9,
     "dram_throughput_pct_of_ncu_peak": float(d["gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"][0]),
     "dram_slice_active_min_pct": float(d["dram__cycles_active.min.pct_of_peak_sustained_elapsed"][0]),
@@ -42,9 +44,16 @@ summ = {"c4": {
                       if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")
                       and float(d[k][0]) > 100},
 }}
-json.dump(summ, open("profiles/ncu_sweep_summary.json", "w"), indent=1)
+try:
+    allsum = json.load(open("profiles/ncu_sweep_summary.json"))
+except (OSError, ValueError):
+    allsum = {}
+allsum.update(summ)
+json.dump(allsum, open("profiles/ncu_sweep_summary.json", "w"), indent=1)
 print(json.dumps(summ, indent=1))
 
+if launches == "-":
+    sys.exit(0)
 rows = [x for x in csv.reader(open(launches)) if len(x) > 10]
 hdr = rows[0]
 ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")

@@ -79,3 +79,12 @@ def test_no_cpu_fallback_without_gpu(jb):
     with pytest.raises(jb.JacobiError) as e:
         jb.solve(np.array([[2.0, 1.0], [1.0, 3.0]]), np.array([3.0, 4.0]), max_iter=5)
     assert e.value.status == jb.ECUDA
+
+
+def test_variant_names_without_gpu(jb):
+    """jacobi_variant_name is pure host code: names for the compiled variants, NULL past the end."""
+    names = [jb.variant_name(v) for v in range(64)]
+    assert names[0].startswith("k_sweep") and names[7] == "k_sweep_cta R4 U1"
+    known = [n for n in names if not n.startswith("variant ")]
+    assert len(known) >= 12 and len(set(known)) == len(known)
+    assert jb._lib.jacobi_variant_name(-1) is None and jb._lib.jacobi_variant_name(10**6) is None
