@@ -250,6 +250,33 @@ def _device_system(jb, cfg):
     return dA, db
 
 
+def test_c3_full_parity_and_shards(jb):
+    """BASELINE.json configs[2] at full size (n = 16384, 2.1 GB, diag = 1.05 x row abs-sum): the tol
+    1e-10 stop run against the full oracle — same status and iteration count, relative L-inf error
+    <= 1e-10, d_k history — and the P = 2/4/8 row-block split of the same plan (P12a, the shards of
+    the 1/2/4/8-GPU runs launched one after another on this GPU) bitwise equal to P = 1."""
+    cfg = g.CONFIGS["c3"]
+    A, b, xs = g.host_system(cfg)
+    st_o, x_o, it_o, h_o = oracle.jacobi(A, b, None, 5000, 1e-10, nthreads=16, history=True)
+    assert st_o == oracle.CONVERGED
+    with jb.Plan(A) as p:
+        r = p.solve(b, None, 5000, 1e-10, history=True)
+        assert (r.status, r.iters) == (jb.CONVERGED, it_o)
+        assert rel_linf(r.x, x_o) <= TOL64
+        np.testing.assert_allclose(r.hist, h_o, rtol=1e-9, atol=1e-14)
+        # the margin of the decisive distance to tol is far above the GPU/oracle d difference (R20)
+        assert h_o[it_o - 2] >= 1e-10 * 1.05 and h_o[it_o - 1] <= 1e-10 / 1.05
+        for nb in (2, 4, 8):
+            p.set_row_blocks(nb)
+            q = p.solve(b, None, 5000, 1e-10, history=True)
+            assert (q.status, q.iters) == (r.status, r.iters)
+            assert np.array_equal(q.x, r.x) and np.array_equal(q.hist, r.hist), nb
+        p.set_row_blocks(1)
+        f = p.solve(b, None, 1000, 0.0)  # the fixed-1000 companion run the rates are quoted on
+        assert (f.status, f.iters) == (jb.MAX_ITER, 1000)
+        assert np.max(np.abs(f.x - xs)) <= 1e-12  # P8 planted solution
+
+
 @pytest.mark.parametrize("name", ["c4", "c5"])
 def test_full_size_sampled_parity(jb, name):
     """BASELINE.json configs[3]/[4] at full size in the bench's launch configuration: sweeps 1 and 2
