@@ -77,6 +77,15 @@ __device__ __forceinline__ void ld_x(const double* p, double (&v)[E]) {
   for (int q = 0; q < E; q += 4) ld_x4<XL>(p + q, v + q);
 }
 
+// x^(k-1) from a shared-memory chunk staged by the bulk-copy engine (k_sweep_panel with XSN > 0).
+template <int E>
+__device__ __forceinline__ void ld_xs(const double* p, double (&v)[E]) {
+#pragma unroll
+  for (int q = 0; q < E; q += 2)
+    asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];"
+                 : "=d"(v[q]), "=d"(v[q + 1]) : "r"((unsigned)__cvta_generic_to_shared(p + q)));
+}
+
 // Prologue of sweep k (PAPER.md:64-66 evaluated on the device): decides whether sweep k runs.
 // Every CTA evaluates the same inputs and reaches the same decision; only the leader writes.
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
@@ -117,12 +126,13 @@ __device__ __forceinline__ bool sweep_prologue(const SweepArgs& a, int j, bool l
 // variant shares: lane l owns columns c0 + (32*s + l)*E + e, accumulated in ascending s then e with
 // one DFMA chain per row; j == i (the diagonal) and j >= n are skipped.  Rows r >= nv
 // are not loaded (their sums are unused).
-template <typename T, int R, int U, int XL = 0, bool POL = false>
+// XSM: x^(k-1) of this chunk comes from shared memory, xs[col - c0] (else from global, xo[col]).
+template <typename T, int R, int U, int XL = 0, bool POL = false, bool XSM = false>
 __device__ __forceinline__ void accumulate_chunk(const T* const (&rowp)[R], const int nv,
                                                  const double* __restrict__ xo, const int64_t c0,
                                                  const int64_t c1, const int chunk, const int64_t n,
                                                  const int64_t g0, const int lane, double (&acc)[R],
-                                                 const uint64_t pol = 0) {
+                                                 const uint64_t pol = 0, const double* xs = nullptr) {
   constexpr int E = VecOf<T>::E;
   constexpr int S = 32 * E;  // columns per warp step
   const int nsteps = chunk / S;
@@ -134,7 +144,8 @@ __device__ __forceinline__ void accumulate_chunk(const T* const (&rowp)[R], cons
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t col = c0 + (int64_t)((s + u) * 32 + lane) * E;
-        ld_x<E, XL>(xo + col, xv[u]);
+        if constexpr (XSM) ld_xs<E>(xs + (col - c0), xv[u]);
+        else ld_x<E, XL>(xo + col, xv[u]);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           if (r < nv) ld_a_p<POL>(rowp[r] + col, av[u][r], pol);
@@ -158,7 +169,8 @@ __device__ __forceinline__ void accumulate_chunk(const T* const (&rowp)[R], cons
       if (col < n) {
         T av[R][E];
         double xv[E];
-        ld_x<E, XL>(xo + col, xv);
+        if constexpr (XSM) ld_xs<E>(xs + (col - c0), xv);
+        else ld_x<E, XL>(xo + col, xv);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           if (r < nv) ld_a_p<POL>(rowp[r] + col, av[r], pol);
@@ -408,9 +420,38 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
 // across the same column chunks at the same rate, each x^(k-1) chunk is fetched from L2 once per CTA
 // and served to the other warps from L1 (in k_sweep_cta every warp reads a different chunk, so x
 // streams from L2 once per tile: +25 % of the A bytes for fp64, +50 % for fp32 A).
-template <typename T, int R, int U, int XL, bool POL, int NV>
+// Shared-memory ring of x^(k-1) chunks (k_sweep_panel with XSN slots).  Item i = t * nchunks + c is
+// chunk c for the warps' t-th tiles; it lives in slot i mod XSN and lands on full[slot] (mbarrier
+// parity (i / XSN) & 1).  Every warp still at its t-th tile consumes every item of round t in order;
+// the last of them (smem arrival counter) refills the slot with item i + XSN.  A warp waits for item
+// i only after consuming item i - XSN, so the parity never aliases a phase two rounds back.
+struct XRing {
+  double* xs;          // [XSN][chunk]
+  uint64_t* full;      // [XSN]
+  unsigned* cnt;       // [XSN]
+  int64_t items;       // rounds * nchunks
+  int xsn;
+};
+__device__ __forceinline__ void xring_issue(const XRing& q, const SweepArgs& a, const double* xo, int64_t i) {
+  if (i >= q.items) return;
+  const int slot = (int)(i % q.xsn);
+  const int64_t c0 = a.col0 + (i % a.nchunks) * (int64_t)a.chunk;
+  const int64_t cols = min((int64_t)a.chunk, a.cend - c0);
+  const unsigned bytes = (unsigned)((cols * 8 + 15) & ~(int64_t)15);  // x is padded past n
+  double* dst = q.xs + (size_t)slot * a.chunk;
+  const unsigned bar = (unsigned)__cvta_generic_to_shared(&q.full[slot]);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the slot before the async write
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)),
+               "l"(xo + c0), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+template <typename T, int R, int U, int XL, bool POL, int NV, int XSN = 0>
 __device__ __forceinline__ void panel_tile(const SweepArgs& a, const T* A, const double* __restrict__ xo,
-                                           const int64_t r0, const int lane, double (&s)[R], const uint64_t pol) {
+                                           const int64_t r0, const int lane, double (&s)[R], const uint64_t pol,
+                                           const XRing* ring = nullptr, int64_t item0 = 0, unsigned arrivals = 0) {
   const T* rowp[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) rowp[r] = A + (r0 + (r < NV ? r : NV - 1)) * a.lda - a.col0;
@@ -421,7 +462,20 @@ __device__ __forceinline__ void panel_tile(const SweepArgs& a, const T* A, const
     for (int r = 0; r < R; ++r) acc[r] = 0.0;
     const int64_t c0 = a.col0 + (int64_t)c * a.chunk;
     const int64_t c1 = min(c0 + (int64_t)a.chunk, a.cend);
-    accumulate_chunk<T, R, U, XL, POL>(rowp, NV, xo, c0, c1, a.chunk, a.cend, g0, lane, acc, pol);
+    if constexpr (XSN > 0) {
+      const int64_t i = item0 + c;
+      const int slot = (int)(i % XSN);
+      mbar_wait(&ring->full[slot], (unsigned)((i / XSN) & 1));
+      accumulate_chunk<T, R, U, XL, POL, true>(rowp, NV, xo, c0, c1, a.chunk, a.cend, g0, lane, acc, pol,
+                                               ring->xs + (size_t)slot * a.chunk);
+      __syncwarp();
+      if (lane == 0 && atomicAdd(&ring->cnt[slot], 1u) + 1u == arrivals) {  // last reader of item i
+        ring->cnt[slot] = 0u;
+        xring_issue(*ring, a, xo, i + XSN);
+      }
+    } else {
+      accumulate_chunk<T, R, U, XL, POL>(rowp, NV, xo, c0, c1, a.chunk, a.cend, g0, lane, acc, pol);
+    }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
 #pragma unroll
@@ -433,24 +487,41 @@ __device__ __forceinline__ void panel_tile(const SweepArgs& a, const T* A, const
 
 // Row count nv in [1, R] as a compile-time constant (a run-time count serialises the loads, see
 // k_sweep_cta).
-template <typename T, int R, int U, int XL, bool POL, int NV = R>
+template <typename T, int R, int U, int XL, bool POL, int XSN, int NV = R>
 __device__ __forceinline__ void panel_tile_nv(const int nv, const SweepArgs& a, const T* A,
                                               const double* __restrict__ xo, const int64_t r0, const int lane,
-                                              double (&s)[R], const uint64_t pol) {
+                                              double (&s)[R], const uint64_t pol, const XRing* ring,
+                                              int64_t item0, unsigned arrivals) {
   if constexpr (NV == 1) {
-    panel_tile<T, R, U, XL, POL, 1>(a, A, xo, r0, lane, s, pol);
+    panel_tile<T, R, U, XL, POL, 1, XSN>(a, A, xo, r0, lane, s, pol, ring, item0, arrivals);
   } else {
-    if (nv == NV) panel_tile<T, R, U, XL, POL, NV>(a, A, xo, r0, lane, s, pol);
-    else panel_tile_nv<T, R, U, XL, POL, NV - 1>(nv, a, A, xo, r0, lane, s, pol);
+    if (nv == NV) panel_tile<T, R, U, XL, POL, NV, XSN>(a, A, xo, r0, lane, s, pol, ring, item0, arrivals);
+    else panel_tile_nv<T, R, U, XL, POL, XSN, NV - 1>(nv, a, A, xo, r0, lane, s, pol, ring, item0, arrivals);
   }
 }
 
 // POL: rows in the first l2_keep_pm/1000 of each warp's share are loaded with L2 evict_last (kept
 // resident across sweeps), the rest with evict_first.
-template <typename T, int R, int NW, int U = 1, int XL = 0, bool POL = false>
+// XSN > 0: x^(k-1) is staged in shared memory, chunk by chunk, through an XSN-slot ring filled by the
+// bulk-copy engine (XRing); else each warp reads it with L1-cached global loads.
+constexpr int kMaxXSN = 16;
+template <typename T, int R, int NW, int U = 1, int XL = 0, bool POL = false, int XSN = 0>
 __global__ void __launch_bounds__(NW * 32, 1) k_sweep_panel(const SweepArgs a, const int j) {
+  static_assert(XSN <= kMaxXSN, "x ring slots");
+  extern __shared__ __align__(128) double s_xring[];  // [XSN][chunk] when XSN > 0
+  __shared__ __align__(8) uint64_t s_xfull[XSN > 0 ? XSN : 1];
+  __shared__ unsigned s_xcnt[XSN > 0 ? XSN : 1];
   __shared__ int s_go;
-  if (threadIdx.x == 0) s_go = sweep_prologue(a, j, blockIdx.x == 0);
+  if (threadIdx.x == 0) {
+    s_go = sweep_prologue(a, j, blockIdx.x == 0);
+    if constexpr (XSN > 0) {
+      for (int q = 0; q < XSN; ++q) {
+        mbar_init(&s_xfull[q], 1);
+        s_xcnt[q] = 0u;
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+  }
   __syncthreads();
   if (!s_go) return;
 
@@ -462,13 +533,30 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_panel(const SweepArgs a, c
   const int64_t rb = (int64_t)blockIdx.x * a.m / gridDim.x;
   const int64_t re = (int64_t)(blockIdx.x + 1) * a.m / gridDim.x;
   const int64_t wb = rb + (re - rb) * w / NW, we = rb + (re - rb) * (w + 1) / NW;
+  // x ring schedule: round t = every warp's t-th tile; arrivals of round t = warps with > t tiles.
+  XRing ring{};
+  auto tiles_of = [&](int ww) {
+    const int64_t b0 = rb + (re - rb) * ww / NW, b1 = rb + (re - rb) * (ww + 1) / NW;
+    return (int)((b1 - b0 + R - 1) / R);
+  };
+  if constexpr (XSN > 0) {
+    int rounds = 0;
+    for (int ww = 0; ww < NW; ++ww) rounds = max(rounds, tiles_of(ww));
+    ring = XRing{s_xring, s_xfull, s_xcnt, (int64_t)rounds * a.nchunks, XSN};
+    if (threadIdx.x == 0)
+      for (int64_t i = 0; i < XSN; ++i) xring_issue(ring, a, xo, i);
+  }
   unsigned long long dmax = 0ull;
-  for (int64_t r0 = wb; r0 < we; r0 += R) {
+  int t = 0;
+  for (int64_t r0 = wb; r0 < we; r0 += R, ++t) {
     const int nv = (int)min((int64_t)R, we - r0);
     double s[R];
     uint64_t pol = 0;
     if constexpr (POL) pol = l2_policy((r0 - wb) * 1000 < (we - wb) * (int64_t)a.l2_keep_pm);
-    panel_tile_nv<T, R, U, XL, POL>(nv, a, A, xo, r0, lane, s, pol);
+    unsigned arrivals = 0;
+    if constexpr (XSN > 0)
+      for (int ww = 0; ww < NW; ++ww) arrivals += tiles_of(ww) > t ? 1u : 0u;
+    panel_tile_nv<T, R, U, XL, POL, XSN>(nv, a, A, xo, r0, lane, s, pol, &ring, (int64_t)t * a.nchunks, arrivals);
     double mine = s[0];
 #pragma unroll
     for (int r = 1; r < R; ++r)
@@ -683,6 +771,9 @@ const Variant kVariants[] = {
     // L2-resident share of A (SweepArgs.l2_keep_pm): 16 = CTA kernel, 17 = panel kernel
     {"k_sweep_cta R4 U1 L2-keep", 4, 512, 1, 1, 1, k_sweep_cta<double, 4, 16, 1, 0, false, true>, k_sweep_cta<float, 4, 16, 1, 0, false, true>},
     {"k_sweep_panel R4 U1 L2-keep", 4, 512, 3, 1, 1, k_sweep_panel<double, 4, 16, 1, 0, true>, k_sweep_panel<float, 4, 16, 1, 0, true>},
+    // row-panel kernel with x^(k-1) staged in shared memory (8-slot chunk ring, cta = 4)
+    {"k_sweep_panel R4 U1 x-smem", 4, 512, 4, 1, 1, k_sweep_panel<double, 4, 16, 1, 0, false, 8>, k_sweep_panel<float, 4, 16, 1, 0, false, 8>},
+    {"k_sweep_panel R4 U1 x-smem L2-keep", 4, 512, 4, 1, 1, k_sweep_panel<double, 4, 16, 1, 0, true, 8>, k_sweep_panel<float, 4, 16, 1, 0, true, 8>},
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
@@ -693,14 +784,16 @@ const char* variant_name(int v) { return v >= 0 && v < kNumVariants ? kVariants[
 bool variant_is_cta(int v) { return kVariants[v].cta != 0; }
 int push_variant() { return 11; }
 // Shared memory of a variant: the CTA kernel's partial slots.
-size_t variant_smem(int v, int nchunks, int /*dtype*/, int /*chunk*/) {
+size_t variant_smem(int v, int nchunks, int /*dtype*/, int chunk) {
   const Variant& V = kVariants[v];
+  if (V.cta == 4) return (size_t)8 * chunk * 8;  // x ring: 8 slots of one chunk of fp64 x
   return (V.cta == 1 || V.cta == 2) ? (size_t)kSlots * nchunks * V.R * 8 : 0;  // 2: fused exchange
 }
 bool variant_fits(int v, int nchunks, int dtype, int chunk) {
   const Variant& V = kVariants[v];
   const int step_cols = 32 * (dtype == JACOBI_F32 ? 8 : 4) * (dtype == JACOBI_F32 ? V.u32 : V.u64);
   if (chunk % step_cols != 0) return false;
+  if (V.cta == 4) return variant_smem(v, nchunks, dtype, chunk) <= 200 * 1024;
   return !V.cta || V.cta == 3 || (nchunks >= V.threads / 32 && variant_smem(v, nchunks, dtype, chunk) <= 48 * 1024);
 }
 bool variant_is_push(int v) { return kVariants[v].cta == 2; }
@@ -710,16 +803,18 @@ int variant_rows_dt(int v, int /*dtype*/) { return kVariants[v].R; }
 //   kernel ties at 7208 / 7187, U=2 instances sit at the 128-register cap and measured lower);
 //   with an L2-resident share of A (l2_keep_pm > 0, A within 4x the L2) its POL instance (c2:
 //   4976 -> 6051 effective GB/s at 55 % kept);
-// - fp32 A, >= 16 chunks: the row-panel kernel R=4 (c5: 7016 / 6771 vs 6983 / 6415 for the CTA kernel,
-//   which re-reads x from L2 once per tile: +50 % of the A bytes with fp32 A);
+// - fp32 A, >= 16 chunks: the row-panel kernel R=4 with x^(k-1) staged in shared memory (c5: 7103 /
+//   6878; with L1-served x 6973 / 6783; the CTA kernel 6983 / 6415, which re-reads x from L2 once per
+//   tile: +50 % of the A bytes with fp32 A).  For fp64 A the shared-memory ring measured 1-2.5 %
+//   slower than the CTA kernel (c4 7092 / 7076, c3 6564 / 6676), so fp64 keeps the CTA kernel;
 // - fewer chunks: the item kernel R=8,U=1 (fp64) or R=4,U=1 (fp32).
 int default_variant(int dtype, int nchunks, int chunk, bool l2_keep) {
-  if (dtype == JACOBI_F32 && nchunks >= 16) return 12;
+  if (dtype == JACOBI_F32 && nchunks >= 16) return variant_fits(18, nchunks, dtype, chunk) ? 18 : 12;
   const int big = l2_keep ? 16 : 7;
   if (variant_fits(big, nchunks, dtype, chunk)) return big;
   return dtype == JACOBI_F32 ? 0 : 1;  // U = 1: fits every chunk
 }
-bool variant_uses_l2_keep(int v) { return v == 16 || v == 17; }
+bool variant_uses_l2_keep(int v) { return v == 16 || v == 17 || v == 19; }
 int variant_rows(int v) { return kVariants[v].R; }
 int variant_threads(int v) { return kVariants[v].threads; }
 
@@ -737,6 +832,7 @@ int sweep_grid(int dtype, int v, int num_sms, int nchunks, int chunk) {
   const Variant& V = kVariants[v];
   const size_t smem = variant_smem(v, nchunks, dtype, chunk);
   auto fn = dtype == JACOBI_F32 ? V.f32 : V.f64;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, V.threads, smem);
   if (e != cudaSuccess || per_sm < 1) per_sm = 1;
   return num_sms * per_sm;
