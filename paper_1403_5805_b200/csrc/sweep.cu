@@ -744,36 +744,40 @@ __global__ void k_fill(double* buf, int64_t n) {
 struct Variant {
   const char* name;
   int R, threads, cta;  // cta = 1: k_sweep_cta (needs nchunks >= threads/32 and its partial slots)
+  int R32;              // rows per tile of the fp32 instance (R: fp64)
   int u64, u32;         // steps in flight (fp64 / fp32 instance): the chunk must be a multiple of 32*E*U
   void (*f64)(const SweepArgs, const int);
   void (*f32)(const SweepArgs, const int);
 };
 const Variant kVariants[] = {
-    {"k_sweep R4 U2", 4, 512, 0, 2, 1, k_sweep<double, 4, 2, 512>, k_sweep<float, 4, 1, 512>},
-    {"k_sweep R8 U1", 8, 512, 0, 1, 1, k_sweep<double, 8, 1, 512>, k_sweep<float, 8, 1, 512>},
-    {"k_sweep R2 U4", 2, 512, 0, 4, 2, k_sweep<double, 2, 4, 512>, k_sweep<float, 2, 2, 512>},
-    {"k_sweep R4 U1", 4, 512, 0, 1, 2, k_sweep<double, 4, 1, 512>, k_sweep<float, 4, 2, 512>},
-    {"k_sweep R4 U2 256t", 4, 256, 0, 2, 1, k_sweep<double, 4, 2, 256>, k_sweep<float, 4, 1, 256>},
-    {"k_sweep R2 U1 1024t", 2, 1024, 0, 1, 1, k_sweep<double, 2, 1, 1024>, k_sweep<float, 2, 1, 1024>},
-    {"k_sweep_cta R8 U1", 8, 512, 1, 1, 1, k_sweep_cta<double, 8, 16>, k_sweep_cta<float, 8, 16>},
-    {"k_sweep_cta R4 U1", 4, 512, 1, 1, 1, k_sweep_cta<double, 4, 16>, k_sweep_cta<float, 4, 16>},
-    {"k_sweep_cta R8 U1 256t", 8, 256, 1, 1, 1, k_sweep_cta<double, 8, 8>, k_sweep_cta<float, 4, 8>},
-    {"k_sweep_cta R4 U2", 4, 512, 1, 2, 2, k_sweep_cta<double, 4, 16, 2>, k_sweep_cta<float, 4, 16, 2>},
-    {"k_sweep_cta R2 U4", 2, 512, 1, 4, 2, k_sweep_cta<double, 2, 16, 4>, k_sweep_cta<float, 2, 16, 2>},
+    {"k_sweep R4 U2", 4, 512, 0, 4, 2, 1, k_sweep<double, 4, 2, 512>, k_sweep<float, 4, 1, 512>},
+    {"k_sweep R8 U1", 8, 512, 0, 8, 1, 1, k_sweep<double, 8, 1, 512>, k_sweep<float, 8, 1, 512>},
+    {"k_sweep R2 U4", 2, 512, 0, 2, 4, 2, k_sweep<double, 2, 4, 512>, k_sweep<float, 2, 2, 512>},
+    {"k_sweep R4 U1", 4, 512, 0, 4, 1, 2, k_sweep<double, 4, 1, 512>, k_sweep<float, 4, 2, 512>},
+    {"k_sweep R4 U2 256t", 4, 256, 0, 4, 2, 1, k_sweep<double, 4, 2, 256>, k_sweep<float, 4, 1, 256>},
+    {"k_sweep R2 U1 1024t", 2, 1024, 0, 2, 1, 1, k_sweep<double, 2, 1, 1024>, k_sweep<float, 2, 1, 1024>},
+    {"k_sweep_cta R8 U1", 8, 512, 1, 8, 1, 1, k_sweep_cta<double, 8, 16>, k_sweep_cta<float, 8, 16>},
+    {"k_sweep_cta R4 U1", 4, 512, 1, 4, 1, 1, k_sweep_cta<double, 4, 16>, k_sweep_cta<float, 4, 16>},
+    {"k_sweep_cta R8 U1 256t", 8, 256, 1, 4, 1, 1, k_sweep_cta<double, 8, 8>, k_sweep_cta<float, 4, 8>},
+    {"k_sweep_cta R4 U2", 4, 512, 1, 4, 2, 2, k_sweep_cta<double, 4, 16, 2>, k_sweep_cta<float, 4, 16, 2>},
+    {"k_sweep_cta R2 U4", 2, 512, 1, 2, 4, 2, k_sweep_cta<double, 2, 16, 4>, k_sweep_cta<float, 2, 16, 2>},
     // fused-exchange (NEXT-1) instances of the defaults; selected only by jacobi_plan_ipc_attach /
     // jacobi_plan_set_p2p_emulation (they need SweepArgs.peers)
-    {"k_sweep_cta R4 U1 fused-exchange", 4, 512, 2, 1, 1, k_sweep_cta<double, 4, 16, 1, 0, true>, k_sweep_cta<float, 4, 16, 1, 0, true>},
+    {"k_sweep_cta R4 U1 fused-exchange", 4, 512, 2, 4, 1, 1, k_sweep_cta<double, 4, 16, 1, 0, true>, k_sweep_cta<float, 4, 16, 1, 0, true>},
     // row-panel kernel (cta = 3): warps own whole rows, x chunks shared through L1
-    {"k_sweep_panel R4 U1", 4, 512, 3, 1, 1, k_sweep_panel<double, 4, 16>, k_sweep_panel<float, 4, 16>},
-    {"k_sweep_panel R4 U1 x-evict_last", 4, 512, 3, 1, 1, k_sweep_panel<double, 4, 16, 1, 1>, k_sweep_panel<float, 4, 16, 1, 1>},
-    {"k_sweep_panel R8 U1", 8, 512, 3, 1, 1, k_sweep_panel<double, 8, 16>, k_sweep_panel<float, 8, 16>},
-    {"k_sweep_panel R4 U2", 4, 512, 3, 2, 1, k_sweep_panel<double, 4, 16, 2>, k_sweep_panel<float, 4, 16, 1, 1>},
+    {"k_sweep_panel R4 U1", 4, 512, 3, 4, 1, 1, k_sweep_panel<double, 4, 16>, k_sweep_panel<float, 4, 16>},
+    {"k_sweep_panel R4 U1 x-evict_last", 4, 512, 3, 4, 1, 1, k_sweep_panel<double, 4, 16, 1, 1>, k_sweep_panel<float, 4, 16, 1, 1>},
+    {"k_sweep_panel R8 U1", 8, 512, 3, 8, 1, 1, k_sweep_panel<double, 8, 16>, k_sweep_panel<float, 8, 16>},
+    {"k_sweep_panel R4 U2", 4, 512, 3, 4, 2, 1, k_sweep_panel<double, 4, 16, 2>, k_sweep_panel<float, 4, 16, 1, 1>},
     // L2-resident share of A (SweepArgs.l2_keep_pm): 16 = CTA kernel, 17 = panel kernel
-    {"k_sweep_cta R4 U1 L2-keep", 4, 512, 1, 1, 1, k_sweep_cta<double, 4, 16, 1, 0, false, true>, k_sweep_cta<float, 4, 16, 1, 0, false, true>},
-    {"k_sweep_panel R4 U1 L2-keep", 4, 512, 3, 1, 1, k_sweep_panel<double, 4, 16, 1, 0, true>, k_sweep_panel<float, 4, 16, 1, 0, true>},
+    {"k_sweep_cta R4 U1 L2-keep", 4, 512, 1, 4, 1, 1, k_sweep_cta<double, 4, 16, 1, 0, false, true>, k_sweep_cta<float, 4, 16, 1, 0, false, true>},
+    {"k_sweep_panel R4 U1 L2-keep", 4, 512, 3, 4, 1, 1, k_sweep_panel<double, 4, 16, 1, 0, true>, k_sweep_panel<float, 4, 16, 1, 0, true>},
     // row-panel kernel with x^(k-1) staged in shared memory (8-slot chunk ring, cta = 4)
-    {"k_sweep_panel R4 U1 x-smem", 4, 512, 4, 1, 1, k_sweep_panel<double, 4, 16, 1, 0, false, 8>, k_sweep_panel<float, 4, 16, 1, 0, false, 8>},
-    {"k_sweep_panel R4 U1 x-smem L2-keep", 4, 512, 4, 1, 1, k_sweep_panel<double, 4, 16, 1, 0, true, 8>, k_sweep_panel<float, 4, 16, 1, 0, true, 8>},
+    {"k_sweep_panel R4 U1 x-smem", 4, 512, 4, 4, 1, 1, k_sweep_panel<double, 4, 16, 1, 0, false, 8>, k_sweep_panel<float, 4, 16, 1, 0, false, 8>},
+    {"k_sweep_panel R4 U1 x-smem L2-keep", 4, 512, 4, 4, 1, 1, k_sweep_panel<double, 4, 16, 1, 0, true, 8>, k_sweep_panel<float, 4, 16, 1, 0, true, 8>},
+    // CTA kernel R = 8 (fp64; the fp32 instances keep R = 4, R = 8 spills): L2-keep and fused exchange
+    {"k_sweep_cta R8 U1 L2-keep", 8, 512, 1, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, false, true>, k_sweep_cta<float, 4, 16, 1, 0, false, true>},
+    {"k_sweep_cta R8 U1 fused-exchange", 8, 512, 2, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, true>, k_sweep_cta<float, 4, 16, 1, 0, true>},
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
@@ -782,12 +786,13 @@ constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 int num_variants() { return kNumVariants; }
 const char* variant_name(int v) { return v >= 0 && v < kNumVariants ? kVariants[v].name : nullptr; }
 bool variant_is_cta(int v) { return kVariants[v].cta != 0; }
-int push_variant() { return 11; }
+int push_variant() { return 21; }
 // Shared memory of a variant: the CTA kernel's partial slots.
-size_t variant_smem(int v, int nchunks, int /*dtype*/, int chunk) {
+size_t variant_smem(int v, int nchunks, int dtype, int chunk) {
   const Variant& V = kVariants[v];
   if (V.cta == 4) return (size_t)8 * chunk * 8;  // x ring: 8 slots of one chunk of fp64 x
-  return (V.cta == 1 || V.cta == 2) ? (size_t)kSlots * nchunks * V.R * 8 : 0;  // 2: fused exchange
+  const int R = dtype == JACOBI_F32 ? V.R32 : V.R;
+  return (V.cta == 1 || V.cta == 2) ? (size_t)kSlots * nchunks * R * 8 : 0;  // 2: fused exchange
 }
 bool variant_fits(int v, int nchunks, int dtype, int chunk) {
   const Variant& V = kVariants[v];
@@ -797,12 +802,13 @@ bool variant_fits(int v, int nchunks, int dtype, int chunk) {
   return !V.cta || V.cta == 3 || (nchunks >= V.threads / 32 && variant_smem(v, nchunks, dtype, chunk) <= 48 * 1024);
 }
 bool variant_is_push(int v) { return kVariants[v].cta == 2; }
-int variant_rows_dt(int v, int /*dtype*/) { return kVariants[v].R; }
+int variant_rows_dt(int v, int dtype) { return dtype == JACOBI_F32 ? kVariants[v].R32 : kVariants[v].R; }
 // Defaults from B200 measurements (profiles/variants*_r01_*.jsonl; sustained = 100-sweep graph solves):
-// - fp64, n with >= 16 chunks: CTA-cooperative R=4 (c4: 7283 burst / 7175 sustained GB/s; the panel
-//   kernel ties at 7208 / 7187, U=2 instances sit at the 128-register cap and measured lower);
-//   with an L2-resident share of A (l2_keep_pm > 0, A within 4x the L2) its POL instance (c2:
-//   4976 -> 6051 effective GB/s at 55 % kept);
+// - fp64, n with >= 16 chunks: CTA-cooperative R=8 (c4: 7316 burst / 7278 sustained GB/s vs 7274 /
+//   7170 for R=4; c3: 7006 / 7115 vs 6732 / 6839; every P-way shard of c3/c4 faster too,
+//   profiles/shard_rates_r01.jsonl; the panel kernel ties R=4 at c4, U=2 instances sit at the
+//   128-register cap and measured lower); with an L2-resident share of A (l2_keep_pm > 0, A within
+//   4x the L2) its POL instance (c2: 4976 -> 6051 effective GB/s with R=4 at 55 % kept, R=8 +2.5 %);
 // - fp32 A, >= 16 chunks: the row-panel kernel R=4 with x^(k-1) staged in shared memory (c5: 7103 /
 //   6878; with L1-served x 6973 / 6783; the CTA kernel 6983 / 6415, which re-reads x from L2 once per
 //   tile: +50 % of the A bytes with fp32 A).  For fp64 A the shared-memory ring measured 1-2.5 %
@@ -810,11 +816,11 @@ int variant_rows_dt(int v, int /*dtype*/) { return kVariants[v].R; }
 // - fewer chunks: the item kernel R=8,U=1 (fp64) or R=4,U=1 (fp32).
 int default_variant(int dtype, int nchunks, int chunk, bool l2_keep) {
   if (dtype == JACOBI_F32 && nchunks >= 16) return variant_fits(18, nchunks, dtype, chunk) ? 18 : 12;
-  const int big = l2_keep ? 16 : 7;
+  const int big = l2_keep ? 20 : 6;
   if (variant_fits(big, nchunks, dtype, chunk)) return big;
   return dtype == JACOBI_F32 ? 0 : 1;  // U = 1: fits every chunk
 }
-bool variant_uses_l2_keep(int v) { return v == 16 || v == 17 || v == 19; }
+bool variant_uses_l2_keep(int v) { return v == 16 || v == 17 || v == 19 || v == 20; }
 int variant_rows(int v) { return kVariants[v].R; }
 int variant_threads(int v) { return kVariants[v].threads; }
 
