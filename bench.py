@@ -50,8 +50,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU oracle sample budget per run")
-    ap.add_argument("--exchange", choices=["nccl", "p2p", "cols"], default="nccl",
-                    help="N > 1: NCCL row-wise (default), fused NVLink push (NEXT-1), or column-wise (NEXT-4)")
+    ap.add_argument("--exchange", choices=["auto", "nccl", "p2p", "cols"], default="auto",
+                    help="N > 1: fused NVLink push (NEXT-1, 'p2p'), NCCL row-wise, or column-wise (NEXT-4); "
+                         "auto = p2p when every GPU pair has peer access (agreed by all ranks), else nccl")
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the per-config rates of the other BASELINE.json configs (N = 1 only)")
@@ -259,6 +260,11 @@ def main():
     row0, m = jb.partition(n, world, rank)
 
     # ---- resident inputs (device twin of the generator; identical bits to the host generator)
+    if world > 1 and args.exchange == "auto":
+        ok = all(torch.cuda.can_device_access_peer(local, q) for q in range(world) if q != local)
+        flag = torch.tensor([1 if ok else 0], device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)  # every rank takes the same decision
+        args.exchange = "p2p" if int(flag.item()) else "nccl"
     cols = world > 1 and args.exchange == "cols"
     db = torch.empty(m, dtype=torch.float64, device="cuda")
     if cols:  # column slab [row0, row0 + m) of all n rows: generate all rows, keep the slab

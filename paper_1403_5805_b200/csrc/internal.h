@@ -20,7 +20,7 @@ struct State {
   int32_t status;     // JACOBI_CONVERGED / JACOBI_MAX_ITER once done
   int64_t iters;      // sweeps performed once done
   int32_t nonfinite;  // b or x0 held NaN/Inf (set by k_prepare): every sweep is a no-op, solve -> ENONFINITE
-  int32_t pad_;
+  int32_t fault;      // fused exchange: a peer's signal did not arrive within kPeerWaitNs (JACOBI_ECUDA)
 };
 
 // NEXT-1 fused exchange: every rank's x buffers, distance slots and arrival counters (peer-mapped
@@ -29,6 +29,7 @@ enum { kMaxPeers = 8 };
 struct PeerArgs {
   int P, rank;
   unsigned long long total_ctas;             // sweep-kernel CTAs over all ranks (arrivals per sweep)
+  unsigned long long wait_ns;                // bound on one wait for the peers' signals (then fault)
   double* x0[kMaxPeers];
   double* x1[kMaxPeers];
   unsigned long long* dslot[kMaxPeers];
@@ -121,6 +122,7 @@ struct jacobi_plan {
   // NEXT-1 fused exchange
   int p2p = 0;                   // 0 off; >= 1: number of ranks (peer-mapped, or emulated on one GPU)
   bool p2p_emul = false;         // P ranks emulated on this GPU (sequential row-block launches)
+  int p2p_drop = -1;             // fault injection (JACOBI_P2P_EMUL_DROP): virtual rank never launched
   jacobi::PeerArgs* peers_dev = nullptr;  // one PeerArgs per (virtual) rank
   unsigned long long* flags = nullptr;    // own arrival counters [2]
   double* ex_x = nullptr;        // emulation: x copies of virtual ranks 1..P-1 (2 buffers each)

@@ -248,6 +248,13 @@ extern "C" int jacobi_plan_set_col_blocks(jacobi_plan* p, int nblocks) {
 }
 
 // NEXT-1 helpers --------------------------------------------------------------------------------
+// Bound on one wait for the peers' sweep signals: 10 s, or JACOBI_PEER_WAIT_MS.
+static unsigned long long peer_wait_ns() {
+  const char* e = getenv("JACOBI_PEER_WAIT_MS");
+  const long long ms = e ? atoll(e) : 10000;
+  return (unsigned long long)std::max(1ll, ms) * 1000000ull;
+}
+
 static int p2p_pick_variant(jacobi_plan* p) {
   const int nch = (int)((p->n + p->chunk - 1) / p->chunk);
   const int v = jacobi::push_variant();
@@ -276,6 +283,7 @@ extern "C" int jacobi_plan_set_p2p_emulation(jacobi_plan* p, int P) {
     a.P = P;
     a.rank = r;
     a.total_ctas = (unsigned long long)P * p->grid;
+    a.wait_ns = peer_wait_ns();
     for (int q = 0; q < P; ++q) {
       a.x0[q] = q == 0 ? p->x[0] : p->ex_x + (size_t)(q - 1) * 2 * p->x_len;
       a.x1[q] = q == 0 ? p->x[1] : a.x0[q] + p->x_len;
@@ -289,6 +297,7 @@ extern "C" int jacobi_plan_set_p2p_emulation(jacobi_plan* p, int P) {
   p->p2p = P;
   p->p2p_emul = true;
   p->nblocks = P;
+  if (const char* e = getenv("JACOBI_P2P_EMUL_DROP")) p->p2p_drop = atoi(e);  // fault-injection test hook
   return 0;
 }
 
@@ -315,6 +324,7 @@ extern "C" int jacobi_plan_ipc_attach(jacobi_plan* p, const void* all_handles) {
   a.P = p->nranks;
   a.rank = p->rank;
   a.total_ctas = (unsigned long long)p->nranks * p->grid;  // same device type on every rank
+  a.wait_ns = peer_wait_ns();
   const cudaIpcMemHandle_t* h = static_cast<const cudaIpcMemHandle_t*>(all_handles);
   for (int q = 0; q < p->nranks; ++q) {
     if (q == p->rank) {
@@ -422,6 +432,7 @@ static int launch_gemv(jacobi_plan* p, int j) {
   if (p->p2p) {  // NEXT-1 fused exchange: (virtual) rank r's launch reads and signals its own copies
     const int nr = p->p2p_emul ? p->p2p : 1;
     for (int r = 0; r < nr; ++r) {
+      if (p->p2p_emul && r == p->p2p_drop) continue;  // injected fault: this virtual rank never signals
       jacobi::SweepArgs a = sweep_args(p, p->p2p_emul ? r : 0);
       a.peers = p->peers_dev + r;
       if (p->p2p_emul && r > 0) {
@@ -589,6 +600,10 @@ static int solve_run(jacobi_plan* p, int64_t max_iter, jacobi::State* fin) {
     ++waited;
     if (p->st_host[slot].nonfinite) {
       rc = nonfinite_error();
+      break;
+    }
+    if (p->st_host[slot].fault) {
+      rc = jacobi_set_error(JACOBI_ECUDA, "fused exchange: a peer's sweep signal did not arrive within 10 s");
       break;
     }
     if (p->st_host[slot].done) {

@@ -94,17 +94,36 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   return v;
 }
 
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ bool sweep_prologue(const SweepArgs& a, int j, bool leader) {
   State* st = a.st;
-  if (*(volatile int32_t*)&st->done || st->nonfinite) return false;
+  if (*(volatile int32_t*)&st->done || st->nonfinite || *(volatile int32_t*)&st->fault) return false;
   const int64_t k = st->kbase + j + 1;
   if (k >= 2 && a.peers) {
     // NEXT-1: wait until every CTA of every rank has pushed its x^(k-1) rows and max|dx| bits here.
+    // Bounded: after pe->wait_ns (10 s by default) the plan is marked faulted (the host reports JACOBI_ECUDA) and every
+    // later sweep is a no-op, so a failed peer cannot hang this GPU.
     const PeerArgs* pe = a.peers;
     const unsigned long long kp = (unsigned long long)(k - 1);
     const unsigned long long target = ((kp + (kp & 1)) / 2) * pe->total_ctas;  // sweeps of this parity
     const unsigned long long* f = pe->flags[pe->rank] + (kp & 1);
-    while (ld_acquire_sys(f) < target) __nanosleep(64);
+    unsigned long long t0 = 0;
+    for (unsigned i = 0; ld_acquire_sys(f) < target; ++i) {
+      __nanosleep(64);
+      if ((i & 4095) == 4095) {
+        const unsigned long long t = global_ns();
+        if (t0 == 0) t0 = t;
+        else if (t - t0 > pe->wait_ns || *(volatile int32_t*)&st->fault) {
+          st->fault = 1;
+          return false;
+        }
+      }
+    }
   }
   if (k >= 2) {
     const double d = __longlong_as_double((long long)a.dslot[(k - 1) & 3]);
@@ -621,7 +640,7 @@ __global__ void k_colsum_epilogue(const double* __restrict__ rsum, int nb, int64
                                   int64_t row0, const double* __restrict__ b, const double* __restrict__ diag,
                                   double* x0buf, double* x1buf, unsigned long long* dslot, double* sq, int norm,
                                   State* st, int j) {
-  if (*(volatile int32_t*)&st->done || st->nonfinite) return;
+  if (*(volatile int32_t*)&st->done || st->nonfinite || st->fault) return;
   const int64_t k = st->kbase + j + 1;
   const double* xo = (k & 1) ? x0buf : x1buf;
   double* xn = (k & 1) ? x1buf : x0buf;
@@ -648,7 +667,7 @@ __global__ void k_colsum_epilogue(const double* __restrict__ rsum, int nb, int64
 // After a graph batch of K sweeps: settle the stop decision for the batch's last sweep (same rule
 // as the prologue) and advance the sweep counter.
 __global__ void k_advance(State* st, const unsigned long long* dslot, int K) {
-  if (st->done || st->nonfinite) return;
+  if (st->done || st->nonfinite || st->fault) return;
   const int64_t k = st->kbase + K + 1;  // the sweep that would come next
   const double d = __longlong_as_double((long long)dslot[(k - 1) & 3]);
   if (st->hist) st->hist[k - 2] = d;

@@ -509,6 +509,27 @@ def test_fused_exchange_emulated_ranks_bitwise(jb):
         assert np.array_equal(r.hist, ref.hist)
 
 
+def test_fused_exchange_silent_peer_faults_instead_of_hanging(jb, monkeypatch):
+    """A rank whose kernels never signal (fault injection: virtual rank 1 of 2 is never launched)
+    must not hang its peers: the next sweep's wait for the signals is bounded (JACOBI_PEER_WAIT_MS),
+    the plan is marked faulted, every later sweep is a no-op and the solve returns JACOBI_ECUDA."""
+    import time
+    A, b, _ = dominant(8192, 17, scale=1.05)
+    monkeypatch.setenv("JACOBI_PEER_WAIT_MS", "300")
+    monkeypatch.setenv("JACOBI_P2P_EMUL_DROP", "1")
+    with jb.Plan(A) as p:
+        p.set_p2p_emulation(2)
+        t0 = time.perf_counter()
+        with pytest.raises(jb.JacobiError) as ei:
+            p.solve(b, None, 40, 0.0)
+        assert ei.value.status == jb.ECUDA and "peer" in str(ei.value)
+        assert time.perf_counter() - t0 < 30.0
+    monkeypatch.delenv("JACOBI_P2P_EMUL_DROP")
+    with jb.Plan(A) as p:  # the device is healthy afterwards
+        p.set_p2p_emulation(2)
+        assert p.solve(b, None, 40, 0.0).iters == 40
+
+
 # ------------------------------------------------------------------ stream ordering of borrowed inputs
 def test_null_stream_plan_sees_default_stream_writes(jb):
     """A plan created with no stream reads a borrowed device A that the caller has just written on
