@@ -491,11 +491,14 @@ static int enqueue_sweep(jacobi_plan* p, int j) {
                           p->stream));
   } else if (p->comm) {
     // k = kbase + j + 1 with kbase a multiple of the batch size (a multiple of 4): parity is static.
+    // One NCCL group: the allgather of x and the one-scalar max allreduce go out as one launch.
     double* xk = p->x[(j + 1) & 1];
+    JNCCL(ncclGroupStart());
     JNCCL(ncclAllGather(xk + p->row0, xk, (size_t)p->m, ncclDouble, p->comm, p->stream));
     if (p->norm == JACOBI_NORM_MAX)
       JNCCL(ncclAllReduce(p->dslot + ((j + 1) & 3), p->dslot + ((j + 1) & 3), 1, ncclUint64, ncclMax, p->comm,
                           p->stream));
+    JNCCL(ncclGroupEnd());
   }
   if (p->norm == JACOBI_NORM_L2) {  // PAPER.md:94 Euclidean distance, fixed-order reduction
     JCUDA(jacobi::launch_l2_partials(p->sq, p->m, p->blk, p->st, p->stream));
