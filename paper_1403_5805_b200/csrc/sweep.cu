@@ -1,23 +1,27 @@
 // sweep.cu — sm_100a kernels of the dense Jacobi sweep.
 //
-// k_sweep: one Jacobi sweep over the launch's rows, fused with the max-norm change
-// d_k = max_i |x_i^(k) - x_i^(k-1)| and the device-side stop test of PAPER.md:61-66.
-//
-// Work decomposition.  Rows are grouped into tiles of R rows, columns into chunks of `chunk`
-// columns (a function of n only).  A work item is (tile, chunk); a warp streams the R rows of its
-// item with 256-bit L1::no_allocate loads (each lane owns E consecutive columns per step: E = 4
-// doubles or 8 floats) and reads the matching x values once per step (L1-cached, reused by the R
-// rows and by the other warps of the CTA, which work on neighbouring tiles of the same chunk).
-// Items are dealt round-robin over a persistent grid sized to fill every SM.
+// One Jacobi sweep over a launch's rows, fused with the max-norm change
+// d_k = max_i |x_i^(k) - x_i^(k-1)| and the device-side stop test of PAPER.md:61-66.  Three work
+// decompositions share one summation order, so every kernel (and every instance: R rows per tile,
+// U steps in flight, CTA size) gives the same bits:
+//   k_sweep       (item kernel, n with < 16 chunks): work item = (tile of R rows, column chunk),
+//                 round-robin over a persistent grid; chunk partials in global memory, the last
+//                 warp to arrive on a tile's counter finalizes it;
+//   k_sweep_cta   (fp64 default): CTA b owns rows [b*m/G, (b+1)*m/G); warp w streams chunks
+//                 w, w+16, ... of each tile; partials meet in a shared-memory ring (mbarriers) and a
+//                 finalizer warp per tile applies the epilogue; also the L2-keep (POL) and the
+//                 fused-exchange (PUSH, NEXT-1) instances;
+//   k_sweep_panel (fp32-A default): each warp owns whole rows and walks all chunks in order;
+//                 optionally x^(k-1) staged in shared memory by a TMA chunk ring (XSN).
 //
 // Summation order (fixed; depends only on column indices, never on the rank count, the row
-// placement, R or the grid): lane l accumulates its columns in ascending order with one DFMA chain
-// per row; the 32 lane sums are combined by a shfl_xor butterfly (16, 8, 4, 2, 1); the chunk sums
-// are added in ascending chunk order by the warp that completes the row tile (last arrival on a
-// per-tile counter).  That warp applies the fused epilogue x_i = (b_i - s_i) / a_ii (IEEE division),
-// stores x_i^(k), and folds |x_i^(k) - x_i^(k-1)| into the sweep's max with an unsigned 64-bit
-// atomicMax on the bit pattern (sign cleared): NaN > +Inf > finite, so the max is NaN-sticky and
-// order independent.
+// placement, R or the grid): columns are cut into chunks of chunk_for(n, dtype) columns; within a
+// chunk lane l accumulates columns c0 + (32 s + l)*E + e (E = 4 doubles / 8 floats per 256-bit
+// load) in ascending s then e with one DFMA chain per row; the 32 lane sums are combined by a
+// shfl_xor butterfly (16, 8, 4, 2, 1); the chunk sums are added in ascending chunk order.  The
+// epilogue is x_i = (b_i - s_i) / a_ii (one IEEE division), and |x_i^(k) - x_i^(k-1)| is folded
+// into the sweep's max with an unsigned 64-bit atomicMax on the bit pattern (sign cleared):
+// NaN > +Inf > finite, so the max is NaN-sticky and order independent.
 #include "internal.h"
 #include <cstdio>
 
