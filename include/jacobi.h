@@ -117,6 +117,10 @@ typedef struct {
   int cluster_ctas;             /* > 0: small-n plan, each solve runs in one thread-block-cluster
                                    launch with A resident in shared memory (same bits); 0: graph
                                    of sweep kernels.  JACOBI_SMALL_N=0 in the environment disables */
+  int persistent_ctas;          /* > 0: mid-size plan, each solve runs as cooperative launches of
+                                   this many CTAs (all sweeps of a launch, grid barrier between
+                                   sweeps; same bits); JACOBI_PERSIST=0/1 disables / forces it
+                                   where it applies (1 GPU, row blocks, max norm)                 */
 } jacobi_plan_info_t;
 int jacobi_plan_info(const jacobi_plan* plan, jacobi_plan_info_t* info);
 

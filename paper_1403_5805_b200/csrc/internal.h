@@ -104,6 +104,10 @@ cudaError_t launch_l2_partials(const double* sq, int64_t m, double* blk, const S
 cudaError_t launch_l2_final(const double* blk, int64_t nblk, unsigned long long* dslot, State* st, int j,
                             cudaStream_t s);
 double bwprobe(int64_t nbytes, int reps);
+// Persistent grid solver (NEXT-3, mid-size n): sweeps k0..k1 in one cooperative launch.
+int gridsync_plan(int dtype, int nchunks, int num_sms, size_t* smem);
+cudaError_t launch_solve_gridsync(int dtype, const SweepArgs& a, unsigned long long* gbar, int64_t k0, int64_t k1,
+                                  int grid, size_t smem, cudaStream_t s);
 
 }  // namespace jacobi
 
@@ -132,6 +136,9 @@ struct jacobi_plan {
   int variant = 0;               // sweep kernel variant (R, U, threads); default per dtype, JACOBI_SWEEP_VARIANT overrides
   int batch = 32;                // sweeps per graph batch
   int l2_keep_pm = 0;            // per-mille of A rows kept L2-resident (evict_last) by the POL variants
+  int grid_G = 0;                // persistent grid solver: CTAs (0 = not used)
+  size_t grid_smem = 0;
+  unsigned long long* gbar = nullptr;  // its grid-barrier counter (zeroed per solve)
   int norm = JACOBI_NORM_MAX;    // distance of the stop test
   int cluster_C = 0;             // > 0: small-n solves run in one cluster launch (cluster.cu)
   size_t cluster_smem = 0;

@@ -17,6 +17,8 @@
 namespace {
 thread_local std::string g_err;
 constexpr int kLookahead = 2;
+// Persistent grid solver by default for A up to this size (profiles/size_sweep_r01.jsonl).
+constexpr double kPersistMaxBytes = 400e6;
 
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 }  // namespace
@@ -42,9 +44,10 @@ static int plan_free(jacobi_plan* p) {
   if (p->comm) ncclCommDestroy(p->comm);
   void* dev[] = {p->dA_owned, p->diag, p->b, p->x[0], p->x[1], p->part, p->cnt, p->dslot, p->st,
                  p->hist_dev, p->flag_dev, p->zmin_dev, p->sq, p->blk, p->blk_all, p->rsum, p->rs_own,
-                 p->flags, p->ex_x, p->ex_dslot, p->ex_flags, p->peers_dev};
+                 p->flags, p->ex_x, p->ex_dslot, p->ex_flags, p->peers_dev, p->gbar};
   const char* names[] = {"A", "diag", "b", "x0", "x1", "part", "cnt", "dslot", "state", "hist", "flag", "zmin",
-                         "sq", "blk", "blk_all", "rsum", "rs_own", "flags", "ex_x", "ex_dslot", "ex_flags", "peers"};
+                         "sq", "blk", "blk_all", "rsum", "rs_own", "flags", "ex_x", "ex_dslot", "ex_flags", "peers",
+                         "gbar"};
   for (void* q : p->ipc_open) chk(cudaIpcCloseMemHandle(q), "cudaIpcCloseMemHandle");
   for (size_t i = 0; i < sizeof(dev) / sizeof(dev[0]); ++i)
     if (dev[i]) chk(cudaFree(dev[i]), names[i]);
@@ -153,6 +156,7 @@ int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dty
   JCUDA(cudaMalloc(&p->sq, (size_t)m * 8));
   JCUDA(cudaMalloc(&p->blk, (size_t)p->nblk * 8));
   JCUDA(cudaMalloc(&p->dslot, 4 * 8));
+  JCUDA(cudaMalloc(&p->gbar, 8));
   JCUDA(cudaMalloc(&p->flags, 2 * 8));
   JCUDA(cudaMemsetAsync(p->flags, 0, 2 * 8, p->stream));
   JCUDA(cudaMalloc(&p->st, sizeof(jacobi::State)));
@@ -203,6 +207,14 @@ extern "C" int jacobi_plan_create(jacobi_plan** out, int64_t n, int dtype, const
     const char* e = getenv("JACOBI_SMALL_N");
     if (!(e && e[0] == '0')) p->cluster_C = jacobi::cluster_plan(n, dtype, &p->cluster_smem);
     rc = check_last("small-n cluster setup");
+  }
+  if (rc == 0 && !p->cluster_C) {  // persistent grid solver where it applies (NEXT-3, mid-size n)
+    const char* e = getenv("JACOBI_PERSIST");
+    const double a_bytes = (double)n * (double)n * (dtype == JACOBI_F32 ? 4.0 : 8.0);
+    const bool want = e ? e[0] == '1' : a_bytes <= kPersistMaxBytes;
+    if (want && n >= p->num_sms)
+      p->grid_G = jacobi::gridsync_plan(dtype, (int)((n + p->chunk - 1) / p->chunk), p->num_sms, &p->grid_smem);
+    cudaGetLastError();  // an unsupported configuration only leaves the path off
   }
   unsigned long long zr = 0;
   int nf = 0;
@@ -371,6 +383,12 @@ extern "C" int jacobi_plan_set_batch(jacobi_plan* p, int K) {
   return 0;
 }
 
+// The persistent grid solver applies to 1-GPU row-block plans with the max-norm stop rule.
+static bool use_grid(const jacobi_plan* p) {
+  return p->grid_G > 0 && p->nblocks == 1 && p->colblocks == 1 && !p->comm && !p->p2p && !p->colwise &&
+         p->norm == JACOBI_NORM_MAX;
+}
+
 extern "C" int jacobi_plan_info(const jacobi_plan* p, jacobi_plan_info_t* info) {
   if (!p || !info) return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_info: NULL argument");
   info->n = p->n;
@@ -392,6 +410,7 @@ extern "C" int jacobi_plan_info(const jacobi_plan* p, jacobi_plan_info_t* info) 
   info->num_variants = jacobi::num_variants();
   info->cluster_ctas =
       (p->cluster_C && p->nblocks == 1 && p->colblocks == 1 && !p->comm && !p->p2p) ? p->cluster_C : 0;
+  info->persistent_ctas = use_grid(p) ? p->grid_G : 0;
   return 0;
 }
 
@@ -554,6 +573,7 @@ static int solve_prepare(jacobi_plan* p, const double* b, const double* x0, bool
   JCUDA(cudaMemcpyAsync(p->b, b, (size_t)p->m * 8, kind, p->stream));
   JCUDA(cudaMemcpyAsync(p->x[0], x0, (size_t)p->n * 8, kind, p->stream));
   JCUDA(cudaMemsetAsync(p->st, 0, sizeof(jacobi::State), p->stream));
+  JCUDA(cudaMemsetAsync(p->gbar, 0, 8, p->stream));
   JCUDA(jacobi::launch_prepare(p->st, max_iter, tol, hist_dev, p->dslot, p->cnt, p->a_rows, p->b, p->m, p->x[0],
                                p->n, p->p2p ? p->flags : nullptr, p->stream));
   if (p->p2p_emul) {  // virtual ranks 1..P-1: their x^(0), slots and counters
@@ -646,6 +666,29 @@ static int solve_cluster(jacobi_plan* p, int64_t max_iter, jacobi::State* fin) {
   }
 }
 
+// Persistent path (NEXT-3, mid-size n): the solve in cooperative launches of at most
+// kMaxSweepsPerLaunch sweeps.
+static int solve_grid(jacobi_plan* p, int64_t max_iter, jacobi::State* fin) {
+  p->sweeps_launched = 0;
+  const jacobi::SweepArgs a = sweep_args(p, 0);
+  for (int64_t k0 = 1;;) {
+    const int64_t k1 = std::min<int64_t>(k0 + jacobi::kMaxSweepsPerLaunch - 1, max_iter);
+    JCUDA(jacobi::launch_solve_gridsync(p->dtype, a, p->gbar, k0, k1, p->grid_G, p->grid_smem, p->stream));
+    JCUDA(cudaMemcpyAsync(&p->st_host[0], p->st, sizeof(jacobi::State), cudaMemcpyDeviceToHost, p->stream));
+    JCUDA(cudaStreamSynchronize(p->stream));
+    p->sweeps_launched += 1;
+    if (p->st_host[0].fault)
+      return jacobi_set_error(JACOBI_ECUDA, "persistent solver: grid barrier wait timed out");
+    if (p->st_host[0].nonfinite) return nonfinite_error();
+    if (p->st_host[0].done) {
+      *fin = p->st_host[0];
+      return 0;
+    }
+    if (k1 >= max_iter) return jacobi_set_error(JACOBI_ECUDA, "internal: persistent solve ended without a stop decision");
+    k0 = k1 + 1;
+  }
+}
+
 static int solve_impl(jacobi_plan* p, const double* b, const double* x0, bool dev, int64_t max_iter, double tol,
                       double* x_out, int64_t* iters_out, double* hist) {
   if (!p || !b || !x0 || !x_out || !iters_out || max_iter < 0 || std::isnan(tol) || tol < 0)
@@ -677,6 +720,9 @@ static int solve_impl(jacobi_plan* p, const double* b, const double* x0, bool de
     fin.iters = 0;
   } else if (p->cluster_C && p->nblocks == 1 && p->colblocks == 1 && !p->comm && !p->p2p) {
     rc = solve_cluster(p, max_iter, &fin);
+    if (rc) return rc;
+  } else if (use_grid(p)) {
+    rc = solve_grid(p, max_iter, &fin);
     if (rc) return rc;
   } else {
     rc = solve_run(p, max_iter, &fin);

@@ -67,13 +67,27 @@ __device__ __forceinline__ void ld_a_p(const T* p, T (&v)[E], uint64_t pol) {
   else ld_a(p, v);
 }
 // x^(k-1) is read-only during the sweep (it lives in the other ping-pong buffer): L1-cached loads.
+// XL = 2: x^(k-1) was written by other SMs earlier in the same (persistent) launch — read it at L2
+// (ld.global.cg), never through a possibly stale L1 line.
 template <int XL>
 __device__ __forceinline__ void ld_x4(const double* p, double* v) {
-  if (XL)  // keep x^(k-1) in L1 with priority over everything else
+  if (XL == 1)  // keep x^(k-1) in L1 with priority over everything else
     asm("ld.global.nc.L1::evict_last.v4.f64 {%0,%1,%2,%3}, [%4];"
         : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+  else if (XL == 2)
+    asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
   else
     asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+}
+template <int XL>
+__device__ __forceinline__ double ld_x1(const double* p) {
+  if constexpr (XL == 2) {
+    double v;
+    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+  } else {
+    return *p;
+  }
 }
 template <int E, int XL = 0>
 __device__ __forceinline__ void ld_x(const double* p, double (&v)[E]) {
@@ -102,6 +116,12 @@ __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
 }
 
 __device__ __forceinline__ bool sweep_prologue(const SweepArgs& a, int j, bool leader) {
@@ -318,23 +338,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
 
 constexpr int kSlots = 4;
 
-template <typename T, int R, int NW, int U = 1, int XL = 0, bool PUSH = false, bool POL = false>
-__global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, const int j) {
-  extern __shared__ __align__(16) double s_part[];  // [kSlots][nchunks][R]
-  __shared__ __align__(8) uint64_t s_full[kSlots], s_empty[kSlots];
-  __shared__ int s_go;
-  if (threadIdx.x == 0) {
-    s_go = sweep_prologue(a, j, blockIdx.x == 0);
-    for (int q = 0; q < kSlots; ++q) {
-      mbar_init(&s_full[q], NW);
-      mbar_init(&s_empty[q], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (!s_go) return;
-
-  const int64_t k = a.st->kbase + j + 1;
+// One sweep k over the CTA's rows (the body of k_sweep_cta, shared with the persistent grid solver).
+// Tiles are numbered from tbase (a running count across the sweeps of a persistent launch) for the
+// slots and mbarrier parities of the partial-sum ring.  Returns this warp's max|dx| bits.
+template <typename T, int R, int NW, int U, int XL, bool PUSH, bool POL>
+__device__ __forceinline__ unsigned long long cta_sweep(const SweepArgs& a, const int64_t k, const int64_t tbase,
+                                                        double* s_part, uint64_t* s_full, uint64_t* s_empty) {
   const double* __restrict__ xo = (k & 1) ? a.x0buf : a.x1buf;  // x^(k-1)
   double* __restrict__ xn = (k & 1) ? a.x1buf : a.x0buf;        // x^(k)
   const T* __restrict__ A = static_cast<const T*>(a.A);
@@ -346,8 +355,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
   unsigned long long dmax = 0ull;
 
   auto finalize = [&](int t) {
-    const int q = t % kSlots;
-    mbar_wait(&s_full[q], (unsigned)((t / kSlots) & 1));
+    const int64_t tt = tbase + t;
+    const int q = (int)(tt % kSlots);
+    mbar_wait(&s_full[q], (unsigned)((tt / kSlots) & 1));
     const int64_t r0 = rb + (int64_t)t * R;
     const int nv = (int)min((int64_t)R, re - r0);
     if (lane < nv) {
@@ -360,7 +370,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
       } else {
         const double xnew = __ddiv_rn(__dsub_rn(a.b[row], s), a.diag[row]);
         const int64_t gi = a.row0 + row;
-        const double dx = __dsub_rn(xnew, xo[gi]);
+        const double dx = __dsub_rn(xnew, ld_x1<XL>(xo + gi));
         if constexpr (PUSH) {  // NEXT-1: push x_i^(k) into every rank's x^(k) buffer (NVLink stores)
           const PeerArgs* pe = a.peers;
           for (int p = 0; p < pe->P; ++p) ((k & 1) ? pe->x1[p] : pe->x0[p])[gi] = xnew;
@@ -377,10 +387,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
   };
 
   for (int t = 0; t < ntile; ++t) {
-    const int q = t % kSlots;
+    const int64_t tt = tbase + t;
+    const int q = (int)(tt % kSlots);
     const int64_t r0 = rb + (int64_t)t * R;
     const int nv = (int)min((int64_t)R, re - r0);
-    if (t >= kSlots) mbar_wait(&s_empty[q], (unsigned)(((t / kSlots) - 1) & 1));
+    if (tt >= kSlots) mbar_wait(&s_empty[q], (unsigned)(((tt / kSlots) - 1) & 1));
     const T* rowp[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) rowp[r] = A + (r0 + min(r, nv - 1)) * a.lda - a.col0;  // global columns
@@ -418,6 +429,28 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
     const unsigned long long o = __shfl_xor_sync(kFull, dmax, off);
     dmax = o > dmax ? o : dmax;
   }
+  return dmax;
+}
+
+template <typename T, int R, int NW, int U = 1, int XL = 0, bool PUSH = false, bool POL = false>
+__global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, const int j) {
+  extern __shared__ __align__(16) double s_part[];  // [kSlots][nchunks][R]
+  __shared__ __align__(8) uint64_t s_full[kSlots], s_empty[kSlots];
+  __shared__ int s_go;
+  if (threadIdx.x == 0) {
+    s_go = sweep_prologue(a, j, blockIdx.x == 0);
+    for (int q = 0; q < kSlots; ++q) {
+      mbar_init(&s_full[q], NW);
+      mbar_init(&s_empty[q], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (!s_go) return;
+
+  const int64_t k = a.st->kbase + j + 1;
+  const int lane = threadIdx.x & 31;
+  const unsigned long long dmax = cta_sweep<T, R, NW, U, XL, PUSH, POL>(a, k, 0, s_part, s_full, s_empty);
   if constexpr (!PUSH) {
     if (lane == 0) atomicMax(&a.dslot[k & 3], dmax);
   } else {
@@ -433,6 +466,79 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// k_solve_gridsync: sweeps k0..k1 in one cooperative launch (NEXT-3 for mid-size n: the graph of
+// sweep kernels pays ~8 µs per sweep in kernel boundaries and dependent global round trips when A
+// fits in or near the L2).  Each sweep is cta_sweep (same bits as k_sweep_cta) with x read at L2;
+// between sweeps a grid barrier (one release atomic per CTA on a global counter, an acquire spin by
+// one thread per CTA); after it every CTA evaluates the same stop test of PAPER.md:64-66 from the
+// same distance slot.  Waits are bounded (fault flag -> JACOBI_ECUDA instead of a hung GPU).
+template <typename T, int R, int NW, bool POL>
+__global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync(const SweepArgs a, unsigned long long* gbar,
+                                                               const int64_t k0, const int64_t k1) {
+  extern __shared__ __align__(16) double s_part[];  // [kSlots][nchunks][R]
+  __shared__ __align__(8) uint64_t s_full[kSlots], s_empty[kSlots];
+  __shared__ int s_go;
+  State* st = a.st;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kSlots; ++q) {
+      mbar_init(&s_full[q], NW);
+      mbar_init(&s_empty[q], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (*(volatile int32_t*)&st->done || st->nonfinite || *(volatile int32_t*)&st->fault) return;  // uniform
+  const int64_t rb = (int64_t)blockIdx.x * a.m / gridDim.x;
+  const int64_t re = (int64_t)(blockIdx.x + 1) * a.m / gridDim.x;
+  const int64_t ntile = (re - rb + R - 1) / R;
+  const int lane = threadIdx.x & 31;
+  for (int64_t k = k0;; ++k) {
+    if (threadIdx.x == 0) {
+      int go = 1;
+      if (k > k0) {  // grid barrier: every CTA has stored its x_i^(k-1) and max|dx| bits
+        const unsigned long long target = (unsigned long long)gridDim.x * (unsigned long long)(k - 1);
+        unsigned long long t0 = 0;
+        for (unsigned i = 0; ld_acquire_gpu(gbar) < target; ++i) {
+          if ((i & 1023) == 1023) {
+            const unsigned long long t = global_ns();
+            if (t0 == 0) t0 = t;
+            else if (t - t0 > 2000000000ull || *(volatile int32_t*)&st->fault) {
+              st->fault = 1;
+              go = 0;
+              break;
+            }
+          }
+        }
+      }
+      if (go && k >= 2) {  // stop test for sweep k-1, identical in every CTA
+        const double d = ld_x1<2>(reinterpret_cast<const double*>(a.dslot + ((k - 1) & 3)));  // bits of max|dx|
+        if (blockIdx.x == 0 && st->hist) st->hist[k - 2] = d;
+        if (d < st->tol) {
+          if (blockIdx.x == 0) { st->status = JACOBI_CONVERGED; st->iters = k - 1; st->done = 1; }
+          go = 0;
+        }
+      }
+      if (go && k > st->max_iter) {
+        if (blockIdx.x == 0) { st->status = JACOBI_MAX_ITER; st->iters = st->max_iter; st->done = 1; }
+        go = 0;
+      }
+      if (go && k > k1) go = 0;  // end of this launch's segment; the next launch resumes at k
+      if (go && blockIdx.x == 0) a.dslot[(k + 1) & 3] = 0ull;
+      s_go = go;
+    }
+    __syncthreads();
+    if (!s_go) break;
+    const unsigned long long dmax =
+        cta_sweep<T, R, NW, 1, 2, false, POL>(a, k, (k - k0) * ntile, s_part, s_full, s_empty);
+    if (lane == 0 && dmax) atomicMax(&a.dslot[k & 3], dmax);
+    __syncthreads();  // every x_i^(k) store and max|dx| atomic of this CTA has been issued
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(gbar, 1ull);
+    }
+  }
+}
 
 // ---------------------------------------------------------------------------------------------
 // k_sweep_panel: every warp owns whole rows.  CTA b of G owns rows [b*m/G, (b+1)*m/G); warp w of NW
@@ -873,6 +979,28 @@ cudaError_t launch_sweep(int dtype, int v, const SweepArgs& a, int j, int grid, 
   if (dtype == JACOBI_F32) V.f32<<<grid, V.threads, smem, s>>>(a, j);
   else V.f64<<<grid, V.threads, smem, s>>>(a, j);
   return cudaGetLastError();
+}
+
+// Persistent grid solver (k_solve_gridsync): one CTA per SM, co-resident (cooperative launch).
+int gridsync_plan(int dtype, int nchunks, int num_sms, size_t* smem) {
+  const int R = dtype == JACOBI_F32 ? 4 : 8;
+  *smem = (size_t)kSlots * nchunks * R * 8;
+  if (*smem > 200 * 1024) return 0;
+  auto fn = dtype == JACOBI_F32 ? k_solve_gridsync<float, 4, 16, true> : k_solve_gridsync<double, 8, 16, true>;
+  if (*smem > 48 * 1024 && cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem) != cudaSuccess)
+    return 0;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 512, *smem) != cudaSuccess || per_sm < 1) return 0;
+  return num_sms;
+}
+
+cudaError_t launch_solve_gridsync(int dtype, const SweepArgs& a, unsigned long long* gbar, int64_t k0, int64_t k1,
+                                  int grid, size_t smem, cudaStream_t s) {
+  SweepArgs aa = a;
+  void* args[] = {&aa, &gbar, &k0, &k1};
+  const void* fn = dtype == JACOBI_F32 ? (const void*)k_solve_gridsync<float, 4, 16, true>
+                                       : (const void*)k_solve_gridsync<double, 8, 16, true>;
+  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(512), args, smem, s);
 }
 
 cudaError_t launch_l2_partials(const double* sq, int64_t m, double* blk, const State* st, cudaStream_t s) {

@@ -1,0 +1,131 @@
+"""GPU: the persistent grid solver (k_solve_gridsync — the sweeps of a launch in one cooperative
+kernel, grid barrier between sweeps; NEXT-3 for mid-size n) against the graph-of-sweep-kernels path
+and the oracle.
+
+Each sweep runs the body of k_sweep_cta (same work split and summation order), so every iterate,
+every d_k and the iteration count must be bitwise identical to the graph path (R10), and
+within the north-star tolerance of the oracle (stop rule PAPER.md:61-66).
+"""
+import numpy as np
+import pytest
+
+import jacobi_gen as g
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def jb():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1403_5805_b200 as jb
+    return jb
+
+
+def dominant(n, seed, scale=None, f32=False):
+    rng = np.random.default_rng(seed)
+    A = rng.uniform(-1, 1, (n, n))
+    np.fill_diagonal(A, 0.0)
+    rs = np.abs(A).sum(1)
+    d = rs * scale if scale else rs + rng.uniform(1, 2, n)
+    np.fill_diagonal(A, d * rng.choice([-1.0, 1.0], n))
+    if f32:
+        A = A.astype(np.float32)
+    xs = rng.uniform(-1, 1, n)
+    return A, A.astype(np.float64) @ xs, xs
+
+
+def solve_both(jb, monkeypatch, A, b, max_iter, tol, x0=None):
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("JACOBI_PERSIST", mode)
+        with jb.Plan(A) as p:
+            assert (p.info.persistent_ctas > 0) == (mode == "1"), p.info.persistent_ctas
+            out[mode] = p.solve(b, x0, max_iter, tol, history=True)
+    return out["1"], out["0"]
+
+
+def same(r, q):
+    return ((r.status, r.iters) == (q.status, q.iters) and np.array_equal(r.x, q.x)
+            and np.array_equal(r.hist, q.hist, equal_nan=True))
+
+
+# several tiles per CTA with a ragged last tile; a ragged column tail; fewer than 8 rows per CTA;
+# fewer and more than 16 column chunks; fp32 A storage.
+@pytest.mark.parametrize("n,f32", [(700, False), (1000, False), (3001, False), (4096, False), (9000, False),
+                                   (2049, True), (5003, True)])
+def test_gridsync_bitwise_vs_graph_and_oracle(jb, monkeypatch, n, f32):
+    A, b, xs = dominant(n, 7 + n, scale=1.05, f32=f32)
+    r, q = solve_both(jb, monkeypatch, A, b, 25, 0.0)
+    assert same(r, q)
+    st_o, x_o, it_o, h_o = oracle.jacobi(A, b, None, 25, 0.0, nthreads=16, history=True)
+    assert r.iters == it_o == 25
+    assert np.max(np.abs(r.x - x_o)) / np.max(np.abs(x_o)) <= 1e-10
+    np.testing.assert_allclose(r.hist, h_o, rtol=1e-9, atol=1e-14)
+
+
+def test_gridsync_c2_config(jb, monkeypatch):
+    """BASELINE.json configs[1]: n = 4096, fixed 500 iterations (the default path for c2)."""
+    A, b, xs = g.host_system(g.CONFIGS["c2"])
+    r, q = solve_both(jb, monkeypatch, A, b, 500, 0.0)
+    assert same(r, q) and (r.status, r.iters) == (jb.MAX_ITER, 500)
+    assert np.max(np.abs(r.x - xs)) <= 1e-12  # P8 planted solution
+
+
+def test_gridsync_stop_rule_segments_split(jb, monkeypatch):
+    """tol stop inside a launch (strict <), max_iter exhausted across several
+    kMaxSweepsPerLaunch = 4096-sweep launches, max_iter = 1 (P3), split runs (P11), determinism (P13)."""
+    A, b, _ = dominant(2048, 11, scale=1.05)
+    r, q = solve_both(jb, monkeypatch, A, b, 5000, 1e-11)
+    assert same(r, q) and r.status == jb.CONVERGED
+    st_o, x_o, it_o = oracle.jacobi(A, b, None, 5000, 1e-11, nthreads=16)
+    assert (r.status, r.iters) == (st_o, it_o)
+    r, q = solve_both(jb, monkeypatch, A, b, 9000, 0.0)  # three launches: 4096 + 4096 + 808
+    assert same(r, q) and r.iters == 9000
+    r, q = solve_both(jb, monkeypatch, A, b, 1, 0.0)
+    assert same(r, q) and np.array_equal(r.x, b / np.diag(A))
+    monkeypatch.setenv("JACOBI_PERSIST", "1")
+    with jb.Plan(A) as p:
+        assert p.info.persistent_ctas > 0
+        r12 = p.solve(b, None, 12, 0.0)
+        r5 = p.solve(b, None, 5, 0.0)
+        r7 = p.solve(b, r5.x, 7, 0.0)
+        assert np.array_equal(r12.x, r7.x)
+        assert np.array_equal(p.solve(b, None, 12, 0.0).x, r12.x)
+        p.set_norm("l2")  # the Euclidean rule runs on the graph path
+        assert p.info.persistent_ctas == 0
+        p.set_norm("max")
+        p.set_row_blocks(4)  # P12a emulation runs on the graph path, same bits
+        assert p.info.persistent_ctas == 0 and np.array_equal(p.solve(b, None, 12, 0.0).x, r12.x)
+
+
+def test_gridsync_nan_sticky(jb, monkeypatch):
+    """The paper's raw regime (A, b ~ U[0,1]) diverges: max|dx| becomes NaN and stays
+    NaN, nothing converges, both paths run to max_iter with the same NaN pattern."""
+    rng = np.random.default_rng(3)
+    n = 1024
+    A = rng.uniform(0, 1, (n, n))
+    b = rng.uniform(0, 1, n)
+    r, q = solve_both(jb, monkeypatch, A, b, 300, 1e-6)
+    assert (r.status, r.iters) == (q.status, q.iters) == (jb.MAX_ITER, 300)
+    assert np.array_equal(np.isnan(r.x), np.isnan(q.x))
+    assert np.array_equal(r.hist, q.hist, equal_nan=True)
+
+
+def test_gridsync_device_borrowed(jb, monkeypatch):
+    """Borrowed device A and device solve, as bench.py and the size sweep use the path."""
+    import torch
+    A, b, _ = dominant(3000, 21, scale=1.05)
+    monkeypatch.setenv("JACOBI_PERSIST", "1")
+    dA = torch.from_numpy(A).cuda()
+    db = torch.from_numpy(b).cuda()
+    dx0 = torch.zeros(3000, dtype=torch.float64, device="cuda")
+    xo = torch.empty_like(dx0)
+    with jb.Plan(dA, n=3000) as p:
+        assert p.info.persistent_ctas > 0
+        r = p.solve_device(db, dx0, xo, 60, 0.0)
+    monkeypatch.setenv("JACOBI_PERSIST", "0")
+    with jb.Plan(A) as p:
+        q = p.solve(b, None, 60, 0.0)
+    assert r.iters == q.iters == 60 and np.array_equal(xo.cpu().numpy(), q.x)
