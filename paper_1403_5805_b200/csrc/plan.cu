@@ -17,8 +17,14 @@
 namespace {
 thread_local std::string g_err;
 constexpr int kLookahead = 2;
-// Persistent grid solver by default for A up to this size (profiles/size_sweep_r01.jsonl).
-constexpr double kPersistMaxBytes = 400e6;
+// Path choice by size (profiles/size_sweep_r01.jsonl, per-sweep µs, 400-sweep solves):
+// - the persistent grid solver removes the ~8 µs per-sweep floor of the graph of sweep kernels
+//   (fp64 n = 768-3584: 8.6-20.5 -> 5.2-17.3 µs; c2 4096: 21.8 -> 20.9; fp32 up to n = 8192 / 268 MB:
+//   52.0 -> 49.7) and ties or loses beyond (fp64 6144: 53.9 vs 52.9; 12288: 192.6 vs 186.0);
+// - the cluster solver (A in shared memory of 16 SMs) beats its ~5 µs floor only for small n
+//   (fp64 256: 2.35 µs, 448: 5.3 vs 5.1; fp32 256: 2.8 vs 4.7, 512: 8.3 vs 4.7).
+constexpr double kPersistMaxBytesF64 = 200e6, kPersistMaxBytesF32 = 300e6;
+constexpr int64_t kClusterPreferMaxN_F64 = 448, kClusterPreferMaxN_F32 = 320;
 
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 }  // namespace
@@ -208,10 +214,10 @@ extern "C" int jacobi_plan_create(jacobi_plan** out, int64_t n, int dtype, const
     if (!(e && e[0] == '0')) p->cluster_C = jacobi::cluster_plan(n, dtype, &p->cluster_smem);
     rc = check_last("small-n cluster setup");
   }
-  if (rc == 0 && !p->cluster_C) {  // persistent grid solver where it applies (NEXT-3, mid-size n)
+  if (rc == 0) {  // persistent grid solver where it applies (NEXT-3, mid-size n)
     const char* e = getenv("JACOBI_PERSIST");
     const double a_bytes = (double)n * (double)n * (dtype == JACOBI_F32 ? 4.0 : 8.0);
-    const bool want = e ? e[0] == '1' : a_bytes <= kPersistMaxBytes;
+    const bool want = e ? e[0] == '1' : a_bytes <= (dtype == JACOBI_F32 ? kPersistMaxBytesF32 : kPersistMaxBytesF64);
     if (want && n >= p->num_sms)
       p->grid_G = jacobi::gridsync_plan(dtype, (int)((n + p->chunk - 1) / p->chunk), p->num_sms, &p->grid_smem);
     cudaGetLastError();  // an unsupported configuration only leaves the path off
@@ -383,11 +389,22 @@ extern "C" int jacobi_plan_set_batch(jacobi_plan* p, int K) {
   return 0;
 }
 
-// The persistent grid solver applies to 1-GPU row-block plans with the max-norm stop rule.
-static bool use_grid(const jacobi_plan* p) {
+// The persistent grid solver applies to 1-GPU row-block plans with the max-norm stop rule; the
+// cluster solver (both norms) to 1-GPU plans whose A fits its shared memory.  Where both apply, the
+// cluster solver is preferred only for small n (measured crossover above) or when forced with
+// JACOBI_PERSIST=0.
+static bool grid_applies(const jacobi_plan* p) {
   return p->grid_G > 0 && p->nblocks == 1 && p->colblocks == 1 && !p->comm && !p->p2p && !p->colwise &&
          p->norm == JACOBI_NORM_MAX;
 }
+static bool use_cluster(const jacobi_plan* p) {
+  if (!(p->cluster_C && p->nblocks == 1 && p->colblocks == 1 && !p->comm && !p->p2p)) return false;
+  const char* e = getenv("JACOBI_PERSIST");
+  const bool force_grid = e && e[0] == '1';
+  return !grid_applies(p) ||
+         (!force_grid && p->n <= (p->dtype == JACOBI_F32 ? kClusterPreferMaxN_F32 : kClusterPreferMaxN_F64));
+}
+static bool use_grid(const jacobi_plan* p) { return grid_applies(p) && !use_cluster(p); }
 
 extern "C" int jacobi_plan_info(const jacobi_plan* p, jacobi_plan_info_t* info) {
   if (!p || !info) return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_info: NULL argument");
@@ -408,8 +425,7 @@ extern "C" int jacobi_plan_info(const jacobi_plan* p, jacobi_plan_info_t* info) 
   info->bytes_per_sweep = (double)p->m * (double)p->n * sA + 8.0 * (double)p->n + 16.0 * (double)p->m;
   info->variant = p->variant;
   info->num_variants = jacobi::num_variants();
-  info->cluster_ctas =
-      (p->cluster_C && p->nblocks == 1 && p->colblocks == 1 && !p->comm && !p->p2p) ? p->cluster_C : 0;
+  info->cluster_ctas = use_cluster(p) ? p->cluster_C : 0;
   info->persistent_ctas = use_grid(p) ? p->grid_G : 0;
   return 0;
 }
@@ -718,7 +734,7 @@ static int solve_impl(jacobi_plan* p, const double* b, const double* x0, bool de
     if (p->st_host[0].nonfinite) return nonfinite_error();
     fin.status = JACOBI_MAX_ITER;
     fin.iters = 0;
-  } else if (p->cluster_C && p->nblocks == 1 && p->colblocks == 1 && !p->comm && !p->p2p) {
+  } else if (use_cluster(p)) {
     rc = solve_cluster(p, max_iter, &fin);
     if (rc) return rc;
   } else if (use_grid(p)) {

@@ -129,3 +129,21 @@ def test_gridsync_device_borrowed(jb, monkeypatch):
     with jb.Plan(A) as p:
         q = p.solve(b, None, 60, 0.0)
     assert r.iters == q.iters == 60 and np.array_equal(xo.cpu().numpy(), q.x)
+
+
+@pytest.mark.parametrize("n,f32,path", [(256, False, "cluster"), (448, False, "cluster"), (600, False, "grid"),
+                                        (320, True, "cluster"), (600, True, "grid"), (3072, False, "grid"),
+                                        (4096, False, "grid"), (8192, False, "graph")])
+def test_default_path_by_size(jb, n, f32, path, monkeypatch):
+    """Default solver path by size (measured crossovers): the cluster solver for small n,
+    the persistent grid solver for mid-size A, the graph of sweep kernels beyond; the Euclidean rule
+    (not supported by the persistent solver) falls back to the cluster or graph path."""
+    monkeypatch.delenv("JACOBI_PERSIST", raising=False)
+    monkeypatch.delenv("JACOBI_SMALL_N", raising=False)
+    A = np.eye(n, dtype=np.float32 if f32 else np.float64) * 2.0
+    with jb.Plan(A) as p:
+        inf = p.info
+        got = "cluster" if inf.cluster_ctas else ("grid" if inf.persistent_ctas else "graph")
+        assert got == path, (n, f32, got)
+        p.set_norm("l2")
+        assert p.info.persistent_ctas == 0

@@ -425,6 +425,7 @@ def test_small_n_cluster_path_bitwise(jb, n, f32, monkeypatch):
     x0 = np.random.default_rng(n).uniform(-1, 1, n)
     runs = [(25, 0.0, "max"), (3000, 1e-12, "max"), (3000, 1e-12, "l2"), (4200, 0.0, "max")]
     res = {}
+    monkeypatch.setenv("JACOBI_PERSIST", "0")  # cluster vs graph of sweep kernels (persistent path: own tests)
     for small in ("1", "0"):
         monkeypatch.setenv("JACOBI_SMALL_N", small)
         with jb.Plan(A) as p:
