@@ -13,7 +13,7 @@ PKG       := paper_1403_5805_b200
 LIB_SRCS  := $(PKG)/csrc/sweep.cu $(PKG)/csrc/cluster.cu $(PKG)/csrc/plan.cu $(PKG)/csrc/dist.cu
 LIB_HDRS  := include/jacobi.h $(PKG)/csrc/internal.h
 
-all: oracle gen lib probe
+all: oracle gen lib lib-check probe
 
 oracle: oracle/liboracle.so
 oracle/liboracle.so: oracle/oracle.c
@@ -29,11 +29,17 @@ $(PKG)/libjacobi.so: $(LIB_SRCS) $(LIB_HDRS)
 	$(NVCC) $(NVFLAGS) -Iinclude -I$(NCCL_DIR)/include -shared -o $@ $(LIB_SRCS) \
 	    -L$(NCCL_DIR)/lib -l:libnccl.so.2 -Xlinker -rpath=$(NCCL_DIR)/lib 2> build_lib.log || (cat build_lib.log; false)
 
+# Bounds-checked build of the product (device-side checks of every tile's A / x ranges; debug aid).
+lib-check: $(PKG)/libjacobi_check.so
+$(PKG)/libjacobi_check.so: $(LIB_SRCS) $(LIB_HDRS)
+	$(NVCC) $(NVFLAGS) -DJACOBI_BOUNDS_CHECK -Iinclude -I$(NCCL_DIR)/include -shared -o $@ $(LIB_SRCS) \
+	    -L$(NCCL_DIR)/lib -l:libnccl.so.2 -Xlinker -rpath=$(NCCL_DIR)/lib 2> build_lib_check.log || (cat build_lib_check.log; false)
+
 probe: probes/bwprobe
 probes/bwprobe: probes/bwprobe.cu
 	$(NVCC) -O3 -std=c++17 $(ARCH) -lineinfo -o $@ $<
 
 clean:
-	rm -f oracle/liboracle.so jacobi_gen/libjacobigen.so $(PKG)/libjacobi.so probes/bwprobe build_lib.log
+	rm -f oracle/liboracle.so jacobi_gen/libjacobigen.so $(PKG)/libjacobi.so $(PKG)/libjacobi_check.so probes/bwprobe build_lib.log build_lib_check.log
 
-.PHONY: all oracle gen lib probe clean
+.PHONY: all oracle gen lib lib-check probe clean

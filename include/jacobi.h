@@ -182,6 +182,11 @@ int jacobi_version(void); /* 100 * major + minor */
 /* Name of a sweep-kernel variant ("k_sweep_cta R4 U1", ...; jacobi_plan_info_t.variant), or NULL
  * when 0 <= variant < num_variants does not hold.  Static storage, never freed.  No CUDA call. */
 const char* jacobi_variant_name(int variant);
+/* Bounds-checked build (libjacobi_check.so, make lib-check): returns 1 and writes the mask of bounds
+ * violations the sweep kernels recorded since the last reset (bit 0/1: A below/past its block, 2: past
+ * the row pitch, 3: x read past its buffer, 4: x ring copy, 5: epilogue row); reset != 0 clears it.
+ * The release library returns 0 and writes 0.  Debug aid replacing compute-sanitizer on this pool. */
+int jacobi_debug_bounds_check(unsigned long long* violations, int reset);
 
 #ifdef __cplusplus
 }

@@ -16,7 +16,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libjacobi.so")
+# JACOBI_LIB=check loads the bounds-checked build (make lib-check) — same API, checks in the kernels.
+LIB_PATH = os.path.join(_HERE, "libjacobi_check.so" if os.environ.get("JACOBI_LIB") == "check" else "libjacobi.so")
 
 CONVERGED, MAX_ITER = 0, 1
 EINVAL, EZERODIAG, ENONFINITE, ENOMEM, ECUDA, ENCCL, EINDIVISIBLE = -1, -2, -3, -4, -5, -6, -7
@@ -32,7 +33,14 @@ EXPORTS = ("jacobi_solve", "jacobi_solve_f32a", "jacobi_plan_create", "jacobi_pl
            "jacobi_nccl_unique_id", "jacobi_dist_plan_create", "jacobi_dist_plan_create_colwise",
            "jacobi_plan_set_col_blocks", "jacobi_plan_ipc_export", "jacobi_plan_ipc_attach",
            "jacobi_plan_set_p2p_emulation", "jacobi_bwprobe", "jacobi_last_error",
-           "jacobi_version", "jacobi_variant_name")
+           "jacobi_version", "jacobi_variant_name", "jacobi_debug_bounds_check")
+
+
+def bounds_violations(reset: bool = True):
+    """(checked_build, mask) from jacobi_debug_bounds_check (libjacobi_check.so records violations)."""
+    v = ctypes.c_ulonglong()
+    checked = _lib.jacobi_debug_bounds_check(ctypes.byref(v), 1 if reset else 0)
+    return bool(checked), int(v.value)
 
 
 def variant_name(v: int) -> str:
@@ -88,6 +96,7 @@ def _load():
         "jacobi_last_error": ([], ctypes.c_char_p),
         "jacobi_version": ([], i32),
         "jacobi_variant_name": ([i32], ctypes.c_char_p),
+        "jacobi_debug_bounds_check": ([P(ctypes.c_ulonglong), i32], i32),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)

@@ -61,7 +61,14 @@ struct SweepArgs {
   int nchunks;              // ceil(n / chunk)
   int tiles;                // ceil(m / R)
   int l2_keep_pm;           // per-mille of the rows loaded with L2 evict_last (variants with POL)
+  const void* a_base;       // the stored block's allocation and its extent in elements, and the
+  int64_t a_elems, x_len;   // x buffers' length: checked by the JACOBI_BOUNDS_CHECK build only
 };
+// Bounds-checked build (make lib-check -> libjacobi_check.so): every tile's A rows and columns, the
+// x range it reads and the rows it writes are checked against the allocations; a violation sets a
+// bit in a device flag that jacobi_debug_bounds_check() reports.  The release build compiles the
+// checks out.
+unsigned long long bounds_violations(bool reset);
 
 // Launchers (sweep.cu).  Return cudaGetLastError() of the launch.
 cudaError_t launch_sweep(int dtype, int variant, const SweepArgs& a, int j, int grid, cudaStream_t s);

@@ -37,6 +37,16 @@ int jacobi_set_error(int code, const std::string& msg) {
 extern "C" const char* jacobi_last_error(void) { return g_err.c_str(); }
 extern "C" int jacobi_version(void) { return 100; }
 extern "C" const char* jacobi_variant_name(int variant) { return jacobi::variant_name(variant); }
+extern "C" int jacobi_debug_bounds_check(unsigned long long* violations, int reset) {
+#ifdef JACOBI_BOUNDS_CHECK
+  if (violations) *violations = jacobi::bounds_violations(reset != 0);
+  return 1;
+#else
+  (void)reset;
+  if (violations) *violations = 0;
+  return 0;
+#endif
+}
 
 // Frees everything the plan owns.  Every release is checked; the first failure is reported through
 // jacobi_last_error (destroy itself cannot return a status) and the runtime's error state is cleared.
@@ -458,6 +468,12 @@ static jacobi::SweepArgs sweep_args(const jacobi_plan* p, int blk) {
   const int R = jacobi::variant_rows_dt(p->variant, p->dtype);
   a.tiles = (int)((mb + R - 1) / R);
   a.l2_keep_pm = p->l2_keep_pm;
+  a.a_base = p->dA;
+  a.a_elems = p->a_rows * p->lda;
+  a.x_len = p->x_len;
+#ifdef JACOBI_BOUNDS_CHECK
+  if (getenv("JACOBI_CHECK_SELFTEST")) a.a_elems -= p->lda;  // checker self-test: the last row is "outside"
+#endif
   return a;
 }
 

@@ -34,6 +34,39 @@ template <typename T> struct VecOf;
 template <> struct VecOf<double> { static constexpr int E = 4; };
 template <> struct VecOf<float> { static constexpr int E = 8; };
 
+#ifdef JACOBI_BOUNDS_CHECK
+__device__ unsigned long long g_oob = 0ull;
+#define JB_CHECK(cond, bit)                                        \
+  do {                                                             \
+    if (!(cond)) atomicOr(&g_oob, 1ull << (bit));                  \
+  } while (0)
+#else
+#define JB_CHECK(cond, bit) \
+  do {                      \
+  } while (0)
+#endif
+
+// Bounds of one tile x chunk: the R row pointers (indexed by global column), the columns the
+// accumulate loop loads ([c0, top): the whole chunk when it is full, else up to n rounded to the
+// 32-byte load), and the x range read.  Bits: 0 A below the block, 1 A past the block, 2 A past the
+// row pitch, 3 x past its buffer.
+template <typename T, int R>
+__device__ __forceinline__ void check_tile(const SweepArgs& a, const T* const (&rowp)[R], int64_t c0, int64_t c1) {
+#ifdef JACOBI_BOUNDS_CHECK
+  constexpr int E = VecOf<T>::E;
+  const int64_t last = min(c1, a.cend);
+  const int64_t top = (c1 - c0 == a.chunk) ? c0 + a.chunk : c0 + ((last - c0 + E - 1) / E) * E;
+  const T* base = static_cast<const T*>(a.a_base);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    JB_CHECK(rowp[r] + c0 >= base, 0);
+    JB_CHECK(rowp[r] + top <= base + a.a_elems, 1);
+    JB_CHECK(top - a.col0 <= a.lda, 2);
+  }
+  JB_CHECK(top <= a.x_len, 3);
+#endif
+}
+
 // 256-bit streaming load of A (read exactly once per sweep): no L1 allocation.
 __device__ __forceinline__ void ld_a(const double* p, double (&v)[4]) {
   asm("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
@@ -263,6 +296,7 @@ __global__ void __launch_bounds__(NT, (NT < 512 ? 512 / NT : 1)) k_sweep(const S
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[r] = 0.0;
 
+    check_tile<T, R>(a, rowp, c0, c1);
     accumulate_chunk<T, R, U>(rowp, R, xo, c0, c1, a.chunk, a.cend, g0, lane, acc);
     // Butterfly: every lane ends with the same, order-fixed row sums.
 #pragma unroll
@@ -288,6 +322,7 @@ __global__ void __launch_bounds__(NT, (NT < 512 ? 512 / NT : 1)) k_sweep(const S
     unsigned long long dbits = 0ull;
     if (lane < R && r0 + lane < a.m) {
       const int64_t row = r0 + lane;
+      JB_CHECK(a.row0 + row < a.x_len, 5);
       double s = __ldcg(a.part + row);
       for (int cc = 1; cc < a.nchunks; ++cc) s += __ldcg(a.part + (int64_t)cc * a.m + row);
       if (a.rsum) {  // column-wise partial product of this slab (epilogue after the reduction)
@@ -365,6 +400,7 @@ __device__ __forceinline__ unsigned long long cta_sweep(const SweepArgs& a, cons
       double s = sp[0];
       for (int c = 1; c < nch; ++c) s += sp[(size_t)c * R];
       const int64_t row = r0 + lane;
+      JB_CHECK(row >= 0 && row < a.m && a.row0 + row < a.x_len, 5);  // bit 5: epilogue row
       if (a.rsum) {  // column-wise partial product of this slab (epilogue after the reduction)
         a.rsum[row] = s;
       } else {
@@ -407,6 +443,7 @@ __device__ __forceinline__ unsigned long long cta_sweep(const SweepArgs& a, cons
       // Full tiles take the constant-row-count instance: with a run-time row count nvcc wraps each
       // row's load (and, for fp32, its converts) in a branch and keeps one A load in flight per warp
       // (c5 fell to 3.97 TB/s); with nv = R the loads are unconditional and software-pipelined.
+      check_tile<T, R>(a, rowp, c0, c1);
       if (nv == R) accumulate_chunk<T, R, U, XL, POL>(rowp, R, xo, c0, c1, a.chunk, a.cend, g0, lane, acc, pol);
       else accumulate_chunk<T, R, U, XL, POL>(rowp, nv, xo, c0, c1, a.chunk, a.cend, g0, lane, acc, pol);
 #pragma unroll
@@ -567,6 +604,7 @@ __device__ __forceinline__ void xring_issue(const XRing& q, const SweepArgs& a, 
   const int64_t c0 = a.col0 + (i % a.nchunks) * (int64_t)a.chunk;
   const int64_t cols = min((int64_t)a.chunk, a.cend - c0);
   const unsigned bytes = (unsigned)((cols * 8 + 15) & ~(int64_t)15);  // x is padded past n
+  JB_CHECK(c0 + (int64_t)(bytes / 8) <= a.x_len && (int64_t)(bytes / 8) <= a.chunk, 4);  // bit 4: x ring copy
   double* dst = q.xs + (size_t)slot * a.chunk;
   const unsigned bar = (unsigned)__cvta_generic_to_shared(&q.full[slot]);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the slot before the async write
@@ -591,6 +629,7 @@ __device__ __forceinline__ void panel_tile(const SweepArgs& a, const T* A, const
     for (int r = 0; r < R; ++r) acc[r] = 0.0;
     const int64_t c0 = a.col0 + (int64_t)c * a.chunk;
     const int64_t c1 = min(c0 + (int64_t)a.chunk, a.cend);
+    check_tile<T, R>(a, rowp, c0, c1);
     if constexpr (XSN > 0) {
       const int64_t i = item0 + c;
       const int slot = (int)(i % XSN);
@@ -692,6 +731,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_panel(const SweepArgs a, c
       if (lane == r) mine = s[r];
     if (lane < nv) {
       const int64_t row = r0 + lane;
+      JB_CHECK(row >= 0 && row < a.m && a.row0 + row < a.x_len, 5);
       if (a.rsum) {  // column-wise partial product of this slab (epilogue after the reduction)
         a.rsum[row] = mine;
       } else {
@@ -911,6 +951,21 @@ const Variant kVariants[] = {
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 }  // namespace
+
+unsigned long long bounds_violations(bool reset) {
+#ifdef JACOBI_BOUNDS_CHECK
+  unsigned long long v = 0;
+  cudaMemcpyFromSymbol(&v, g_oob, sizeof(v));
+  if (reset) {
+    const unsigned long long z = 0;
+    cudaMemcpyToSymbol(g_oob, &z, sizeof(z));
+  }
+  return v;
+#else
+  (void)reset;
+  return 0;
+#endif
+}
 
 int num_variants() { return kNumVariants; }
 const char* variant_name(int v) { return v >= 0 && v < kNumVariants ? kVariants[v].name : nullptr; }

@@ -1,7 +1,7 @@
-"""Small solves touching every kernel path, for compute-sanitizer (memcheck / racecheck / synccheck).
-
-Run ONE tool per gpurun call, e.g.
-  compute-sanitizer --tool memcheck --error-exitcode 9 python probes/sanitize_small.py
+"""Small solves touching every kernel path.  compute-sanitizer is closed on this GPU pool, so the
+driver for it is the bounds-checked build instead:
+  JACOBI_LIB=check python probes/sanitize_small.py   (exit 3 and the mask if a check fired)
+(tests/test_bounds_gpu.py runs it, plus a self-test of the checker.)
 """
 import os
 import sys
@@ -20,10 +20,19 @@ def dominant(n, seed, f32=False):
     return (A.astype(np.float32) if f32 else A), rng.uniform(-1, 1, n)
 
 
-for n, f32, variants in ((1, False, [None]), (37, False, [None]), (300, True, [None]),
-                         (8190, False, [None, "1", "6", "9", "10"]), (8190, True, [None])):
+# (n, fp32 A, variants, persistent modes): the cluster path (small n), the persistent grid solver
+# (mid n, JACOBI_PERSIST=1), and the graph path with the item / CTA / row-panel / x-smem / L2-keep
+# kernels, including ragged rows and columns.
+QUICK = "--quick" in sys.argv  # one graph-path case (checker self-test)
+CASES = ((1, False, [None], ["0"]), (37, False, [None], ["0"]), (300, True, [None], ["0"]),
+         (700, False, [None], ["1", "0"]), (3001, False, [None, "7", "12", "18"], ["1", "0"]),
+         (2049, True, [None, "18"], ["1", "0"]),
+         (8190, False, [None, "1", "6", "9", "10", "16", "19", "20"], ["0"]),
+         (8190, True, [None, "12", "18"], ["0"]))
+for n, f32, variants, modes in (((3001, False, [None], ["0"]),) if QUICK else CASES):
     A, b = dominant(n, n, f32)
-    for v in variants:
+    for v, mode in [(v, m) for v in variants for m in modes]:
+        os.environ["JACOBI_PERSIST"] = mode
         if v is None:
             os.environ.pop("JACOBI_SWEEP_VARIANT", None)
         else:
@@ -34,5 +43,9 @@ for n, f32, variants in ((1, False, [None]), (37, False, [None]), (300, True, [N
             if n % 2 == 0:
                 p.set_row_blocks(2)
                 p.solve(b, None, 5, 0.0)
-        print(n, f32, v, r.iters, r2.status, r2.iters, flush=True)
+        print(n, f32, v, mode, r.iters, r2.status, r2.iters, flush=True)
+checked, mask = jb.bounds_violations()
+if checked:
+    print(f"bounds check: violations mask = {mask:#x}", flush=True)
+    sys.exit(3 if mask else 0)
 print("sanitize_small ok")

@@ -88,3 +88,20 @@ def test_variant_names_without_gpu(jb):
     known = [n for n in names if not n.startswith("variant ")]
     assert len(known) >= 12 and len(set(known)) == len(known)
     assert jb._lib.jacobi_variant_name(-1) is None and jb._lib.jacobi_variant_name(10**6) is None
+
+
+def test_bounds_checked_build_exports_the_same_abi(jb):
+    """libjacobi_check.so (make lib-check) is the same C-ABI with device-side bounds checks: it exports
+    every header symbol and reports itself as checked; the release library reports 0 (checks compiled out)."""
+    import subprocess
+    so = os.path.join(ROOT, "paper_1403_5805_b200", "libjacobi_check.so")
+    if not os.path.exists(so):
+        r = subprocess.run(["make", "-C", ROOT, "lib-check"], capture_output=True, text=True)
+        assert r.returncode == 0, r.stdout + r.stderr
+    chk = ctypes.CDLL(so)
+    for name in _header_functions():
+        assert hasattr(chk, name), name
+    v = ctypes.c_ulonglong(7)
+    assert jb._lib.jacobi_debug_bounds_check(ctypes.byref(v), 0) == 0 and v.value == 0
+    chk.jacobi_debug_bounds_check.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
+    assert chk.jacobi_debug_bounds_check(ctypes.byref(v), 0) == 1
