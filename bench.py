@@ -207,6 +207,7 @@ def other_configs(jb, g, torch, stream):
                             "us_per_sweep": round(1e3 * best / r.iters, 2),
                             "effective_gbs": round(inf.bytes_per_sweep * its / 1e9, 1),
                             "path": (f"cluster x{inf.cluster_ctas}" if inf.cluster_ctas else
+                                     f"persistent x{inf.persistent_ctas}: cta_sweep" if inf.persistent_ctas else
                                      f"graph: {jb.variant_name(inf.variant)}")})
         del dA, db
         torch.cuda.empty_cache()
