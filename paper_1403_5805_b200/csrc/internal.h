@@ -78,8 +78,11 @@ cudaError_t launch_setup_diag(int dtype, const void* A, int64_t lda, int64_t m, 
 cudaError_t launch_scan_nonfinite_A(int dtype, const void* A, int64_t lda, int64_t m, int64_t n,
                                     int* flag, cudaStream_t s);
 cudaError_t launch_prepare(State* st, int64_t max_iter, double tol, double* hist, unsigned long long* dslot,
-                           unsigned* cnt, int64_t ncnt, const double* b, int64_t m, const double* x0, int64_t n,
-                           unsigned long long* flags, cudaStream_t s);
+                           unsigned* cnt, int64_t ncnt, double* b, const double* b_src, int64_t m, double* x0,
+                           const double* x0_src, int64_t n, unsigned long long* flags, unsigned long long* gbar,
+                           cudaStream_t s);
+cudaError_t launch_finalize(const State* st, const double* x0buf, const double* x1buf, double* dst, int64_t n,
+                            cudaStream_t s);
 cudaError_t launch_copy_pitched(int dtype, const void* src, int64_t src_ld, void* dst, int64_t dst_ld,
                                 int64_t rows, int64_t n, cudaStream_t s);
 int num_variants();

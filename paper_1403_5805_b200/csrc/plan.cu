@@ -601,13 +601,14 @@ static int ensure_graph(jacobi_plan* p) {
 // also scans b and x0 for NaN/Inf).  No host round trip: ENONFINITE is read with the stop state.
 static int solve_prepare(jacobi_plan* p, const double* b, const double* x0, bool dev, int64_t max_iter, double tol,
                          double* hist_dev) {
-  const cudaMemcpyKind kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-  JCUDA(cudaMemcpyAsync(p->b, b, (size_t)p->m * 8, kind, p->stream));
-  JCUDA(cudaMemcpyAsync(p->x[0], x0, (size_t)p->n * 8, kind, p->stream));
+  if (!dev) {  // host inputs: H2D copies; device inputs are copied by k_prepare itself
+    JCUDA(cudaMemcpyAsync(p->b, b, (size_t)p->m * 8, cudaMemcpyHostToDevice, p->stream));
+    JCUDA(cudaMemcpyAsync(p->x[0], x0, (size_t)p->n * 8, cudaMemcpyHostToDevice, p->stream));
+  }
   JCUDA(cudaMemsetAsync(p->st, 0, sizeof(jacobi::State), p->stream));
-  JCUDA(cudaMemsetAsync(p->gbar, 0, 8, p->stream));
-  JCUDA(jacobi::launch_prepare(p->st, max_iter, tol, hist_dev, p->dslot, p->cnt, p->a_rows, p->b, p->m, p->x[0],
-                               p->n, p->p2p ? p->flags : nullptr, p->stream));
+  JCUDA(jacobi::launch_prepare(p->st, max_iter, tol, hist_dev, p->dslot, p->cnt, p->a_rows, p->b, dev ? b : nullptr,
+                               p->m, p->x[0], dev ? x0 : nullptr, p->n, p->p2p ? p->flags : nullptr, p->gbar,
+                               p->stream));
   if (p->p2p_emul) {  // virtual ranks 1..P-1: their x^(0), slots and counters
     for (int r = 1; r < p->p2p; ++r)
       JCUDA(cudaMemcpyAsync(p->ex_x + (size_t)(r - 1) * 2 * p->x_len, p->x[0], (size_t)p->n * 8,
@@ -679,12 +680,15 @@ static int solve_run(jacobi_plan* p, int64_t max_iter, jacobi::State* fin) {
 }
 
 // Small-n path (NEXT-3): the whole solve in cluster launches of at most kMaxSweepsPerLaunch sweeps.
-static int solve_cluster(jacobi_plan* p, int64_t max_iter, jacobi::State* fin) {
+// dev_out (device solves): k_finalize copies x^(iters) there before the state is read back, so the
+// solve needs one host synchronisation.
+static int solve_cluster(jacobi_plan* p, int64_t max_iter, jacobi::State* fin, double* dev_out) {
   p->sweeps_launched = 0;
   for (int64_t k0 = 1;;) {
     const int64_t k1 = std::min<int64_t>(k0 + jacobi::kMaxSweepsPerLaunch - 1, max_iter);
     JCUDA(jacobi::launch_solve_cluster(p->dtype, p->cluster_C, p->cluster_smem, p->dA, p->lda, p->n, p->chunk,
                                        p->norm, p->diag, p->b, p->x[0], p->x[1], p->st, k0, k1, p->stream));
+    if (dev_out) JCUDA(jacobi::launch_finalize(p->st, p->x[0], p->x[1], dev_out, p->n, p->stream));
     JCUDA(cudaMemcpyAsync(&p->st_host[0], p->st, sizeof(jacobi::State), cudaMemcpyDeviceToHost, p->stream));
     JCUDA(cudaStreamSynchronize(p->stream));
     p->sweeps_launched += 1;
@@ -700,12 +704,13 @@ static int solve_cluster(jacobi_plan* p, int64_t max_iter, jacobi::State* fin) {
 
 // Persistent path (NEXT-3, mid-size n): the solve in cooperative launches of at most
 // kMaxSweepsPerLaunch sweeps.
-static int solve_grid(jacobi_plan* p, int64_t max_iter, jacobi::State* fin) {
+static int solve_grid(jacobi_plan* p, int64_t max_iter, jacobi::State* fin, double* dev_out) {
   p->sweeps_launched = 0;
   const jacobi::SweepArgs a = sweep_args(p, 0);
   for (int64_t k0 = 1;;) {
     const int64_t k1 = std::min<int64_t>(k0 + jacobi::kMaxSweepsPerLaunch - 1, max_iter);
     JCUDA(jacobi::launch_solve_gridsync(p->dtype, a, p->gbar, k0, k1, p->grid_G, p->grid_smem, p->stream));
+    if (dev_out) JCUDA(jacobi::launch_finalize(p->st, p->x[0], p->x[1], dev_out, p->n, p->stream));
     JCUDA(cudaMemcpyAsync(&p->st_host[0], p->st, sizeof(jacobi::State), cudaMemcpyDeviceToHost, p->stream));
     JCUDA(cudaStreamSynchronize(p->stream));
     p->sweeps_launched += 1;
@@ -744,6 +749,7 @@ static int solve_impl(jacobi_plan* p, const double* b, const double* x0, bool de
   int rc = solve_prepare(p, b, x0, dev, max_iter, tol, hist_dev);
   if (rc < 0) return rc;
   jacobi::State fin{};
+  bool finalized = false;  // x_out already written on the device (k_finalize, device solves)
   if (max_iter == 0) {  // X^0 (reading R14), once the inputs are known to be finite
     JCUDA(cudaMemcpyAsync(&p->st_host[0], p->st, sizeof(jacobi::State), cudaMemcpyDeviceToHost, p->stream));
     JCUDA(cudaStreamSynchronize(p->stream));
@@ -751,11 +757,13 @@ static int solve_impl(jacobi_plan* p, const double* b, const double* x0, bool de
     fin.status = JACOBI_MAX_ITER;
     fin.iters = 0;
   } else if (use_cluster(p)) {
-    rc = solve_cluster(p, max_iter, &fin);
+    rc = solve_cluster(p, max_iter, &fin, dev ? x_out : nullptr);
     if (rc) return rc;
+    finalized = dev;
   } else if (use_grid(p)) {
-    rc = solve_grid(p, max_iter, &fin);
+    rc = solve_grid(p, max_iter, &fin, dev ? x_out : nullptr);
     if (rc) return rc;
+    finalized = dev;
   } else {
     rc = solve_run(p, max_iter, &fin);
     if (rc) return rc;
@@ -765,10 +773,10 @@ static int solve_impl(jacobi_plan* p, const double* b, const double* x0, bool de
     JNCCL(ncclAllGather(xf + p->row0, xf, (size_t)p->m, ncclDouble, p->comm, p->stream));
   }
   const cudaMemcpyKind kind = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-  JCUDA(cudaMemcpyAsync(x_out, p->x[fin.iters & 1], (size_t)p->n * 8, kind, p->stream));
+  if (!finalized) JCUDA(cudaMemcpyAsync(x_out, p->x[fin.iters & 1], (size_t)p->n * 8, kind, p->stream));
   if (hist && !dev && fin.iters > 0)
     JCUDA(cudaMemcpyAsync(hist, hist_dev, (size_t)fin.iters * 8, cudaMemcpyDeviceToHost, p->stream));
-  JCUDA(cudaStreamSynchronize(p->stream));
+  if (!finalized || (hist && !dev && fin.iters > 0)) JCUDA(cudaStreamSynchronize(p->stream));
   JLAST("solve");
   *iters_out = fin.iters;
   return fin.status;

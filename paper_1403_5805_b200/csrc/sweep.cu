@@ -859,21 +859,46 @@ __global__ void k_scan_A(const T* __restrict__ A, int64_t lda, int64_t m, int64_
 // counters cleared, and the non-finite scan of b and x0 (PAPER.md:59 inputs; ENONFINITE is reported
 // when the host reads the final state).  The state was zeroed by a memset just before.
 __global__ void k_prepare(State* st, int64_t max_iter, double tol, double* hist, unsigned long long* dslot,
-                          unsigned* cnt, int64_t ncnt, const double* __restrict__ b, int64_t m,
-                          const double* __restrict__ x0, int64_t n, unsigned long long* flags) {
+                          unsigned* cnt, int64_t ncnt, double* __restrict__ b, const double* __restrict__ b_src,
+                          int64_t m, double* __restrict__ x0, const double* __restrict__ x0_src, int64_t n,
+                          unsigned long long* flags, unsigned long long* gbar) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
   if (tid == 0) {
     st->max_iter = max_iter;
     st->tol = tol;
     st->hist = hist;
+    if (gbar) *gbar = 0ull;
   }
   if (tid < 4) dslot[tid] = 0ull;
   if (flags && tid < 2) flags[tid] = 0ull;
   for (int64_t i = tid; i < ncnt; i += stride) cnt[i] = 0u;
   bool bad = false;
-  for (int64_t i = tid; i < m; i += stride) bad |= nonfinite(b[i]);
-  for (int64_t i = tid; i < n; i += stride) bad |= nonfinite(x0[i]);
+  // Device inputs are copied in here (one launch instead of two memcpys); host inputs were copied
+  // by the caller, and are only scanned.
+  for (int64_t i = tid; i < m; i += stride) {
+    const double v = b_src ? b_src[i] : b[i];
+    if (b_src) b[i] = v;
+    bad |= nonfinite(v);
+  }
+  for (int64_t i = tid; i < n; i += stride) {
+    const double v = x0_src ? x0_src[i] : x0[i];
+    if (x0_src) x0[i] = v;
+    bad |= nonfinite(v);
+  }
   if (bad) st->nonfinite = 1;
+}
+
+// Solve end, device x_out: copy x^(iters) (ping-pong buffer iters & 1) to the caller's buffer, decided
+// on the device from the final state — enqueued after every solver launch, before the state is read
+// back, so a device solve needs one host synchronisation.  Nothing is written unless the solve has
+// finished (done) without failing (non-finite input, a wait fault): x_out is only written for a
+// status >= 0.
+__global__ void k_finalize(const State* st, const double* __restrict__ x0buf, const double* __restrict__ x1buf,
+                           double* __restrict__ dst, int64_t n) {
+  if (!st->done || st->nonfinite || st->fault) return;  // only a finished, successful solve
+  const double* src = (st->iters & 1) ? x1buf : x0buf;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
 }
 
 template <typename T>
@@ -1100,10 +1125,18 @@ cudaError_t launch_scan_nonfinite_A(int dtype, const void* A, int64_t lda, int64
 }
 
 cudaError_t launch_prepare(State* st, int64_t max_iter, double tol, double* hist, unsigned long long* dslot,
-                           unsigned* cnt, int64_t ncnt, const double* b, int64_t m, const double* x0, int64_t n,
-                           unsigned long long* flags, cudaStream_t s) {
+                           unsigned* cnt, int64_t ncnt, double* b, const double* b_src, int64_t m, double* x0,
+                           const double* x0_src, int64_t n, unsigned long long* flags, unsigned long long* gbar,
+                           cudaStream_t s) {
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((std::max(n, ncnt) + 255) / 256, 592));
-  k_prepare<<<grid, 256, 0, s>>>(st, max_iter, tol, hist, dslot, cnt, ncnt, b, m, x0, n, flags);
+  k_prepare<<<grid, 256, 0, s>>>(st, max_iter, tol, hist, dslot, cnt, ncnt, b, b_src, m, x0, x0_src, n, flags, gbar);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(const State* st, const double* x0buf, const double* x1buf, double* dst, int64_t n,
+                            cudaStream_t s) {
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 592));
+  k_finalize<<<grid, 256, 0, s>>>(st, x0buf, x1buf, dst, n);
   return cudaGetLastError();
 }
 
