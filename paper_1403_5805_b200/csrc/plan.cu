@@ -6,6 +6,7 @@
 // pinned memory behind each batch); sweeps after the device's stop decision exit in their prologue.
 // No batch is issued beyond ceil(max_iter / K), so tol = 0 runs never wait on a poll.
 #include "internal.h"
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX: ranges cost nothing unless a tracing tool is attached
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -17,6 +18,14 @@
 namespace {
 thread_local std::string g_err;
 constexpr int kLookahead = 2;
+
+// NVTX range for tracing tools (Nsight Systems / ncu --nvtx): plan setup, solve phases.
+struct Range {
+  explicit Range(const char* name) { nvtxRangePushA(name); }
+  ~Range() { nvtxRangePop(); }
+  Range(const Range&) = delete;
+  Range& operator=(const Range&) = delete;
+};
 // Path choice by size (profiles/size_sweep_r01.jsonl, per-sweep µs, 400-sweep solves):
 // - the persistent grid solver removes the ~8 µs per-sweep floor of the graph of sweep kernels
 //   (fp64 n = 768-3584: 8.6-20.5 -> 5.2-17.3 µs; c2 4096: 21.8 -> 20.9; fp32 up to n = 8192 / 268 MB:
@@ -106,6 +115,7 @@ static void choose_variant(const jacobi_plan* p, int64_t ncols, int* variant, in
 // (row-wise) or the n x m column slab [row0, row0 + m) (column-wise, NEXT-4).
 int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dtype, const void* A, int64_t a_rows,
                      int64_t a_cols, int64_t lda, int a_on_device, void* stream) {
+  Range nvtx_range("jacobi: plan setup (A upload)");
   JLAST("pending CUDA error before plan creation");
   p->n = n;
   p->m = m;
@@ -601,6 +611,7 @@ static int ensure_graph(jacobi_plan* p) {
 // also scans b and x0 for NaN/Inf).  No host round trip: ENONFINITE is read with the stop state.
 static int solve_prepare(jacobi_plan* p, const double* b, const double* x0, bool dev, int64_t max_iter, double tol,
                          double* hist_dev) {
+  Range nvtx_range("jacobi: solve prepare");
   if (!dev) {  // host inputs: H2D copies; device inputs are copied by k_prepare itself
     JCUDA(cudaMemcpyAsync(p->b, b, (size_t)p->m * 8, cudaMemcpyHostToDevice, p->stream));
     JCUDA(cudaMemcpyAsync(p->x[0], x0, (size_t)p->n * 8, cudaMemcpyHostToDevice, p->stream));
@@ -625,6 +636,7 @@ static int nonfinite_error() { return jacobi_set_error(JACOBI_ENONFINITE, "b or 
 
 // Runs graph batches until the device decides to stop.  Fills *fin with the final state.
 static int solve_run(jacobi_plan* p, int64_t max_iter, jacobi::State* fin) {
+  Range nvtx_range("jacobi: sweeps (CUDA graph batches)");
   int rc = ensure_graph(p);
   if (rc) return rc;
   const int64_t K = p->batch;
@@ -683,6 +695,7 @@ static int solve_run(jacobi_plan* p, int64_t max_iter, jacobi::State* fin) {
 // dev_out (device solves): k_finalize copies x^(iters) there before the state is read back, so the
 // solve needs one host synchronisation.
 static int solve_cluster(jacobi_plan* p, int64_t max_iter, jacobi::State* fin, double* dev_out) {
+  Range nvtx_range("jacobi: sweeps (cluster solver)");
   p->sweeps_launched = 0;
   for (int64_t k0 = 1;;) {
     const int64_t k1 = std::min<int64_t>(k0 + jacobi::kMaxSweepsPerLaunch - 1, max_iter);
@@ -705,6 +718,7 @@ static int solve_cluster(jacobi_plan* p, int64_t max_iter, jacobi::State* fin, d
 // Persistent path (NEXT-3, mid-size n): the solve in cooperative launches of at most
 // kMaxSweepsPerLaunch sweeps.
 static int solve_grid(jacobi_plan* p, int64_t max_iter, jacobi::State* fin, double* dev_out) {
+  Range nvtx_range("jacobi: sweeps (persistent grid solver)");
   p->sweeps_launched = 0;
   const jacobi::SweepArgs a = sweep_args(p, 0);
   for (int64_t k0 = 1;;) {
@@ -728,6 +742,7 @@ static int solve_grid(jacobi_plan* p, int64_t max_iter, jacobi::State* fin, doub
 
 static int solve_impl(jacobi_plan* p, const double* b, const double* x0, bool dev, int64_t max_iter, double tol,
                       double* x_out, int64_t* iters_out, double* hist) {
+  Range nvtx_range("jacobi: solve");
   if (!p || !b || !x0 || !x_out || !iters_out || max_iter < 0 || std::isnan(tol) || tol < 0)
     return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_solve: bad argument (NULL pointer, max_iter < 0, tol < 0 or NaN)");
   JCUDA(cudaSetDevice(p->device));
