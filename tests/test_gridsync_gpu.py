@@ -147,3 +147,27 @@ def test_default_path_by_size(jb, n, f32, path, monkeypatch):
         assert got == path, (n, f32, got)
         p.set_norm("l2")
         assert p.info.persistent_ctas == 0
+
+
+@pytest.mark.parametrize("n", [256, 1000, 8192])  # cluster, persistent and graph paths
+def test_device_solve_x_out_aliases_x0(jb, n, monkeypatch):
+    """include/jacobi.h: x_out may alias x0 (inputs are copied in before any write), on every path;
+    and x_out is untouched when the solve fails (non-finite b -> ENONFINITE)."""
+    import torch
+    monkeypatch.delenv("JACOBI_PERSIST", raising=False)
+    A, b, _ = dominant(n, 41 + n, scale=1.05)
+    dA = torch.from_numpy(A).cuda()
+    db = torch.from_numpy(b).cuda()
+    x0 = np.random.default_rng(n).uniform(-1, 1, n)
+    with jb.Plan(dA, n=n) as p:
+        ref_x = torch.empty(n, dtype=torch.float64, device="cuda")
+        r = p.solve_device(db, torch.from_numpy(x0).cuda(), ref_x, 30, 0.0)
+        io = torch.from_numpy(x0).cuda()
+        q = p.solve_device(db, io, io, 30, 0.0)  # x_out is x0
+        assert (q.status, q.iters) == (r.status, r.iters) and torch.equal(io, ref_x)
+        bad = db.clone()
+        bad[n // 2] = float("nan")
+        keep = io.clone()
+        with pytest.raises(jb.JacobiError) as ei:
+            p.solve_device(bad, io, io, 30, 0.0)
+        assert ei.value.status == jb.ENONFINITE and torch.equal(io, keep)
