@@ -114,7 +114,9 @@ cudaError_t launch_l2_partials(const double* sq, int64_t m, double* blk, const S
 cudaError_t launch_l2_final(const double* blk, int64_t nblk, unsigned long long* dslot, State* st, int j,
                             cudaStream_t s);
 double bwprobe(int64_t nbytes, int reps);
-// Persistent grid solver (NEXT-3, mid-size n): sweeps k0..k1 in one cooperative launch.
+// Persistent grid solver (NEXT-3, mid-size n): sweeps k0..k1 in one cooperative launch.  With the
+// Euclidean rule every CTA reduces all rows' dx^2 itself, for at most kGridMaxL2Rows rows.
+enum : int64_t { kGridMaxL2Rows = 64 * kL2Block };
 int gridsync_plan(int dtype, int nchunks, int num_sms, size_t* smem);
 cudaError_t launch_solve_gridsync(int dtype, const SweepArgs& a, unsigned long long* gbar, int64_t k0, int64_t k1,
                                   int grid, size_t smem, cudaStream_t s);

@@ -179,7 +179,7 @@ int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dty
   JCUDA(cudaMalloc(&p->part, (size_t)(nchunks * a_rows) * 8));
   JCUDA(cudaMalloc(&p->cnt, (size_t)a_rows * 4));
   p->nblk = (m + jacobi::kL2Block - 1) / jacobi::kL2Block;
-  JCUDA(cudaMalloc(&p->sq, (size_t)m * 8));
+  JCUDA(cudaMalloc(&p->sq, (size_t)m * 2 * 8));  // two halves: the persistent solver double-buffers dx^2
   JCUDA(cudaMalloc(&p->blk, (size_t)p->nblk * 8));
   JCUDA(cudaMalloc(&p->dslot, 4 * 8));
   JCUDA(cudaMalloc(&p->gbar, 8));
@@ -409,13 +409,13 @@ extern "C" int jacobi_plan_set_batch(jacobi_plan* p, int K) {
   return 0;
 }
 
-// The persistent grid solver applies to 1-GPU row-block plans with the max-norm stop rule; the
-// cluster solver (both norms) to 1-GPU plans whose A fits its shared memory.  Where both apply, the
+// The persistent grid solver applies to 1-GPU row-block plans (the Euclidean rule up to
+// kGridMaxL2Rows rows); the cluster solver (both norms) to 1-GPU plans whose A fits its shared memory.  Where both apply, the
 // cluster solver is preferred only for small n (measured crossover above) or when forced with
 // JACOBI_PERSIST=0.
 static bool grid_applies(const jacobi_plan* p) {
   return p->grid_G > 0 && p->nblocks == 1 && p->colblocks == 1 && !p->comm && !p->p2p && !p->colwise &&
-         p->norm == JACOBI_NORM_MAX;
+         (p->norm == JACOBI_NORM_MAX || p->m <= (int64_t)jacobi::kGridMaxL2Rows);
 }
 static bool use_cluster(const jacobi_plan* p) {
   if (!(p->cluster_C && p->nblocks == 1 && p->colblocks == 1 && !p->comm && !p->p2p)) return false;

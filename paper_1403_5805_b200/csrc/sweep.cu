@@ -510,12 +510,17 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
 // between sweeps a grid barrier (one release atomic per CTA on a global counter, an acquire spin by
 // one thread per CTA); after it every CTA evaluates the same stop test of PAPER.md:64-66 from the
 // same distance slot.  Waits are bounded (fault flag -> JACOBI_ECUDA instead of a hung GPU).
+constexpr int kGridMaxL2Blocks = 64;  // Euclidean rule in the persistent solver: m <= 64 * kL2Block rows
+
 template <typename T, int R, int NW, bool POL>
 __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync(const SweepArgs a, unsigned long long* gbar,
                                                                const int64_t k0, const int64_t k1) {
   extern __shared__ __align__(16) double s_part[];  // [kSlots][nchunks][R]
   __shared__ __align__(8) uint64_t s_full[kSlots], s_empty[kSlots];
   __shared__ int s_go;
+  __shared__ double s_red[NW * 32];             // Euclidean rule: two 256-row block trees at a time
+  __shared__ double s_blk[kGridMaxL2Blocks];    // ... and the block partials
+  __shared__ double s_d2;                       // ... and sum of squares
   State* st = a.st;
   if (threadIdx.x == 0) {
     for (int q = 0; q < kSlots; ++q) {
@@ -530,10 +535,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync(const SweepArgs a
   const int64_t re = (int64_t)(blockIdx.x + 1) * a.m / gridDim.x;
   const int64_t ntile = (re - rb + R - 1) / R;
   const int lane = threadIdx.x & 31;
+  const bool l2 = a.norm == JACOBI_NORM_L2;
   for (int64_t k = k0;; ++k) {
     if (threadIdx.x == 0) {
       int go = 1;
-      if (k > k0) {  // grid barrier: every CTA has stored its x_i^(k-1) and max|dx| bits
+      if (k > k0) {  // grid barrier: every CTA has stored its x_i^(k-1), max|dx| bits (and dx^2)
         const unsigned long long target = (unsigned long long)gridDim.x * (unsigned long long)(k - 1);
         unsigned long long t0 = 0;
         for (unsigned i = 0; ld_acquire_gpu(gbar) < target; ++i) {
@@ -548,8 +554,41 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync(const SweepArgs a
           }
         }
       }
+      s_go = go;
+    }
+    __syncthreads();
+    if (l2 && s_go && k >= 2) {
+      // The Euclidean distance of PAPER.md:94 over all rows, computed redundantly by every CTA in the
+      // order of k_l2_partials / k_l2_final (256-row shared-memory trees, then a strided ascending
+      // warp sum and a butterfly), so the bits equal the graph path's.  dx^2 of sweep k-1 lives in
+      // the half (k-1) & 1 of the double-buffered sq array; sweep k writes the other half.
+      const double* sq = a.sq + ((k - 1) & 1) * a.m;
+      const int64_t nblk = (a.m + kL2Block - 1) / kL2Block;
+      const int half = threadIdx.x / kL2Block, t = threadIdx.x % kL2Block;
+      for (int64_t b0 = 0; b0 < nblk; b0 += NW * 32 / kL2Block) {
+        const int64_t blk = b0 + half, i = blk * kL2Block + t;
+        s_red[threadIdx.x] = (blk < nblk && i < a.m) ? ld_x1<2>(sq + i) : 0.0;
+        __syncthreads();
+        for (int off = kL2Block / 2; off > 0; off >>= 1) {
+          if (t < off) s_red[threadIdx.x] = __dadd_rn(s_red[threadIdx.x], s_red[threadIdx.x + off]);
+          __syncthreads();
+        }
+        if (t == 0 && blk < nblk) s_blk[blk] = s_red[threadIdx.x];
+        __syncthreads();
+      }
+      if (threadIdx.x < 32) {
+        double v = 0.0;
+        for (int64_t q = threadIdx.x; q < nblk; q += 32) v = __dadd_rn(v, s_blk[q]);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v = __dadd_rn(v, __shfl_xor_sync(kFull, v, off));
+        if (threadIdx.x == 0) s_d2 = __dsqrt_rn(v);
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      int go = s_go;
       if (go && k >= 2) {  // stop test for sweep k-1, identical in every CTA
-        const double d = ld_x1<2>(reinterpret_cast<const double*>(a.dslot + ((k - 1) & 3)));  // bits of max|dx|
+        const double d = l2 ? s_d2 : ld_x1<2>(reinterpret_cast<const double*>(a.dslot + ((k - 1) & 3)));
         if (blockIdx.x == 0 && st->hist) st->hist[k - 2] = d;
         if (d < st->tol) {
           if (blockIdx.x == 0) { st->status = JACOBI_CONVERGED; st->iters = k - 1; st->done = 1; }
@@ -566,8 +605,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync(const SweepArgs a
     }
     __syncthreads();
     if (!s_go) break;
+    SweepArgs ak = a;
+    ak.sq = a.sq + (k & 1) * a.m;  // double-buffered dx^2 (Euclidean rule)
     const unsigned long long dmax =
-        cta_sweep<T, R, NW, 1, 2, false, POL>(a, k, (k - k0) * ntile, s_part, s_full, s_empty);
+        cta_sweep<T, R, NW, 1, 2, false, POL>(ak, k, (k - k0) * ntile, s_part, s_full, s_empty);
     if (lane == 0 && dmax) atomicMax(&a.dslot[k & 3], dmax);
     __syncthreads();  // every x_i^(k) store and max|dx| atomic of this CTA has been issued
     if (threadIdx.x == 0) {

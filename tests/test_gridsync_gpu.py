@@ -93,8 +93,8 @@ def test_gridsync_stop_rule_segments_split(jb, monkeypatch):
         r7 = p.solve(b, r5.x, 7, 0.0)
         assert np.array_equal(r12.x, r7.x)
         assert np.array_equal(p.solve(b, None, 12, 0.0).x, r12.x)
-        p.set_norm("l2")  # the Euclidean rule runs on the graph path
-        assert p.info.persistent_ctas == 0
+        p.set_norm("l2")  # the Euclidean rule runs in the persistent solver too (m <= 16384)
+        assert p.info.persistent_ctas > 0
         p.set_norm("max")
         p.set_row_blocks(4)  # P12a emulation runs on the graph path, same bits
         assert p.info.persistent_ctas == 0 and np.array_equal(p.solve(b, None, 12, 0.0).x, r12.x)
@@ -137,7 +137,7 @@ def test_gridsync_device_borrowed(jb, monkeypatch):
 def test_default_path_by_size(jb, n, f32, path, monkeypatch):
     """Default solver path by size (measured crossovers): the cluster solver for small n,
     the persistent grid solver for mid-size A, the graph of sweep kernels beyond; the Euclidean rule
-    (not supported by the persistent solver) falls back to the cluster or graph path."""
+    keeps the persistent solver up to 16384 rows."""
     monkeypatch.delenv("JACOBI_PERSIST", raising=False)
     monkeypatch.delenv("JACOBI_SMALL_N", raising=False)
     A = np.eye(n, dtype=np.float32 if f32 else np.float64) * 2.0
@@ -146,7 +146,7 @@ def test_default_path_by_size(jb, n, f32, path, monkeypatch):
         got = "cluster" if inf.cluster_ctas else ("grid" if inf.persistent_ctas else "graph")
         assert got == path, (n, f32, got)
         p.set_norm("l2")
-        assert p.info.persistent_ctas == 0
+        assert (p.info.persistent_ctas > 0) == (path == "grid")
 
 
 @pytest.mark.parametrize("n", [256, 1000, 8192])  # cluster, persistent and graph paths
@@ -171,3 +171,22 @@ def test_device_solve_x_out_aliases_x0(jb, n, monkeypatch):
         with pytest.raises(jb.JacobiError) as ei:
             p.solve_device(bad, io, io, 30, 0.0)
         assert ei.value.status == jb.ENONFINITE and torch.equal(io, keep)
+
+
+@pytest.mark.parametrize("n,f32", [(700, False), (4096, False), (3001, True)])
+def test_gridsync_euclidean_rule_bitwise(jb, monkeypatch, n, f32):
+    """The paper's Euclidean stop rule in the persistent solver: every CTA reduces all
+    rows' dx^2 in the order of k_l2_partials/k_l2_final, so histories, stop iterations and iterates
+    equal the graph path's bit for bit, and the stop iteration matches the oracle's Euclidean rule."""
+    A, b, _ = dominant(n, 3 + n, scale=1.05, f32=f32)
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("JACOBI_PERSIST", mode)
+        with jb.Plan(A) as p:
+            p.set_norm("l2")
+            assert (p.info.persistent_ctas > 0) == (mode == "1")
+            out[mode] = (p.solve(b, None, 40, 0.0, history=True), p.solve(b, None, 5000, 1e-11, history=True))
+    for r, q in zip(out["1"], out["0"]):
+        assert same(r, q)
+    st_o, x_o, it_o = oracle.jacobi(A, b, None, 5000, 1e-11, nthreads=16, norm="l2")
+    assert (out["1"][1].status, out["1"][1].iters) == (st_o, it_o)
