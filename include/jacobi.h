@@ -14,7 +14,14 @@
  *   Precondition a_ii != 0: violated -> JACOBI_EZERODIAG (lowest such i).
  *   Row-block distribution (§3 / §3.1): rank r of P owns rows [r*n/P, (r+1)*n/P);
  *       P must divide n.  Every sweep ends with an allgather of x (the MPI_Allgather variant of
- *       §3.1, done with NCCL over NVLink) and a one-scalar max allreduce of d_k.
+ *       §3.1, done with NCCL over NVLink) and a one-scalar max allreduce of d_k — or, after
+ *       jacobi_plan_ipc_attach, with the fused exchange: the sweep kernel itself stores its new x
+ *       rows into every peer's buffer over NVLink and signals their arrival counters (§3.3 one-sided
+ *       puts; overlapping transfer and compute).
+ *   Single-GPU solver path (chosen per plan from measured crossovers, same results bit for bit):
+ *       small n: one thread-block-cluster launch with A in shared memory; mid-size A (<= 200 MB
+ *       fp64 / 300 MB fp32): persistent cooperative launches with a grid barrier per sweep; larger
+ *       A: CUDA graphs of sweep kernels.  jacobi_plan_info reports which.
  *
  * Conventions (all functions):
  *   - Sizes are int64_t.  A is row-major: a_ij = A[i*lda + j], lda >= n (elements).  b, x0, x_out
