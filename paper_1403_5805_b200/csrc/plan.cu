@@ -410,9 +410,9 @@ extern "C" int jacobi_plan_set_batch(jacobi_plan* p, int K) {
 }
 
 // The persistent grid solver applies to 1-GPU row-block plans (the Euclidean rule up to
-// kGridMaxL2Rows rows); the cluster solver (both norms) to 1-GPU plans whose A fits its shared memory.  Where both apply, the
-// cluster solver is preferred only for small n (measured crossover above) or when forced with
-// JACOBI_PERSIST=0.
+// kGridMaxL2Rows rows); the cluster solver (both norms) to 1-GPU plans whose A fits its shared
+// memory.  Where both apply, the cluster solver is preferred only for small n (the measured
+// crossover above) unless JACOBI_PERSIST=1 forces the grid solver.
 static bool grid_applies(const jacobi_plan* p) {
   return p->grid_G > 0 && p->nblocks == 1 && p->colblocks == 1 && !p->comm && !p->p2p && !p->colwise &&
          (p->norm == JACOBI_NORM_MAX || p->m <= (int64_t)jacobi::kGridMaxL2Rows);
