@@ -407,9 +407,17 @@ __device__ __forceinline__ unsigned long long cta_sweep(const SweepArgs& a, cons
   auto finalize = [&](int t) {
     const int64_t tt = tbase + t;
     const int q = (int)(tt % kSlots);
-    mbar_wait(&s_full[q], (unsigned)((tt / kSlots) & 1));
     const int64_t r0 = rb + (int64_t)t * R;
     const int nv = (int)min((int64_t)R, re - r0);
+    // The epilogue's own operands (b_i, a_ii, x_i^(k-1)) do not depend on the partial sums: load
+    // them before waiting for the tile, so their latency hides behind the other warps' work.
+    double bi = 0.0, dii = 1.0, xoi = 0.0;
+    if (lane < nv && !a.rsum) {
+      bi = a.b[r0 + lane];
+      dii = a.diag[r0 + lane];
+      xoi = ld_x1<XL>(xo + a.row0 + r0 + lane);
+    }
+    mbar_wait(&s_full[q], (unsigned)((tt / kSlots) & 1));
     if (lane < nv) {
       const double* sp = s_part + (size_t)q * nch * R + lane;
       double s = sp[0];
@@ -419,9 +427,9 @@ __device__ __forceinline__ unsigned long long cta_sweep(const SweepArgs& a, cons
       if (a.rsum) {  // column-wise partial product of this slab (epilogue after the reduction)
         a.rsum[row] = s;
       } else {
-        const double xnew = __ddiv_rn(__dsub_rn(a.b[row], s), a.diag[row]);
+        const double xnew = __ddiv_rn(__dsub_rn(bi, s), dii);
         const int64_t gi = a.row0 + row;
-        const double dx = __dsub_rn(xnew, ld_x1<XL>(xo + gi));
+        const double dx = __dsub_rn(xnew, xoi);
         if constexpr (PUSH) {  // NEXT-1: push x_i^(k) into every rank's x^(k) buffer (NVLink stores)
           const PeerArgs* pe = a.peers;
           for (int p = 0; p < pe->P; ++p) ((k & 1) ? pe->x1[p] : pe->x0[p])[gi] = xnew;
