@@ -549,3 +549,17 @@ def test_null_stream_plan_sees_default_stream_writes(jb):
         assert np.array_equal(r.x, bh / d)  # P3: sweep 1 from x0 = 0 is b / diag bitwise
         del dA, db
         torch.cuda.empty_cache()
+
+
+def test_enomem_on_oversized_plan_then_healthy(jb):
+    """A plan whose A cannot fit in HBM (n = 200000 fp64: 320 GB) fails with JACOBI_ENOMEM at the
+    device allocation (before any copy from the host pointer), releases what it allocated, and the
+    device stays usable."""
+    import ctypes
+    h = ctypes.c_void_p()
+    dummy = np.zeros(8)
+    st = jb._lib.jacobi_plan_create(ctypes.byref(h), 200000, jb.F64, dummy.ctypes.data, 200000, 0, None)
+    assert st == jb.ENOMEM and "out of memory" in jb.last_error().lower() and not h.value
+    A, b, _ = dominant(512, 3, scale=1.05)
+    with jb.Plan(A) as p:
+        assert p.solve(b, None, 10, 0.0).iters == 10
