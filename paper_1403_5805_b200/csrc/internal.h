@@ -120,6 +120,10 @@ enum : int64_t { kGridMaxL2Rows = 64 * kL2Block };
 int gridsync_plan(int dtype, int nchunks, int num_sms, size_t* smem);
 cudaError_t launch_solve_gridsync(int dtype, const SweepArgs& a, unsigned long long* gbar, int64_t k0, int64_t k1,
                                   int grid, size_t smem, cudaStream_t s);
+// ... and over P ranks with the fused exchange (the launch holds nvr virtual ranks when emulated).
+int gridsync_push_plan(int dtype, int nchunks, int num_sms, size_t* smem);
+cudaError_t launch_solve_gridsync_push(int dtype, const SweepArgs* ranks_dev, int nvr, int64_t k0, int64_t k1,
+                                       int grid, size_t smem, cudaStream_t s);
 
 }  // namespace jacobi
 
@@ -145,6 +149,12 @@ struct jacobi_plan {
   unsigned long long* ex_dslot = nullptr;
   unsigned long long* ex_flags = nullptr;
   std::vector<void*> ipc_open;   // opened peer mappings (closed at destroy)
+  // persistent fused-exchange solver (k_solve_gridsync_push): one SweepArgs per (virtual) rank of
+  // the launch; emulation uses its own PeerArgs (total_ctas = the one grid's CTAs)
+  int push_G = 0;
+  size_t push_smem = 0;
+  jacobi::SweepArgs* push_ranks_dev = nullptr;
+  jacobi::PeerArgs* push_peers_dev = nullptr;
   int variant = 0;               // sweep kernel variant (R, U, threads); default per dtype, JACOBI_SWEEP_VARIANT overrides
   int batch = 32;                // sweeps per graph batch
   int l2_keep_pm = 0;            // per-mille of A rows kept L2-resident (evict_last) by the POL variants

@@ -69,10 +69,11 @@ static int plan_free(jacobi_plan* p) {
   if (p->comm) ncclCommDestroy(p->comm);
   void* dev[] = {p->dA_owned, p->diag, p->b, p->x[0], p->x[1], p->part, p->cnt, p->dslot, p->st,
                  p->hist_dev, p->flag_dev, p->zmin_dev, p->sq, p->blk, p->blk_all, p->rsum, p->rs_own,
-                 p->flags, p->ex_x, p->ex_dslot, p->ex_flags, p->peers_dev, p->gbar};
+                 p->flags, p->ex_x, p->ex_dslot, p->ex_flags, p->peers_dev, p->gbar, p->push_ranks_dev,
+                 p->push_peers_dev};
   const char* names[] = {"A", "diag", "b", "x0", "x1", "part", "cnt", "dslot", "state", "hist", "flag", "zmin",
                          "sq", "blk", "blk_all", "rsum", "rs_own", "flags", "ex_x", "ex_dslot", "ex_flags", "peers",
-                         "gbar"};
+                         "gbar", "push_ranks", "push_peers"};
   for (void* q : p->ipc_open) chk(cudaIpcCloseMemHandle(q), "cudaIpcCloseMemHandle");
   for (size_t i = 0; i < sizeof(dev) / sizeof(dev[0]); ++i)
     if (dev[i]) chk(cudaFree(dev[i]), names[i]);
@@ -425,6 +426,12 @@ static bool use_cluster(const jacobi_plan* p) {
          (!force_grid && p->n <= (p->dtype == JACOBI_F32 ? kClusterPreferMaxN_F32 : kClusterPreferMaxN_F64));
 }
 static bool use_grid(const jacobi_plan* p) { return grid_applies(p) && !use_cluster(p); }
+// Persistent fused-exchange solver: opt-in (JACOBI_PERSIST=1) on a fused-exchange plan.
+static bool use_grid_push(const jacobi_plan* p) {
+  const char* e = getenv("JACOBI_PERSIST");
+  return p->p2p && e && e[0] == '1' && p->norm == JACOBI_NORM_MAX && p->colblocks == 1 && !p->colwise;
+}
+
 
 extern "C" int jacobi_plan_info(const jacobi_plan* p, jacobi_plan_info_t* info) {
   if (!p || !info) return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_info: NULL argument");
@@ -446,7 +453,7 @@ extern "C" int jacobi_plan_info(const jacobi_plan* p, jacobi_plan_info_t* info) 
   info->variant = p->variant;
   info->num_variants = jacobi::num_variants();
   info->cluster_ctas = use_cluster(p) ? p->cluster_C : 0;
-  info->persistent_ctas = use_grid(p) ? p->grid_G : 0;
+  info->persistent_ctas = use_grid(p) ? p->grid_G : (use_grid_push(p) ? p->num_sms : 0);
   return 0;
 }
 
@@ -740,6 +747,72 @@ static int solve_grid(jacobi_plan* p, int64_t max_iter, jacobi::State* fin, doub
   }
 }
 
+// Persistent fused-exchange solver (opt-in with JACOBI_PERSIST=1 on a fused-exchange plan; validated
+// with emulated ranks on one GPU): builds the per-rank launch arguments once, then runs the solve in
+// cooperative launches of at most kMaxSweepsPerLaunch sweeps, like solve_grid.
+
+static int grid_push_setup(jacobi_plan* p) {
+  if (p->push_ranks_dev) return 0;
+  const int nch = (int)((p->n + p->chunk - 1) / p->chunk);
+  p->push_G = jacobi::gridsync_push_plan(p->dtype, nch, p->num_sms, &p->push_smem);
+  cudaGetLastError();
+  if (!p->push_G) return jacobi_set_error(JACOBI_EINVAL, "persistent fused exchange: configuration not supported");
+  const int nvr = p->p2p_emul ? p->p2p : 1;
+  std::vector<jacobi::SweepArgs> ra(nvr);
+  std::vector<jacobi::PeerArgs> pa;
+  if (p->p2p_emul) {  // the emulated ranks' PeerArgs, with the one grid's CTAs as the arrival count
+    pa.resize(nvr);
+    JCUDA(cudaMemcpy(pa.data(), p->peers_dev, sizeof(jacobi::PeerArgs) * nvr, cudaMemcpyDeviceToHost));
+    for (auto& q : pa) q.total_ctas = (unsigned long long)p->push_G;
+    JCUDA(cudaMalloc(&p->push_peers_dev, sizeof(jacobi::PeerArgs) * nvr));
+    JCUDA(cudaMemcpy(p->push_peers_dev, pa.data(), sizeof(jacobi::PeerArgs) * nvr, cudaMemcpyHostToDevice));
+  } else {
+    jacobi::PeerArgs q;  // real ranks: every rank launches push_G CTAs
+    JCUDA(cudaMemcpy(&q, p->peers_dev, sizeof(q), cudaMemcpyDeviceToHost));
+    q.total_ctas = (unsigned long long)p->nranks * p->push_G;
+    JCUDA(cudaMalloc(&p->push_peers_dev, sizeof(q)));
+    JCUDA(cudaMemcpy(p->push_peers_dev, &q, sizeof(q), cudaMemcpyHostToDevice));
+  }
+  for (int r = 0; r < nvr; ++r) {
+    jacobi::SweepArgs a = sweep_args(p, p->p2p_emul ? r : 0);
+    a.peers = p->push_peers_dev + r;
+    if (p->p2p_emul && r > 0) {
+      a.x0buf = p->ex_x + (size_t)(r - 1) * 2 * p->x_len;
+      a.x1buf = a.x0buf + p->x_len;
+      a.dslot = p->ex_dslot + (size_t)(r - 1) * 4;
+    }
+    ra[r] = a;
+  }
+  JCUDA(cudaMalloc(&p->push_ranks_dev, sizeof(jacobi::SweepArgs) * nvr));
+  JCUDA(cudaMemcpy(p->push_ranks_dev, ra.data(), sizeof(jacobi::SweepArgs) * nvr, cudaMemcpyHostToDevice));
+  return 0;
+}
+
+static int solve_grid_push(jacobi_plan* p, int64_t max_iter, jacobi::State* fin, double* dev_out) {
+  Range nvtx_range("jacobi: sweeps (persistent fused exchange)");
+  JRC(grid_push_setup(p));
+  p->sweeps_launched = 0;
+  const int nvr = p->p2p_emul ? p->p2p : 1;
+  for (int64_t k0 = 1;;) {
+    const int64_t k1 = std::min<int64_t>(k0 + jacobi::kMaxSweepsPerLaunch - 1, max_iter);
+    JCUDA(jacobi::launch_solve_gridsync_push(p->dtype, p->push_ranks_dev, nvr, k0, k1, p->push_G, p->push_smem,
+                                             p->stream));
+    if (dev_out) JCUDA(jacobi::launch_finalize(p->st, p->x[0], p->x[1], dev_out, p->n, p->stream));
+    JCUDA(cudaMemcpyAsync(&p->st_host[0], p->st, sizeof(jacobi::State), cudaMemcpyDeviceToHost, p->stream));
+    JCUDA(cudaStreamSynchronize(p->stream));
+    p->sweeps_launched += 1;
+    if (p->st_host[0].fault)
+      return jacobi_set_error(JACOBI_ECUDA, "fused exchange: a peer's sweep signal did not arrive within the wait bound");
+    if (p->st_host[0].nonfinite) return nonfinite_error();
+    if (p->st_host[0].done) {
+      *fin = p->st_host[0];
+      return 0;
+    }
+    if (k1 >= max_iter) return jacobi_set_error(JACOBI_ECUDA, "internal: persistent solve ended without a stop decision");
+    k0 = k1 + 1;
+  }
+}
+
 static int solve_impl(jacobi_plan* p, const double* b, const double* x0, bool dev, int64_t max_iter, double tol,
                       double* x_out, int64_t* iters_out, double* hist) {
   Range nvtx_range("jacobi: solve");
@@ -777,6 +850,10 @@ static int solve_impl(jacobi_plan* p, const double* b, const double* x0, bool de
     finalized = dev;
   } else if (use_grid(p)) {
     rc = solve_grid(p, max_iter, &fin, dev ? x_out : nullptr);
+    if (rc) return rc;
+    finalized = dev;
+  } else if (use_grid_push(p)) {
+    rc = solve_grid_push(p, max_iter, &fin, dev ? x_out : nullptr);
     if (rc) return rc;
     finalized = dev;
   } else {

@@ -393,14 +393,15 @@ __device__ __forceinline__ unsigned long long cta_max_bits(unsigned long long wm
 // slots and mbarrier parities of the partial-sum ring.  Returns this warp's max|dx| bits.
 template <typename T, int R, int NW, int U, int XL, bool PUSH, bool POL>
 __device__ __forceinline__ unsigned long long cta_sweep(const SweepArgs& a, const int64_t k, const int64_t tbase,
-                                                        double* s_part, uint64_t* s_full, uint64_t* s_empty) {
+                                                        double* s_part, uint64_t* s_full, uint64_t* s_empty,
+                                                        const int cta, const int ncta) {
   const double* __restrict__ xo = (k & 1) ? a.x0buf : a.x1buf;  // x^(k-1)
   double* __restrict__ xn = (k & 1) ? a.x1buf : a.x0buf;        // x^(k)
   const T* __restrict__ A = static_cast<const T*>(a.A);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int nch = a.nchunks;
-  const int64_t rb = (int64_t)blockIdx.x * a.m / gridDim.x;
-  const int64_t re = (int64_t)(blockIdx.x + 1) * a.m / gridDim.x;
+  const int64_t rb = (int64_t)cta * a.m / ncta;  // this CTA's rows of the launch (rank)
+  const int64_t re = (int64_t)(cta + 1) * a.m / ncta;
   const int ntile = (int)((re - rb + R - 1) / R);
   unsigned long long dmax = 0ull;
 
@@ -510,7 +511,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
 
   const int64_t k = a.st->kbase + j + 1;
   __shared__ unsigned long long s_wmax[NW];
-  const unsigned long long dmax = cta_sweep<T, R, NW, U, XL, PUSH, POL>(a, k, 0, s_part, s_full, s_empty);
+  const unsigned long long dmax =
+      cta_sweep<T, R, NW, U, XL, PUSH, POL>(a, k, 0, s_part, s_full, s_empty, blockIdx.x, gridDim.x);
   if constexpr (!PUSH) {
     if ((threadIdx.x & 31) == 0 && dmax) atomicMax(&a.dslot[k & 3], dmax);  // local L2: one per warp is fine
   } else {
@@ -633,12 +635,100 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync(const SweepArgs a
     SweepArgs ak = a;
     ak.sq = a.sq + (k & 1) * a.m;  // double-buffered dx^2 (Euclidean rule)
     const unsigned long long dmax =
-        cta_sweep<T, R, NW, 1, 2, false, POL>(ak, k, (k - k0) * ntile, s_part, s_full, s_empty);
+        cta_sweep<T, R, NW, 1, 2, false, POL>(ak, k, (k - k0) * ntile, s_part, s_full, s_empty, blockIdx.x, gridDim.x);
     if (lane == 0 && dmax) atomicMax(&a.dslot[k & 3], dmax);
     __syncthreads();  // every x_i^(k) store and max|dx| atomic of this CTA has been issued
     if (threadIdx.x == 0) {
       __threadfence();
       atomicAdd(gbar, 1ull);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// k_solve_gridsync_push: the persistent solver over P ranks with the fused exchange (NEXT-1 x
+// NEXT-3).  Each rank runs one cooperative launch of G CTAs for the sweeps k0..k1; each sweep is
+// cta_sweep with the NVLink push of x_i^(k) into every rank's buffer, then per CTA one remote
+// atomicMax of the max|dx| bits into every rank's slot and, after a system fence, one arrival on
+// every rank's counter for the sweep's parity.  Before sweep k >= 2 a CTA waits on its own rank's
+// counter (all CTAs of all ranks have pushed x^(k-1)) — also at k = k0, since other GPUs may still
+// be finishing the previous launch — and then every CTA of every rank takes the same stop decision
+// from its own copy of the distance slot.  x is read at L2 (peers write it during the launch).
+// Single-GPU emulation: one launch holds nvr virtual ranks (CTA groups) with their own x copies,
+// slots and counters (jacobi_plan_set_p2p_emulation) — the whole protocol in one co-resident grid.
+template <typename T, int R, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync_push(const SweepArgs* __restrict__ ranks, const int nvr,
+                                                                    const int64_t k0, const int64_t k1) {
+  extern __shared__ __align__(16) double s_part[];  // [kSlots][nchunks][R]
+  __shared__ __align__(8) uint64_t s_full[kSlots], s_empty[kSlots];
+  __shared__ unsigned long long s_wmax[NW];
+  __shared__ int s_go;
+  // this CTA's virtual rank and its CTA range within it (balanced split of the grid)
+  int vr = 0;
+  while (vr + 1 < nvr && (int64_t)(vr + 1) * gridDim.x / nvr <= (int64_t)blockIdx.x) ++vr;
+  const int c0 = (int)((int64_t)vr * gridDim.x / nvr), c1 = (int)((int64_t)(vr + 1) * gridDim.x / nvr);
+  const SweepArgs a = ranks[vr];
+  const PeerArgs* pe = a.peers;
+  State* st = a.st;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kSlots; ++q) {
+      mbar_init(&s_full[q], NW);
+      mbar_init(&s_empty[q], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (*(volatile int32_t*)&st->done || st->nonfinite || *(volatile int32_t*)&st->fault) return;  // uniform
+  const int64_t rb = (int64_t)(blockIdx.x - c0) * a.m / (c1 - c0);
+  const int64_t re = (int64_t)(blockIdx.x - c0 + 1) * a.m / (c1 - c0);
+  const int64_t ntile = (re - rb + R - 1) / R;
+  const bool leader = blockIdx.x == c0;  // writes this rank's state, history and slot clears
+  for (int64_t k = k0;; ++k) {
+    if (threadIdx.x == 0) {
+      int go = 1;
+      if (k >= 2) {  // every CTA of every rank has pushed x^(k-1) and its max|dx| bits here
+        const unsigned long long kp = (unsigned long long)(k - 1);
+        const unsigned long long target = ((kp + (kp & 1)) / 2) * pe->total_ctas;  // sweeps of this parity
+        const unsigned long long* f = pe->flags[pe->rank] + (kp & 1);
+        unsigned long long t0 = 0;
+        for (unsigned i = 0; ld_acquire_sys(f) < target; ++i) {
+          if ((i & 1023) == 1023) {
+            const unsigned long long t = global_ns();
+            if (t0 == 0) t0 = t;
+            else if (t - t0 > pe->wait_ns || *(volatile int32_t*)&st->fault) {
+              st->fault = 1;
+              go = 0;
+              break;
+            }
+          }
+        }
+      }
+      if (go && k >= 2) {  // stop test for sweep k-1, identical on every rank
+        const double d = ld_x1<2>(reinterpret_cast<const double*>(a.dslot + ((k - 1) & 3)));
+        if (leader && st->hist) st->hist[k - 2] = d;
+        if (d < st->tol) {
+          if (leader) { st->status = JACOBI_CONVERGED; st->iters = k - 1; st->done = 1; }
+          go = 0;
+        }
+      }
+      if (go && k > st->max_iter) {
+        if (leader) { st->status = JACOBI_MAX_ITER; st->iters = st->max_iter; st->done = 1; }
+        go = 0;
+      }
+      if (go && k > k1) go = 0;  // end of this launch's segment; the next launch resumes at k
+      if (go && leader) a.dslot[(k + 1) & 3] = 0ull;
+      s_go = go;
+    }
+    __syncthreads();
+    if (!s_go) break;
+    const unsigned long long dmax =
+        cta_sweep<T, R, NW, 1, 2, true, false>(a, k, (k - k0) * ntile, s_part, s_full, s_empty, blockIdx.x - c0, c1 - c0);
+    __threadfence_system();  // this thread's x pushes, before the arrivals below
+    const unsigned long long m = cta_max_bits<NW>(dmax, s_wmax);
+    if (threadIdx.x == 0) {
+      for (int p = 0; p < pe->P; ++p) atomicMax(pe->dslot[p] + (k & 3), m);
+      __threadfence_system();
+      for (int p = 0; p < pe->P; ++p) atomicAdd(pe->flags[p] + (k & 1), 1ull);
     }
   }
 }
@@ -1146,6 +1236,26 @@ cudaError_t launch_solve_gridsync(int dtype, const SweepArgs& a, unsigned long l
   void* args[] = {&aa, &gbar, &k0, &k1};
   const void* fn = dtype == JACOBI_F32 ? (const void*)k_solve_gridsync<float, 4, 16, true>
                                        : (const void*)k_solve_gridsync<double, 8, 16, true>;
+  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(512), args, smem, s);
+}
+
+int gridsync_push_plan(int dtype, int nchunks, int num_sms, size_t* smem) {
+  const int R = dtype == JACOBI_F32 ? 4 : 8;
+  *smem = (size_t)kSlots * nchunks * R * 8;
+  if (*smem > 200 * 1024) return 0;
+  auto fn = dtype == JACOBI_F32 ? k_solve_gridsync_push<float, 4, 16> : k_solve_gridsync_push<double, 8, 16>;
+  if (*smem > 48 * 1024 && cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem) != cudaSuccess)
+    return 0;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 512, *smem) != cudaSuccess || per_sm < 1) return 0;
+  return num_sms;
+}
+
+cudaError_t launch_solve_gridsync_push(int dtype, const SweepArgs* ranks_dev, int nvr, int64_t k0, int64_t k1,
+                                       int grid, size_t smem, cudaStream_t s) {
+  void* args[] = {&ranks_dev, &nvr, &k0, &k1};
+  const void* fn = dtype == JACOBI_F32 ? (const void*)k_solve_gridsync_push<float, 4, 16>
+                                       : (const void*)k_solve_gridsync_push<double, 8, 16>;
   return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(512), args, smem, s);
 }
 

@@ -190,3 +190,46 @@ def test_gridsync_euclidean_rule_bitwise(jb, monkeypatch, n, f32):
         assert same(r, q)
     st_o, x_o, it_o = oracle.jacobi(A, b, None, 5000, 1e-11, nthreads=16, norm="l2")
     assert (out["1"][1].status, out["1"][1].iters) == (st_o, it_o)
+
+
+def test_persistent_fused_exchange_emulated_ranks_bitwise(jb, monkeypatch):
+    """NEXT-1 x NEXT-3: the persistent solver over P ranks with the fused exchange (each rank's CTAs
+    push x_i^(k) into every rank's x copy, fold max|dx| into every rank's slot, bump every rank's
+    counter; the next sweep waits on its own counter), emulated as P CTA groups of one cooperative
+    launch, must equal the plain plan bit for bit — fixed runs, tol stops, runs over several launch
+    segments — and so must the real IPC path with one rank."""
+    import torch
+    monkeypatch.setenv("JACOBI_PERSIST", "1")
+    for n, scale in ((8192, 1.05), (4096, 1.02)):  # >= 16 column chunks (the fused-exchange plans need it)
+        A, b, _ = dominant(n, 211 + n, scale=scale)
+        x0 = np.random.default_rng(n).uniform(-1, 1, n)
+        monkeypatch.setenv("JACOBI_PERSIST", "0")
+        with jb.Plan(A) as p:
+            ref = p.solve(b, x0, 40, 0.0, history=True)
+            ref2 = p.solve(b, x0, 3000, 1e-11, history=True)
+            ref3 = p.solve(b, x0, 4200, 0.0)
+        monkeypatch.setenv("JACOBI_PERSIST", "1")
+        for P in (1, 2, 4, 8):
+            with jb.Plan(A) as p:
+                p.set_p2p_emulation(P)
+                assert p.info.persistent_ctas > 0
+                r = p.solve(b, x0, 40, 0.0, history=True)
+                assert r.iters == 40 and np.array_equal(r.x, ref.x) and np.array_equal(r.hist, ref.hist), (n, P)
+                r2 = p.solve(b, x0, 3000, 1e-11, history=True)
+                assert (r2.status, r2.iters) == (ref2.status, ref2.iters) and np.array_equal(r2.x, ref2.x), (n, P)
+                assert np.array_equal(r2.hist, ref2.hist)
+                if P in (1, 8):
+                    r3 = p.solve(b, x0, 4200, 0.0)  # two launch segments
+                    assert r3.iters == 4200 and np.array_equal(r3.x, ref3.x), (n, P)
+    A, b, _ = dominant(8192, 5, scale=1.05)
+    monkeypatch.setenv("JACOBI_PERSIST", "0")
+    with jb.Plan(A) as p0:
+        ref = p0.solve(b, None, 3000, 1e-11, history=True)
+    monkeypatch.setenv("JACOBI_PERSIST", "1")
+    dA = torch.from_numpy(A).cuda()
+    with jb.Plan(dA, n=8192, dist=(jb.nccl_unique_id(), 0, 1)) as p:
+        p.ipc_attach(p.ipc_export())
+        assert p.info.persistent_ctas > 0
+        r = p.solve(b, None, 3000, 1e-11, history=True)
+        assert (r.status, r.iters) == (ref.status, ref.iters) and np.array_equal(r.x, ref.x)
+        assert np.array_equal(r.hist, ref.hist)
