@@ -44,6 +44,17 @@ for n, f32, variants, modes in (((3001, False, [None], ["0"]),) if QUICK else CA
                 p.set_row_blocks(2)
                 p.solve(b, None, 5, 0.0)
         print(n, f32, v, mode, r.iters, r2.status, r2.iters, flush=True)
+# fused exchange with emulated ranks: graph path and persistent solver
+if not QUICK:
+    A, b = dominant(4096, 4096, False)
+    for mode in ("0", "1"):
+        os.environ["JACOBI_PERSIST"] = mode
+        os.environ.pop("JACOBI_SWEEP_VARIANT", None)
+        with jb.Plan(A) as p:
+            p.set_p2p_emulation(4)
+            r = p.solve(b, None, 8, 0.0)
+        print("p2p-emulation", mode, r.iters, flush=True)
+
 checked, mask = jb.bounds_violations()
 if checked:
     print(f"bounds check: violations mask = {mask:#x}", flush=True)
