@@ -233,3 +233,37 @@ def test_persistent_fused_exchange_emulated_ranks_bitwise(jb, monkeypatch):
         r = p.solve(b, None, 3000, 1e-11, history=True)
         assert (r.status, r.iters) == (ref.status, ref.iters) and np.array_equal(r.x, ref.x)
         assert np.array_equal(r.hist, ref.hist)
+
+
+def test_distinct_plans_on_distinct_threads(jb, monkeypatch):
+    """include/jacobi.h threading rule: distinct plans may run concurrently on distinct host threads
+    (each on its own stream).  Two plans on different paths (cluster, persistent, graph) solved from
+    three threads at once give the same bits as solved alone."""
+    import threading
+    monkeypatch.delenv("JACOBI_PERSIST", raising=False)
+    systems = [dominant(n, 500 + n, scale=1.05) for n in (256, 2048, 8192)]
+    alone = []
+    for A, b, _ in systems:
+        with jb.Plan(A) as p:
+            alone.append(p.solve(b, None, 60, 0.0).x)
+    plans = [jb.Plan(A) for A, _, _ in systems]
+    out = [None] * len(systems)
+    errs = []
+
+    def run(i):
+        try:
+            for _ in range(3):
+                out[i] = plans[i].solve(systems[i][1], None, 60, 0.0).x
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(len(systems))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for p in plans:
+        p.close()
+    assert not errs, errs
+    for i in range(len(systems)):
+        assert np.array_equal(out[i], alone[i]), i
