@@ -1126,7 +1126,7 @@ const Variant kVariants[] = {
     {"k_sweep_panel R4 U1 x-smem", 4, 512, 4, 4, 1, 1, k_sweep_panel<double, 4, 16, 1, 0, false, 8>, k_sweep_panel<float, 4, 16, 1, 0, false, 8>},
     {"k_sweep_panel R4 U1 x-smem L2-keep", 4, 512, 4, 4, 1, 1, k_sweep_panel<double, 4, 16, 1, 0, true, 8>, k_sweep_panel<float, 4, 16, 1, 0, true, 8>},
     // CTA kernel R = 8 (fp64; the fp32 instances keep R = 4, R = 8 spills): L2-keep and fused exchange
-    {"k_sweep_cta R8 U1 L2-keep", 8, 512, 1, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, false, true>, k_sweep_cta<float, 4, 16, 1, 0, false, true>},
+    {"k_sweep_cta R8 U1 L2-policy", 8, 512, 1, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, false, true>, k_sweep_cta<float, 4, 16, 1, 0, false, true>},
     {"k_sweep_cta R8 U1 fused-exchange", 8, 512, 2, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, true>, k_sweep_cta<float, 4, 16, 1, 0, true>},
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
@@ -1174,6 +1174,8 @@ int variant_rows_dt(int v, int dtype) { return dtype == JACOBI_F32 ? kVariants[v
 //   profiles/shard_rates_r01.jsonl; the panel kernel ties R=4 at c4, U=2 instances sit at the
 //   128-register cap and measured lower); with an L2-resident share of A (l2_keep_pm > 0, A within
 //   4x the L2) its POL instance (c2: 4976 -> 6051 effective GB/s with R=4 at 55 % kept, R=8 +2.5 %);
+//   the POL instance is the default for every fp64 size: with nothing kept it loads A with
+//   L2::evict_first, +0.3 % over plain loads (c4 7416 vs 7396, c3 7199 vs 7179 sustained, 3 runs);
 // - fp32 A, >= 16 chunks: the row-panel kernel R=4 with x^(k-1) staged in shared memory (c5: 7103 /
 //   6878; with L1-served x 6973 / 6783; the CTA kernel 6983 / 6415, which re-reads x from L2 once per
 //   tile: +50 % of the A bytes with fp32 A).  For fp64 A the shared-memory ring measured 1-2.5 %
@@ -1181,7 +1183,8 @@ int variant_rows_dt(int v, int dtype) { return dtype == JACOBI_F32 ? kVariants[v
 // - fewer chunks: the item kernel R=8,U=1 (fp64) or R=4,U=1 (fp32).
 int default_variant(int dtype, int nchunks, int chunk, bool l2_keep) {
   if (dtype == JACOBI_F32 && nchunks >= 16) return variant_fits(18, nchunks, dtype, chunk) ? 18 : 12;
-  const int big = l2_keep ? 20 : 6;
+  (void)l2_keep;  // the POL instance streams A with evict_first when no share is kept (l2_keep_pm = 0)
+  const int big = 20;
   if (variant_fits(big, nchunks, dtype, chunk)) return big;
   return dtype == JACOBI_F32 ? 0 : 1;  // U = 1: fits every chunk
 }
