@@ -722,7 +722,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync_push(const SweepA
     __syncthreads();
     if (!s_go) break;
     const unsigned long long dmax =
-        cta_sweep<T, R, NW, 1, 2, true, false>(a, k, (k - k0) * ntile, s_part, s_full, s_empty, blockIdx.x - c0, c1 - c0);
+        cta_sweep<T, R, NW, 1, 2, true, true>(a, k, (k - k0) * ntile, s_part, s_full, s_empty, blockIdx.x - c0, c1 - c0);
     __threadfence_system();  // this thread's x pushes, before the arrivals below
     const unsigned long long m = cta_max_bits<NW>(dmax, s_wmax);
     if (threadIdx.x == 0) {
@@ -1127,7 +1127,7 @@ const Variant kVariants[] = {
     {"k_sweep_panel R4 U1 x-smem L2-keep", 4, 512, 4, 4, 1, 1, k_sweep_panel<double, 4, 16, 1, 0, true, 8>, k_sweep_panel<float, 4, 16, 1, 0, true, 8>},
     // CTA kernel R = 8 (fp64; the fp32 instances keep R = 4, R = 8 spills): L2-keep and fused exchange
     {"k_sweep_cta R8 U1 L2-policy", 8, 512, 1, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, false, true>, k_sweep_cta<float, 4, 16, 1, 0, false, true>},
-    {"k_sweep_cta R8 U1 fused-exchange", 8, 512, 2, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, true>, k_sweep_cta<float, 4, 16, 1, 0, true>},
+    {"k_sweep_cta R8 U1 fused-exchange", 8, 512, 2, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, true, true>, k_sweep_cta<float, 4, 16, 1, 0, true>},
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
