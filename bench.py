@@ -297,9 +297,30 @@ def main():
     def step():
         return plan.solve_device(db, dx0, dxo, sweeps, tol)
 
+    def planted_error():
+        """max |x - x*| after the warm-up solves (BASELINE.json: b = A x*, so the fixed-iteration
+        configs end at x* to ~1e-16), max over ranks: a cheap end-to-end check of the exchange."""
+        xs = torch.empty(n, dtype=torch.float64, device="cuda")
+        g.device_xstar(cfg, xs.data_ptr(), sh)
+        e = (dxo - xs).abs().max().reshape(1)
+        if world > 1:
+            dist.all_reduce(e, op=dist.ReduceOp.MAX)
+        return float(e.item())
+
     for _ in range(max(3, args.warmup)):
         r = step()
     assert r.iters == sweeps and r.status == jb.MAX_ITER
+    if world > 1 and args.exchange == "p2p" and tol == 0.0 and not planted_error() <= 1e-10:
+        # safety net for the fused exchange (validated with emulated ranks only): fall back to NCCL
+        print("bench: fused exchange failed the planted-solution check; using the NCCL exchange", file=sys.stderr)
+        plan.close()
+        from paper_1403_5805_b200.dist import dist_plan
+        args.exchange = "nccl"
+        plan = dist_plan(dA, n, stream=sh)
+        plan.set_batch(K)
+        for _ in range(max(3, args.warmup)):
+            r = step()
+    planted = planted_error() if tol == 0.0 else None  # reported: the solve reached x*
     info = plan.info
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
@@ -426,6 +447,8 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "other_configs": configs,
+            "check": {"planted_max_abs_err": planted,
+                      "what": "max_i |x_i - x*_i| after the warm-up solves (b = A x*), max over ranks"},
         }
         s = json.dumps(line)
         print(s, flush=True)
