@@ -109,6 +109,8 @@ __device__ __forceinline__ void ld_x4(const double* p, double* v) {
         : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
   else if (XL == 2)
     asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
+  else if (XL == 3)  // weak, L1-cacheable: coherent after the launch's acquire + barrier (memory model)
+    asm("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p) : "memory");
   else
     asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
 }
@@ -537,6 +539,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
 // between sweeps a grid barrier (one release atomic per CTA on a global counter, an acquire spin by
 // one thread per CTA); after it every CTA evaluates the same stop test of PAPER.md:64-66 from the
 // same distance slot.  Waits are bounded (fault flag -> JACOBI_ECUDA instead of a hung GPU).
+#ifndef JACOBI_GRID_XL
+#define JACOBI_GRID_XL 3
+#endif
+constexpr int kGridXL = JACOBI_GRID_XL;  // x loads in the persistent solver (2: ld.cg, 3: weak ld)
 constexpr int kGridMaxL2Blocks = 64;  // Euclidean rule in the persistent solver: m <= 64 * kL2Block rows
 
 template <typename T, int R, int NW, bool POL>
@@ -635,7 +641,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync(const SweepArgs a
     SweepArgs ak = a;
     ak.sq = a.sq + (k & 1) * a.m;  // double-buffered dx^2 (Euclidean rule)
     const unsigned long long dmax =
-        cta_sweep<T, R, NW, 1, 2, false, POL>(ak, k, (k - k0) * ntile, s_part, s_full, s_empty, blockIdx.x, gridDim.x);
+        cta_sweep<T, R, NW, 1, kGridXL, false, POL>(ak, k, (k - k0) * ntile, s_part, s_full, s_empty, blockIdx.x, gridDim.x);
     if (lane == 0 && dmax) atomicMax(&a.dslot[k & 3], dmax);
     __syncthreads();  // every x_i^(k) store and max|dx| atomic of this CTA has been issued
     if (threadIdx.x == 0) {
