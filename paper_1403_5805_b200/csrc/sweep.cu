@@ -393,7 +393,10 @@ __device__ __forceinline__ unsigned long long cta_max_bits(unsigned long long wm
 // One sweep k over the CTA's rows (the body of k_sweep_cta, shared with the persistent grid solver).
 // Tiles are numbered from tbase (a running count across the sweeps of a persistent launch) for the
 // slots and mbarrier parities of the partial-sum ring.  Returns this warp's max|dx| bits.
-template <typename T, int R, int NW, int U, int XL, bool PUSH, bool POL>
+// GR > 1: a work unit is (chunk, group of R/GR rows of the tile) instead of (chunk, tile): with
+// nchunks not a multiple of the warp count, nchunks x GR units balance the warps (24 chunks: 1.5
+// chunks per warp per tile — warps 0-7 do two — become 3 units each).  Same per-row order.
+template <typename T, int R, int NW, int U, int XL, bool PUSH, bool POL, int GR = 1>
 __device__ __forceinline__ unsigned long long cta_sweep(const SweepArgs& a, const int64_t k, const int64_t tbase,
                                                         double* s_part, uint64_t* s_full, uint64_t* s_empty,
                                                         const int cta, const int ncta) {
@@ -460,26 +463,36 @@ __device__ __forceinline__ unsigned long long cta_sweep(const SweepArgs& a, cons
     const int64_t g0 = a.row0 + r0;
     uint64_t pol = 0;  // POL: the first l2_keep_pm/1000 of the CTA's rows stay in L2 (evict_last)
     if constexpr (POL) pol = l2_policy((r0 - rb) * 1000 < (re - rb) * (int64_t)a.l2_keep_pm);
-    for (int c = w; c < nch; c += NW) {
-      double acc[R];
+    constexpr int RG = R / GR;  // rows per unit
+    for (int u = w; u < nch * GR; u += NW) {
+      const int c = u / GR, rg = u % GR;
+      const int nvg = min(RG, nv - rg * RG);  // rows of this group that exist (last tile)
+      if (nvg <= 0) continue;
+      const T* rp[RG];
 #pragma unroll
-      for (int r = 0; r < R; ++r) acc[r] = 0.0;
+      for (int r = 0; r < RG; ++r)
+        rp[r] = GR == 1 ? rowp[r] : A + (r0 + min(rg * RG + r, nv - 1)) * a.lda - a.col0;
+      double acc[RG];
+#pragma unroll
+      for (int r = 0; r < RG; ++r) acc[r] = 0.0;
       const int64_t c0 = a.col0 + (int64_t)c * a.chunk;
       const int64_t c1 = min(c0 + (int64_t)a.chunk, a.cend);
-      // Full tiles take the constant-row-count instance: with a run-time row count nvcc wraps each
+      // Full units take the constant-row-count instance: with a run-time row count nvcc wraps each
       // row's load (and, for fp32, its converts) in a branch and keeps one A load in flight per warp
       // (c5 fell to 3.97 TB/s); with nv = R the loads are unconditional and software-pipelined.
-      check_tile<T, R>(a, rowp, c0, c1);
-      if (nv == R) accumulate_chunk<T, R, U, XL, POL>(rowp, R, xo, c0, c1, a.chunk, a.cend, g0, lane, acc, pol);
-      else accumulate_chunk<T, R, U, XL, POL>(rowp, nv, xo, c0, c1, a.chunk, a.cend, g0, lane, acc, pol);
+      check_tile<T, RG>(a, rp, c0, c1);
+      if (nvg == RG)
+        accumulate_chunk<T, RG, U, XL, POL>(rp, RG, xo, c0, c1, a.chunk, a.cend, g0 + rg * RG, lane, acc, pol);
+      else
+        accumulate_chunk<T, RG, U, XL, POL>(rp, nvg, xo, c0, c1, a.chunk, a.cend, g0 + rg * RG, lane, acc, pol);
 #pragma unroll
-      for (int r = 0; r < R; ++r)
+      for (int r = 0; r < RG; ++r)
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) acc[r] += __shfl_xor_sync(kFull, acc[r], off);
       if (lane == 0) {
-        double* dst = s_part + ((size_t)q * nch + c) * R;
+        double* dst = s_part + ((size_t)q * nch + c) * R + rg * RG;
 #pragma unroll
-        for (int r = 0; r < R; ++r) dst[r] = acc[r];
+        for (int r = 0; r < RG; ++r) dst[r] = acc[r];
       }
     }
     __syncwarp();
@@ -495,7 +508,7 @@ __device__ __forceinline__ unsigned long long cta_sweep(const SweepArgs& a, cons
   return dmax;
 }
 
-template <typename T, int R, int NW, int U = 1, int XL = 0, bool PUSH = false, bool POL = false>
+template <typename T, int R, int NW, int U = 1, int XL = 0, bool PUSH = false, bool POL = false, int GR = 1>
 __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, const int j) {
   extern __shared__ __align__(16) double s_part[];  // [kSlots][nchunks][R]
   __shared__ __align__(8) uint64_t s_full[kSlots], s_empty[kSlots];
@@ -514,7 +527,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
   const int64_t k = a.st->kbase + j + 1;
   __shared__ unsigned long long s_wmax[NW];
   const unsigned long long dmax =
-      cta_sweep<T, R, NW, U, XL, PUSH, POL>(a, k, 0, s_part, s_full, s_empty, blockIdx.x, gridDim.x);
+      cta_sweep<T, R, NW, U, XL, PUSH, POL, GR>(a, k, 0, s_part, s_full, s_empty, blockIdx.x, gridDim.x);
   if constexpr (!PUSH) {
     if ((threadIdx.x & 31) == 0 && dmax) atomicMax(&a.dslot[k & 3], dmax);  // local L2: one per warp is fine
   } else {
@@ -1134,6 +1147,9 @@ const Variant kVariants[] = {
     // CTA kernel R = 8 (fp64; the fp32 instances keep R = 4, R = 8 spills): L2-keep and fused exchange
     {"k_sweep_cta R8 U1 L2-policy", 8, 512, 1, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, false, true>, k_sweep_cta<float, 4, 16, 1, 0, false, true>},
     {"k_sweep_cta R8 U1 fused-exchange", 8, 512, 2, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, true, true>, k_sweep_cta<float, 4, 16, 1, 0, true>},
+    // CTA kernel R8 L2-policy with (chunk, row group) units: balanced when nchunks is not a multiple of 16
+    {"k_sweep_cta R8 U1 L2-policy rows/2", 8, 512, 1, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, false, true, 2>, k_sweep_cta<float, 4, 16, 1, 0, false, true, 2>},
+    {"k_sweep_cta R8 U1 L2-policy rows/4", 8, 512, 1, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, false, true, 4>, k_sweep_cta<float, 4, 16, 1, 0, false, true, 4>},
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
@@ -1190,7 +1206,9 @@ int variant_rows_dt(int v, int dtype) { return dtype == JACOBI_F32 ? kVariants[v
 int default_variant(int dtype, int nchunks, int chunk, bool l2_keep) {
   if (dtype == JACOBI_F32 && nchunks >= 16) return variant_fits(18, nchunks, dtype, chunk) ? 18 : 12;
   (void)l2_keep;  // the POL instance streams A with evict_first when no share is kept (l2_keep_pm = 0)
-  const int big = 20;
+  // 16 < nchunks < 32, not a multiple of 16: (chunk, half-tile) units balance the 16 warps (n = 12288 /
+  // 20000 / 24576: +3 / +4 / +2 %; from 40 chunks on, and for multiples of 16, whole-tile units win).
+  const int big = (dtype == JACOBI_F64 && nchunks > 16 && nchunks < 32 && nchunks % 16 != 0) ? 22 : 20;
   if (variant_fits(big, nchunks, dtype, chunk)) return big;
   return dtype == JACOBI_F32 ? 0 : 1;  // U = 1: fits every chunk
 }
