@@ -558,7 +558,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
 constexpr int kGridXL = JACOBI_GRID_XL;  // x loads in the persistent solver (2: ld.cg, 3: weak ld)
 constexpr int kGridMaxL2Blocks = 64;  // Euclidean rule in the persistent solver: m <= 64 * kL2Block rows
 
-template <typename T, int R, int NW, bool POL>
+template <typename T, int R, int NW, bool POL, int GR = 1>
 __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync(const SweepArgs a, unsigned long long* gbar,
                                                                const int64_t k0, const int64_t k1) {
   extern __shared__ __align__(16) double s_part[];  // [kSlots][nchunks][R]
@@ -654,7 +654,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync(const SweepArgs a
     SweepArgs ak = a;
     ak.sq = a.sq + (k & 1) * a.m;  // double-buffered dx^2 (Euclidean rule)
     const unsigned long long dmax =
-        cta_sweep<T, R, NW, 1, kGridXL, false, POL>(ak, k, (k - k0) * ntile, s_part, s_full, s_empty, blockIdx.x, gridDim.x);
+        cta_sweep<T, R, NW, 1, kGridXL, false, POL, GR>(ak, k, (k - k0) * ntile, s_part, s_full, s_empty, blockIdx.x,
+                                                       gridDim.x);
     if (lane == 0 && dmax) atomicMax(&a.dslot[k & 3], dmax);
     __syncthreads();  // every x_i^(k) store and max|dx| atomic of this CTA has been issued
     if (threadIdx.x == 0) {
@@ -1245,11 +1246,38 @@ cudaError_t launch_sweep(int dtype, int v, const SweepArgs& a, int j, int grid, 
 }
 
 // Persistent grid solver (k_solve_gridsync): one CTA per SM, co-resident (cooperative launch).
+// Instance with (chunk, row-group) units for A with few chunks: measured per sweep (fp64, 400-sweep
+// solves, GR = 1 / 2 / 4): n = 1024 (4 chunks) 4.83 / 4.27 / 4.25 µs; 1536 (6) 7.10 / 6.11 / 7.09;
+// 2048 (8) 7.38 / 6.64 / 7.38; 2560 (10) 10.23 / 10.93 / 11.72; 3072 (12) 10.91 / 11.75 / 11.87;
+// 3584 (14) 16.6 / 18.0 / 23.2 — half-tile units pay off up to 8 chunks only.
+static int gridsync_gr(int dtype, int nchunks) {
+  if (const char* e = getenv("JACOBI_GRID_GR")) {  // tuning override: 1, 2, 4 (, 8 fp64)
+    const int g = atoi(e);
+    if (g == 1 || g == 2 || g == 4 || (g == 8 && dtype != JACOBI_F32)) return g;
+  }
+  return nchunks <= 8 ? 2 : 1;
+}
+static const void* gridsync_fn(int dtype, int gr) {
+  if (dtype == JACOBI_F32) {
+    switch (gr) {
+      case 1: return (const void*)k_solve_gridsync<float, 4, 16, true, 1>;
+      case 2: return (const void*)k_solve_gridsync<float, 4, 16, true, 2>;
+      default: return (const void*)k_solve_gridsync<float, 4, 16, true, 4>;
+    }
+  }
+  switch (gr) {
+    case 1: return (const void*)k_solve_gridsync<double, 8, 16, true, 1>;
+    case 2: return (const void*)k_solve_gridsync<double, 8, 16, true, 2>;
+    case 4: return (const void*)k_solve_gridsync<double, 8, 16, true, 4>;
+    default: return (const void*)k_solve_gridsync<double, 8, 16, true, 8>;
+  }
+}
+
 int gridsync_plan(int dtype, int nchunks, int num_sms, size_t* smem) {
   const int R = dtype == JACOBI_F32 ? 4 : 8;
   *smem = (size_t)kSlots * nchunks * R * 8;
   if (*smem > 200 * 1024) return 0;
-  auto fn = dtype == JACOBI_F32 ? k_solve_gridsync<float, 4, 16, true> : k_solve_gridsync<double, 8, 16, true>;
+  const void* fn = gridsync_fn(dtype, gridsync_gr(dtype, nchunks));
   if (*smem > 48 * 1024 && cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem) != cudaSuccess)
     return 0;
   int per_sm = 0;
@@ -1261,9 +1289,8 @@ cudaError_t launch_solve_gridsync(int dtype, const SweepArgs& a, unsigned long l
                                   int grid, size_t smem, cudaStream_t s) {
   SweepArgs aa = a;
   void* args[] = {&aa, &gbar, &k0, &k1};
-  const void* fn = dtype == JACOBI_F32 ? (const void*)k_solve_gridsync<float, 4, 16, true>
-                                       : (const void*)k_solve_gridsync<double, 8, 16, true>;
-  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(512), args, smem, s);
+  return cudaLaunchCooperativeKernel(gridsync_fn(dtype, gridsync_gr(dtype, a.nchunks)), dim3(grid), dim3(512), args,
+                                     smem, s);
 }
 
 int gridsync_push_plan(int dtype, int nchunks, int num_sms, size_t* smem) {
