@@ -41,7 +41,9 @@ for n in sizes:
         us = 1e3 * best / sweeps
         print(json.dumps({"n": n, "f32": f32, "a_mb": n * n * (4 if f32 else 8) / 1e6, "us_per_sweep": us,
                           "it_per_s": 1e6 / us, "effective_gbs": inf.bytes_per_sweep / us / 1e3,
-                          "path": f"cluster x{inf.cluster_ctas}" if inf.cluster_ctas else jb.variant_name(inf.variant)}),
+                          "path": (f"cluster x{inf.cluster_ctas}" if inf.cluster_ctas else
+                                   f"persistent x{inf.persistent_ctas}" if inf.persistent_ctas else
+                                   f"graph: {jb.variant_name(inf.variant)}")}),
               flush=True)
     del dA
     torch.cuda.empty_cache()
