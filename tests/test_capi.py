@@ -105,3 +105,13 @@ def test_bounds_checked_build_exports_the_same_abi(jb):
     assert jb._lib.jacobi_debug_bounds_check(ctypes.byref(v), 0) == 0 and v.value == 0
     chk.jacobi_debug_bounds_check.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
     assert chk.jacobi_debug_bounds_check(ctypes.byref(v), 0) == 1
+
+
+def test_default_variant_indices_keep_their_names(jb):
+    """csrc/sweep.cu selects defaults by table index (default_variant, push_variant); the measurements
+    in DESIGN.md and profiles/ name variants by index too.  Appending variants must not shift them."""
+    expect = {1: "k_sweep R8 U1", 6: "k_sweep_cta R8 U1", 7: "k_sweep_cta R4 U1", 12: "k_sweep_panel R4 U1",
+              18: "k_sweep_panel R4 U1 x-smem", 20: "k_sweep_cta R8 U1 L2-policy",
+              21: "k_sweep_cta R8 U1 fused-exchange", 22: "k_sweep_cta R8 U1 L2-policy rows/2"}
+    for v, name in expect.items():
+        assert jb.variant_name(v) == name, (v, jb.variant_name(v))
