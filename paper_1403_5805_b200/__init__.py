@@ -204,6 +204,7 @@ class Plan:
             _check(create(ctypes.byref(h), ub, int(rank), int(nranks), self.n, self.dtype, ctypes.c_void_p(ptr), lda,
                           int(on_dev), s))
         self._h = h
+        self._rows = self.info.rows  # rows this plan owns (b's length); fixed for the plan's life
 
     def close(self):
         if getattr(self, "_h", None) and self._h.value:
@@ -255,8 +256,7 @@ class Plan:
 
     def solve(self, b, x0=None, max_iter=100, tol=0.0, history=False):
         """Host-pointer solve.  b: this plan's rows; x0/x: length n (numpy)."""
-        inf = self.info
-        b = _host_f64(b, inf.rows, "b")
+        b = _host_f64(b, self._rows, "b")
         x0 = np.zeros(self.n) if x0 is None else _host_f64(x0, self.n, "x0")
         x = np.empty(self.n)
         it = ctypes.c_int64(-1)
@@ -267,10 +267,9 @@ class Plan:
 
     def solve_device(self, b, x0, x_out, max_iter=100, tol=0.0, hist=None):
         """Device-pointer solve on torch CUDA tensors (results written into x_out / hist)."""
-        inf = self.info
         it = ctypes.c_int64(-1)
         st = _check(_lib.jacobi_plan_solve_device(
-            self._h, _dev_ptr(b, inf.rows, "b"), _dev_ptr(x0, self.n, "x0"), int(max_iter), float(tol),
+            self._h, _dev_ptr(b, self._rows, "b"), _dev_ptr(x0, self.n, "x0"), int(max_iter), float(tol),
             _dev_ptr(x_out, self.n, "x_out"), ctypes.byref(it),
             _dev_ptr(hist, hist.numel(), "hist") if hist is not None else None))
         return SolveResult(st, x_out, it.value, hist)
