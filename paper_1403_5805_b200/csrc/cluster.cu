@@ -93,6 +93,14 @@ struct ClusterArgs {
   double* x0buf;
   double* x1buf;
   State* st;
+  // Fused start (device solves in one launch): x0_src non-null -> the kernel itself initialises the
+  // stop state (max_iter, tol, hist below), scans b (= the caller's b) and x0 for NaN/Inf and loads
+  // x^(0) from x0_src; x_out non-null -> it also writes X^(iters) there when the solve has finished.
+  const double* x0_src;
+  double* x_out;
+  int64_t max_iter;
+  double tol;
+  double* hist;
 };
 
 template <typename T>
@@ -115,10 +123,26 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
   __shared__ __align__(8) uint64_t s_full[2];  // per parity: x^(k), the C maxima (and dx^2) have landed
 
   State* st = a.st;
-  if (*(volatile int32_t*)&st->done || st->nonfinite) return;  // uniform for the whole cluster
-  const double tol = st->tol;
-  const int64_t max_iter = st->max_iter;
-  double* hist = st->hist;
+  const bool fused = a.x0_src != nullptr;
+  if (fused) {
+    if (rank == 0 && tid == 0) {  // the whole stop state of a fresh solve (no host memset / k_prepare)
+      st->kbase = 0;
+      st->max_iter = a.max_iter;
+      st->tol = a.tol;
+      st->hist = a.hist;
+      st->done = 0;
+      st->status = 0;
+      st->iters = 0;
+      st->nonfinite = 0;
+      st->fault = 0;
+    }
+  } else if (*(volatile int32_t*)&st->done || st->nonfinite) {
+    return;  // uniform for the whole cluster
+  }
+  const double tol = fused ? a.tol : st->tol;
+  const int64_t max_iter = fused ? a.max_iter : st->max_iter;
+  double* hist = fused ? a.hist : st->hist;
+  __shared__ int s_bad;
   const int r_begin = (int)((int64_t)rank * n / C), r_end = (int)((int64_t)(rank + 1) * n / C);
   const int nr = r_end - r_begin;
 
@@ -129,8 +153,17 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
     As[idx] = c < n ? Ag[(int64_t)(r_begin + r) * a.lda + c] : T(0);
   }
   const int p0 = (int)((k0 - 1) & 1);
-  const double* xg = p0 ? a.x1buf : a.x0buf;
-  for (int i = tid; i < L.xlen; i += kCT) xs[p0 * L.xlen + i] = i < n ? xg[i] : 0.0;
+  const double* xg = fused ? a.x0_src : (p0 ? a.x1buf : a.x0buf);
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  bool bad = false;
+  for (int i = tid; i < L.xlen; i += kCT) {
+    const double v = i < n ? xg[i] : 0.0;
+    xs[p0 * L.xlen + i] = v;
+    if (fused && i >= r_begin && i < r_end)  // this CTA's slice of x0 and b (PAPER.md:59 inputs)
+      bad |= !isfinite(v) || !isfinite(a.b[i]);
+  }
+  if (bad) atomicOr(&s_bad, 1);
   for (int i = tid; i < 2 * L.n256; i += kCT) sq[i] = 0.0;
   if (tid == 0) {
     mbar_init_local(&s_full[0], 1);
@@ -138,6 +171,15 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   cl.sync();  // every CTA's barriers and buffers are ready before the first remote store
+  if (fused) {  // any non-finite input anywhere in the cluster: ENONFINITE, no sweep
+    int any = 0;
+    for (int q = 0; q < C; ++q) any |= *cl.map_shared_rank(&s_bad, q);
+    cl.sync();  // no CTA leaves while a peer may still read its flag
+    if (any) {
+      if (rank == 0 && tid == 0) st->nonfinite = 1;
+      return;
+    }
+  }
   // bytes that land in each CTA per sweep: all n values of x^(k), C maxima, and n dx^2 for L2
   const unsigned tx_bytes = (unsigned)(8 * n + 8 * C + (a.norm == JACOBI_NORM_L2 ? 8 * n : 0));
   unsigned phase[2] = {0u, 0u};
@@ -231,6 +273,8 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
   double* xgo = (klast & 1) ? a.x1buf : a.x0buf;
   const double* xsl = xs + (int)(klast & 1) * L.xlen;
   for (int r = tid; r < nr; r += kCT) xgo[r_begin + r] = xsl[r_begin + r];
+  if (stop && a.x_out)  // finished: X^(iters) straight to the caller's buffer (iters = klast)
+    for (int r = tid; r < nr; r += kCT) a.x_out[r_begin + r] = xsl[r_begin + r];
   if (rank == 0 && tid == 0) {
     if (stop == 1) { st->status = JACOBI_CONVERGED; st->iters = klast; st->done = 1; }
     if (stop == 2) { st->status = JACOBI_MAX_ITER; st->iters = max_iter; st->done = 1; }
@@ -289,8 +333,14 @@ int cluster_plan(int64_t n, int dtype, size_t* smem) {
 
 cudaError_t launch_solve_cluster(int dtype, int C, size_t smem, const void* A, int64_t lda, int64_t n, int chunk,
                                  int norm, const double* diag, const double* b, double* x0buf, double* x1buf,
-                                 State* st, int64_t k0, int64_t k1, cudaStream_t s) {
+                                 State* st, int64_t k0, int64_t k1, cudaStream_t s, const double* x0_src,
+                                 double* x_out, int64_t max_iter, double tol, double* hist) {
   ClusterArgs a;
+  a.x0_src = x0_src;
+  a.x_out = x_out;
+  a.max_iter = max_iter;
+  a.tol = tol;
+  a.hist = hist;
   a.A = A;
   a.lda = lda;
   a.n = (int)n;

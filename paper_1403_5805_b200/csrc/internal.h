@@ -107,7 +107,9 @@ cudaError_t launch_colsum_epilogue(const double* rsum, int nb, int64_t stride, i
 int cluster_plan(int64_t n, int dtype, size_t* smem);
 cudaError_t launch_solve_cluster(int dtype, int C, size_t smem, const void* A, int64_t lda, int64_t n, int chunk,
                                  int norm, const double* diag, const double* b, double* x0buf, double* x1buf,
-                                 State* st, int64_t k0, int64_t k1, cudaStream_t s);
+                                 State* st, int64_t k0, int64_t k1, cudaStream_t s, const double* x0_src = nullptr,
+                                 double* x_out = nullptr, int64_t max_iter = 0, double tol = 0.0,
+                                 double* hist = nullptr);
 enum { kMaxSweepsPerLaunch = 4096 };
 enum { kL2Block = 256 };  // rows per L2 partial sum (P-invariant when it divides the rows per rank)
 cudaError_t launch_l2_partials(const double* sq, int64_t m, double* blk, const State* st, cudaStream_t s);

@@ -834,6 +834,22 @@ static int solve_impl(jacobi_plan* p, const double* b, const double* x0, bool de
       hist_dev = p->hist_dev;
     }
   }
+  if (dev && max_iter > 0 && max_iter <= jacobi::kMaxSweepsPerLaunch && use_cluster(p)) {
+    // Small-n device solve in ONE launch: the cluster kernel initialises the stop state, scans b and
+    // x0, reads them in place and writes x_out itself; one read-back of the state, one sync.
+    Range nvtx_fused("jacobi: sweeps (cluster solver, fused start)");
+    JCUDA(jacobi::launch_solve_cluster(p->dtype, p->cluster_C, p->cluster_smem, p->dA, p->lda, p->n, p->chunk,
+                                       p->norm, p->diag, b, p->x[0], p->x[1], p->st, 1, max_iter, p->stream, x0,
+                                       x_out, max_iter, tol, hist_dev));
+    JCUDA(cudaMemcpyAsync(&p->st_host[0], p->st, sizeof(jacobi::State), cudaMemcpyDeviceToHost, p->stream));
+    JCUDA(cudaStreamSynchronize(p->stream));
+    JLAST("solve");
+    p->sweeps_launched = 1;
+    if (p->st_host[0].nonfinite) return nonfinite_error();
+    if (!p->st_host[0].done) return jacobi_set_error(JACOBI_ECUDA, "internal: small-n solve ended without a stop decision");
+    *iters_out = p->st_host[0].iters;
+    return p->st_host[0].status;
+  }
   int rc = solve_prepare(p, b, x0, dev, max_iter, tol, hist_dev);
   if (rc < 0) return rc;
   jacobi::State fin{};
