@@ -18,6 +18,17 @@ f32 = sys.argv[1] == "f32"
 sizes = [int(v) for v in sys.argv[2].split(",")]
 sweeps = int(sys.argv[3]) if len(sys.argv) > 3 else 400
 stream = torch.cuda.Stream()
+if os.environ.get("SETASIDE_MB"):  # experiment: persisting-L2 set-aside (cudaLimitPersistingL2CacheSize)
+    import ctypes
+    torch.cuda.init()
+    rt = ctypes.CDLL("libcudart.so.12")
+    mx = ctypes.c_int(0)
+    rt.cudaDeviceGetAttribute(ctypes.byref(mx), 108, 0)  # cudaDevAttrMaxPersistingL2CacheSize
+    want = min(mx.value, int(float(os.environ["SETASIDE_MB"]) * 1e6))
+    err = rt.cudaDeviceSetLimit(0x06, ctypes.c_size_t(want))  # cudaLimitPersistingL2CacheSize
+    got = ctypes.c_size_t(0)
+    rt.cudaDeviceGetLimit(ctypes.byref(got), 0x06)
+    print(json.dumps({"setaside_max": mx.value, "want": want, "err": err, "got": got.value}), flush=True)
 for n in sizes:
     cfg = g.GenConfig(n, a_dtype=g.F32 if f32 else g.F64, diag_mode=g.DIAG_SCALE, diag_scale=1.2)
     dA = torch.empty((n, n), dtype=torch.float32 if f32 else torch.float64, device="cuda")
