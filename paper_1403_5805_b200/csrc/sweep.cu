@@ -205,7 +205,8 @@ __device__ __forceinline__ bool sweep_prologue(const SweepArgs& a, int j, bool l
 // one DFMA chain per row; j == i (the diagonal) and j >= n are skipped.  Rows r >= nv
 // are not loaded (their sums are unused).
 // XSM: x^(k-1) of this chunk comes from shared memory, xs[col - c0] (else from global, xo[col]).
-template <typename T, int R, int U, int XL = 0, bool POL = false, bool XSM = false>
+// PIN: see the step loop below.
+template <typename T, int R, int U, int XL = 0, bool POL = false, bool XSM = false, bool PIN = false>
 __device__ __forceinline__ void accumulate_chunk(const T* const (&rowp)[R], const int nv,
                                                  const double* __restrict__ xo, const int64_t c0,
                                                  const int64_t c1, const int chunk, const int64_t n,
@@ -216,7 +217,7 @@ __device__ __forceinline__ void accumulate_chunk(const T* const (&rowp)[R], cons
   const int nsteps = chunk / S;
   const bool masked = (c1 - c0 != chunk) || (g0 < c1 && g0 + R > c0);
   if (!masked) {
-    for (int s = 0; s < nsteps; s += U) {
+    auto step = [&](const int s) {
       T av[U][R][E];
       double xv[U][E];
 #pragma unroll
@@ -239,6 +240,16 @@ __device__ __forceinline__ void accumulate_chunk(const T* const (&rowp)[R], cons
         for (int r = 0; r < R; ++r)
 #pragma unroll
           for (int e = 0; e < E; ++e) acc[r] = __fma_rn((double)av[u][r][e], xv[u][e], acc[r]);
+    };
+    // PIN: one step per loop trip (no compiler unrolling).  In the persistent solver's register
+    // budget an unrolled pair of steps is interleaved so that the first FMA waits on the first loads
+    // with only ~4 of the 9 loads issued; one step per trip issues all 9 first (c2: -4 %).  The
+    // HBM-streaming kernels are faster unrolled (c3/c5 +1-2.6 %).
+    if constexpr (PIN) {
+#pragma unroll 1
+      for (int s = 0; s < nsteps; s += U) step(s);
+    } else {
+      for (int s = 0; s < nsteps; s += U) step(s);
     }
   } else {
     // Diagonal chunk or ragged tail: same order, j == i and j >= n terms skipped.
@@ -396,7 +407,7 @@ __device__ __forceinline__ unsigned long long cta_max_bits(unsigned long long wm
 // GR > 1: a work unit is (chunk, group of R/GR rows of the tile) instead of (chunk, tile): with
 // nchunks not a multiple of the warp count, nchunks x GR units balance the warps (24 chunks: 1.5
 // chunks per warp per tile — warps 0-7 do two — become 3 units each).  Same per-row order.
-template <typename T, int R, int NW, int U, int XL, bool PUSH, bool POL, int GR = 1>
+template <typename T, int R, int NW, int U, int XL, bool PUSH, bool POL, int GR = 1, bool PIN = false>
 __device__ __forceinline__ unsigned long long cta_sweep(const SweepArgs& a, const int64_t k, const int64_t tbase,
                                                         double* s_part, uint64_t* s_full, uint64_t* s_empty,
                                                         const int cta, const int ncta) {
@@ -482,9 +493,11 @@ __device__ __forceinline__ unsigned long long cta_sweep(const SweepArgs& a, cons
       // (c5 fell to 3.97 TB/s); with nv = R the loads are unconditional and software-pipelined.
       check_tile<T, RG>(a, rp, c0, c1);
       if (nvg == RG)
-        accumulate_chunk<T, RG, U, XL, POL>(rp, RG, xo, c0, c1, a.chunk, a.cend, g0 + rg * RG, lane, acc, pol);
+        accumulate_chunk<T, RG, U, XL, POL, false, PIN>(rp, RG, xo, c0, c1, a.chunk, a.cend, g0 + rg * RG, lane, acc,
+                                                        pol);
       else
-        accumulate_chunk<T, RG, U, XL, POL>(rp, nvg, xo, c0, c1, a.chunk, a.cend, g0 + rg * RG, lane, acc, pol);
+        accumulate_chunk<T, RG, U, XL, POL, false, PIN>(rp, nvg, xo, c0, c1, a.chunk, a.cend, g0 + rg * RG, lane, acc,
+                                                        pol);
 #pragma unroll
       for (int r = 0; r < RG; ++r)
 #pragma unroll
@@ -654,8 +667,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync(const SweepArgs a
     SweepArgs ak = a;
     ak.sq = a.sq + (k & 1) * a.m;  // double-buffered dx^2 (Euclidean rule)
     const unsigned long long dmax =
-        cta_sweep<T, R, NW, 1, kGridXL, false, POL, GR>(ak, k, (k - k0) * ntile, s_part, s_full, s_empty, blockIdx.x,
-                                                       gridDim.x);
+        cta_sweep<T, R, NW, 1, kGridXL, false, POL, GR, GR == 1>(ak, k, (k - k0) * ntile, s_part, s_full, s_empty,
+                                                                 blockIdx.x, gridDim.x);
     if (lane == 0 && dmax) atomicMax(&a.dslot[k & 3], dmax);
     __syncthreads();  // every x_i^(k) store and max|dx| atomic of this CTA has been issued
     if (threadIdx.x == 0) {
