@@ -18,6 +18,7 @@
 // runs stay interruptible; the next launch resumes from global x.
 #include "internal.h"
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 namespace cg = cooperative_groups;
 
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
   }
   // bytes that land in each CTA per sweep: all n values of x^(k), C maxima, and n dx^2 for L2
   const unsigned tx_bytes = (unsigned)(8 * n + 8 * C + (a.norm == JACOBI_NORM_L2 ? 8 * n : 0));
-  unsigned phase[2] = {0u, 0u};
+  unsigned phase = 0u;  // bit p: the parity of the next phase of s_full[p] (a register, not a local array)
 
   const int nsteps = a.chunk / (32 * E);
   int stop = 0;  // 1 converged, 2 iteration limit
@@ -213,6 +214,7 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
     for (int r = warp; r < nr; r += kCT / 32) {
       const int grow = r_begin + r;
       const T* arow = As + (size_t)r * L.lds;
+      const double bi = a.b[grow], dii = a.diag[grow];  // issued before the row's FMA chain
       double s = 0.0;
       for (int c = 0; c < a.nchunks; ++c) {
         const int c0 = c * a.chunk;
@@ -235,7 +237,7 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
         for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(kFull, acc, off);
         s = c == 0 ? acc : s + acc;
       }
-      const double xnew = __ddiv_rn(__dsub_rn(a.b[grow], s), a.diag[grow]);
+      const double xnew = __ddiv_rn(__dsub_rn(bi, s), dii);
       const double dx = __dsub_rn(xnew, xo[grow]);
       if (lane < C) {  // lane q pushes x_i^(k) (and dx^2) into CTA q
         const unsigned rbar = mapa(smem_addr(&s_full[par]), lane);
@@ -256,8 +258,8 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
       for (int w = 0; w < kCT / 32; ++w) m = s_wmax[w] > m ? s_wmax[w] : m;
       st_async_b64(mapa(smem_addr(dsl + par * kMaxC + rank), tid), m, mapa(smem_addr(&s_full[par]), tid));
     }
-    mbar_wait_cluster(&s_full[par], phase[par]);  // x^(k), the maxima and dx^2 of every row have landed
-    phase[par] ^= 1u;
+    mbar_wait_cluster(&s_full[par], (phase >> par) & 1u);  // x^(k), the maxima and dx^2 of every row have landed
+    phase ^= 1u << par;
 
     double d;
     if (a.norm == JACOBI_NORM_L2) {  // identical arithmetic to k_l2_partials + k_l2_final
@@ -343,7 +345,10 @@ cudaError_t try_cluster(int n, int C, size_t* smem_out, int* ok) {
 // Largest usable cluster (16, else 8) for an n x n system of this dtype; 0 when A does not fit.
 int cluster_plan(int64_t n, int dtype, size_t* smem) {
   if (n < 1 || n > 4096) return 0;
-  for (int C : {16, 8}) {
+  int only = 0;  // JACOBI_CLUSTER_C=16|8|4|2: tuning override (that size or nothing)
+  if (const char* e = getenv("JACOBI_CLUSTER_C")) only = atoi(e);
+  for (int C : {16, 8, 4, 2}) {
+    if (only ? C != only : C < 8) continue;
     int ok = 0;
     cudaError_t e = dtype == JACOBI_F32 ? try_cluster<float>((int)n, C, smem, &ok)
                                         : try_cluster<double>((int)n, C, smem, &ok);
