@@ -30,10 +30,12 @@ struct Range {
 // - the persistent grid solver removes the ~8 µs per-sweep floor of the graph of sweep kernels
 //   (fp64 n = 768-3584: 8.6-20.5 -> 5.2-17.3 µs; c2 4096: 21.8 -> 20.9; fp32 up to n = 8192 / 268 MB:
 //   52.0 -> 49.7) and ties or loses beyond (fp64 6144: 53.9 vs 52.9; 12288: 192.6 vs 186.0);
-// - the cluster solver (A in shared memory of 16 SMs) beats its ~5 µs floor only for small n
-//   (fp64 256: 2.35 µs, 448: 5.3 vs 5.1; fp32 256: 2.8 vs 4.7, 512: 8.3 vs 4.7).
+// - the cluster solver (A in shared memory of 16 SMs, vector smem loads) beats the persistent
+//   solver's ~4 µs floor for small n (cluster vs persistent, JACOBI_CLUSTER_MAXN sweep: fp64 256:
+//   1.72 vs 4.2, 448: 3.58 vs 3.94, 512: 4.11 vs 4.21, 576: 6.06 vs 4.18; fp32 256: 1.84 vs 3.93,
+//   384: 3.42 vs 4.04, 448: 3.93 vs 3.74).
 constexpr double kPersistMaxBytesF64 = 200e6, kPersistMaxBytesF32 = 300e6;
-constexpr int64_t kClusterPreferMaxN_F64 = 448, kClusterPreferMaxN_F32 = 320;
+constexpr int64_t kClusterPreferMaxN_F64 = 512, kClusterPreferMaxN_F32 = 384;
 
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 }  // namespace
@@ -422,8 +424,9 @@ static bool use_cluster(const jacobi_plan* p) {
   if (!(p->cluster_C && p->nblocks == 1 && p->colblocks == 1 && !p->comm && !p->p2p)) return false;
   const char* e = getenv("JACOBI_PERSIST");
   const bool force_grid = e && e[0] == '1';
-  return !grid_applies(p) ||
-         (!force_grid && p->n <= (p->dtype == JACOBI_F32 ? kClusterPreferMaxN_F32 : kClusterPreferMaxN_F64));
+  int64_t prefer = p->dtype == JACOBI_F32 ? kClusterPreferMaxN_F32 : kClusterPreferMaxN_F64;
+  if (const char* m = getenv("JACOBI_CLUSTER_MAXN")) prefer = atoll(m);  // tuning override
+  return !grid_applies(p) || (!force_grid && p->n <= prefer);
 }
 static bool use_grid(const jacobi_plan* p) { return grid_applies(p) && !use_cluster(p); }
 // Persistent fused-exchange solver: opt-in (JACOBI_PERSIST=1) on a fused-exchange plan.

@@ -131,8 +131,8 @@ def test_gridsync_device_borrowed(jb, monkeypatch):
     assert r.iters == q.iters == 60 and np.array_equal(xo.cpu().numpy(), q.x)
 
 
-@pytest.mark.parametrize("n,f32,path", [(256, False, "cluster"), (448, False, "cluster"), (600, False, "grid"),
-                                        (320, True, "cluster"), (600, True, "grid"), (3072, False, "grid"),
+@pytest.mark.parametrize("n,f32,path", [(256, False, "cluster"), (512, False, "cluster"), (600, False, "grid"),
+                                        (384, True, "cluster"), (448, True, "grid"), (600, True, "grid"), (3072, False, "grid"),
                                         (4096, False, "grid"), (8192, False, "graph")])
 def test_default_path_by_size(jb, n, f32, path, monkeypatch):
     """Default solver path by size (measured crossovers): the cluster solver for small n,
