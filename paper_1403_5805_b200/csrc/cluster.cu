@@ -18,6 +18,7 @@
 // runs stay interruptible; the next launch resumes from global x.
 #include "internal.h"
 #include <cooperative_groups.h>
+#include <cstdio>
 #include <cstdlib>
 
 namespace cg = cooperative_groups;
@@ -36,6 +37,18 @@ template <> struct EOf<float> { static constexpr int E = 8; };
 
 __host__ __device__ inline size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
 
+// Shared-memory order of a row of A and of x (bank-conflict-free 16-byte loads).  In the canonical
+// summation order lane l of step s owns columns s S + l E + e (S = 32 E, e < E); storing column
+// s S + l E + e at s S + (e / V) 32 V + l V + e % V, V = elements per 16-byte load (2 doubles,
+// 4 floats), makes each 16-byte ld.shared of the warp read 512 contiguous bytes (4 wavefronts; the
+// natural order, lanes 32 bytes apart, takes 8).  Only the placement changes, not the arithmetic.
+template <int E, int V>
+__host__ __device__ inline int perm(int j) {
+  constexpr int S = 32 * E;
+  const int s = j / S, w = j - s * S, l = w / E, e = w - l * E;
+  return s * S + (e / V) * (32 * V) + l * V + e % V;
+}
+
 struct Layout {  // dynamic shared memory of one CTA
   size_t a_off, xs_off, sq_off, dsl_off, red_off, blk_off, total;
   int lds, xlen, n256;
@@ -44,7 +57,8 @@ struct Layout {  // dynamic shared memory of one CTA
 __host__ __device__ inline Layout layout(int n, int C, int esz) {
   Layout L;
   const int rows_max = (n + C - 1) / C;
-  L.lds = (n + 7) / 8 * 8;
+  const int S = 32 * (esz == 8 ? 4 : 8);  // columns per warp step (whole step blocks: see perm)
+  L.lds = (n + S - 1) / S * S;
   L.xlen = L.lds;
   L.n256 = (n + kL2Block - 1) / kL2Block * kL2Block;
   L.a_off = 0;
@@ -85,22 +99,26 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, unsigned parity) 
       : "memory");
 }
 
-// 32-byte shared-memory loads of a lane's E consecutive elements (A: 4 doubles / 8 floats; x: E
-// doubles).  Scalar loads at the lane stride of E elements were 8-way bank conflicted (32 B apart):
-// 8 wavefronts per load, ~2000 smem cycles per sweep at n = 256.
-__device__ __forceinline__ void lds_vec(const double* p, double (&v)[4]) {
-  asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(v[0]), "=d"(v[1]) : "r"(smem_addr(p)) : "memory");
-  asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(v[2]), "=d"(v[3]) : "r"(smem_addr(p + 2)) : "memory");
+// A lane's E elements of one step block (see perm): 16-byte shared loads at lane stride 16 bytes.
+__device__ __forceinline__ void lds2(const double* p, double& v0, double& v1) {
+  asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(v0), "=d"(v1) : "r"(smem_addr(p)) : "memory");
 }
-__device__ __forceinline__ void lds_vec(const double* p, double (&v)[8]) {
-  lds_vec(p, *reinterpret_cast<double(*)[4]>(&v[0]));
-  lds_vec(p + 4, *reinterpret_cast<double(*)[4]>(&v[4]));
+__device__ __forceinline__ void lds_a(const double* blk, int lane, double (&v)[4]) {
+  lds2(blk + 2 * lane, v[0], v[1]);
+  lds2(blk + 64 + 2 * lane, v[2], v[3]);
 }
-__device__ __forceinline__ void lds_vec(const float* p, float (&v)[8]) {
-  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "r"(smem_addr(p)) : "memory");
-  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]) : "r"(smem_addr(p + 4)) : "memory");
+__device__ __forceinline__ void lds_a(const float* blk, int lane, float (&v)[8]) {
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v[4 * q]), "=f"(v[4 * q + 1]), "=f"(v[4 * q + 2]), "=f"(v[4 * q + 3])
+                 : "r"(smem_addr(blk + 128 * q + 4 * lane))
+                 : "memory");
+}
+template <int E>
+__device__ __forceinline__ void lds_x(const double* blk, int lane, double (&v)[E]) {
+#pragma unroll
+  for (int q = 0; q < E / 2; ++q) lds2(blk + 64 * q + 2 * lane, v[2 * q], v[2 * q + 1]);
 }
 
 struct ClusterArgs {
@@ -169,7 +187,7 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
   const T* Ag = static_cast<const T*>(a.A);
   for (int64_t idx = tid; idx < (int64_t)nr * L.lds; idx += kCT) {
     const int r = (int)(idx / L.lds), c = (int)(idx % L.lds);
-    As[idx] = c < n ? Ag[(int64_t)(r_begin + r) * a.lda + c] : T(0);
+    As[(int64_t)r * L.lds + perm<E, 16 / (int)sizeof(T)>(c)] = c < n ? Ag[(int64_t)(r_begin + r) * a.lda + c] : T(0);
   }
   const int p0 = (int)((k0 - 1) & 1);
   const double* xg = fused ? a.x0_src : (p0 ? a.x1buf : a.x0buf);
@@ -178,7 +196,7 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
   bool bad = false;
   for (int i = tid; i < L.xlen; i += kCT) {
     const double v = i < n ? xg[i] : 0.0;
-    xs[p0 * L.xlen + i] = v;
+    xs[p0 * L.xlen + perm<E, 2>(i)] = v;
     if (fused && i >= r_begin && i < r_end)  // this CTA's slice of x0 and b (PAPER.md:59 inputs)
       bad |= !isfinite(v) || !isfinite(a.b[i]);
   }
@@ -204,28 +222,47 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
   unsigned phase = 0u;  // bit p: the parity of the next phase of s_full[p] (a register, not a local array)
 
   const int nsteps = a.chunk / (32 * E);
+#ifdef JACOBI_CLUSTER_PROF  // probe build: per-phase clock64 sums of CTA 0 thread 0, printed at exit
+  long long pt[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, tprev = clock64();
+#define CPROF(i)                              \
+  do {                                        \
+    if (rank == 0 && tid == 0) {              \
+      const long long t_ = clock64();         \
+      pt[i] += t_ - tprev;                    \
+      tprev = t_;                             \
+    }                                         \
+  } while (0)
+#else
+#define CPROF(i) \
+  do {           \
+  } while (0)
+#endif
   int stop = 0;  // 1 converged, 2 iteration limit
   int64_t k = k0;
   for (; k <= k1; ++k) {
     const int par = (int)(k & 1);
     const double* xo = xs + (1 - par) * L.xlen;
     if (tid == 0) mbar_expect(&s_full[par], tx_bytes);
+    CPROF(8);
     unsigned long long dmax = 0ull;
     for (int r = warp; r < nr; r += kCT / 32) {
       const int grow = r_begin + r;
       const T* arow = As + (size_t)r * L.lds;
       const double bi = a.b[grow], dii = a.diag[grow];  // issued before the row's FMA chain
+      CPROF(9);
       double s = 0.0;
       for (int c = 0; c < a.nchunks; ++c) {
         const int c0 = c * a.chunk;
         double acc = 0.0;
         for (int step = 0; step < nsteps; ++step) {
           const int col = c0 + (step * 32 + lane) * E;
-          if (col < n) {  // rows are zero padded to lds (a multiple of 8 >= col + E): vector loads
+          if (col < n) {  // rows are zero padded to whole step blocks (lds): 16-byte loads, see perm
             T av[E];
             double xv[E];
-            lds_vec(arow + col, av);
-            lds_vec(xo + col, xv);
+            const int blk = col - lane * E;  // s S: this step's block
+            lds_a(arow + blk, lane, av);
+            lds_x(xo + blk, lane, xv);
+            CPROF(10);
 #pragma unroll
             for (int e = 0; e < E; ++e) {
               const int cc = col + e;
@@ -233,15 +270,19 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
             }
           }
         }
+        CPROF(0);
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(kFull, acc, off);
         s = c == 0 ? acc : s + acc;
+        CPROF(1);
       }
       const double xnew = __ddiv_rn(__dsub_rn(bi, s), dii);
-      const double dx = __dsub_rn(xnew, xo[grow]);
+      const int gp = perm<E, 2>(grow);  // x_i's place in the shared-memory order
+      const double dx = __dsub_rn(xnew, xo[gp]);
+      CPROF(2);
       if (lane < C) {  // lane q pushes x_i^(k) (and dx^2) into CTA q
         const unsigned rbar = mapa(smem_addr(&s_full[par]), lane);
-        st_async_b64(mapa(smem_addr(xs + par * L.xlen + grow), lane), (unsigned long long)__double_as_longlong(xnew),
+        st_async_b64(mapa(smem_addr(xs + par * L.xlen + gp), lane), (unsigned long long)__double_as_longlong(xnew),
                      rbar);
         if (a.norm == JACOBI_NORM_L2)
           st_async_b64(mapa(smem_addr(sq + par * L.n256 + grow), lane),
@@ -249,17 +290,21 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
       }
       const unsigned long long bits = (unsigned long long)__double_as_longlong(dx) & 0x7fffffffffffffffull;
       dmax = bits > dmax ? bits : dmax;
+      CPROF(3);
     }
     if (lane == 0) s_wmax[warp] = dmax;
     __syncthreads();
+    CPROF(4);
     if (tid < C) {
       unsigned long long m = 0ull;
 #pragma unroll
       for (int w = 0; w < kCT / 32; ++w) m = s_wmax[w] > m ? s_wmax[w] : m;
       st_async_b64(mapa(smem_addr(dsl + par * kMaxC + rank), tid), m, mapa(smem_addr(&s_full[par]), tid));
     }
+    CPROF(5);
     mbar_wait_cluster(&s_full[par], (phase >> par) & 1u);  // x^(k), the maxima and dx^2 of every row have landed
     phase ^= 1u << par;
+    CPROF(6);
 
     double d;
     if (a.norm == JACOBI_NORM_L2) {  // identical arithmetic to k_l2_partials + k_l2_final
@@ -290,15 +335,24 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
       d = __longlong_as_double((long long)m);
     }
     if (rank == 0 && tid == 0 && hist) hist[k - 1] = d;
+    CPROF(7);
     if (d < tol) { stop = 1; break; }        // return X
     if (k == max_iter) { stop = 2; break; }  // iteration limit
   }
+#ifdef JACOBI_CLUSTER_PROF
+  if (rank == 0 && tid == 0) {
+    const double ns = (double)(k - k0 + 1);
+    printf("{\"cluster_prof\": true, \"n\": %d, \"C\": %d, \"sweeps\": %.0f, \"cycles\": [%.1f, %.1f, %.1f, %.1f, %.1f, "
+           "%.1f, %.1f, %.1f], \"top\": [%.1f, %.1f, %.1f]}\n", n, C, ns, pt[0] / ns, pt[1] / ns, pt[2] / ns, pt[3] / ns,
+           pt[4] / ns, pt[5] / ns, pt[6] / ns, pt[7] / ns, pt[8] / ns, pt[9] / ns, pt[10] / ns);
+  }
+#endif
   const int64_t klast = stop ? k : k1;
   double* xgo = (klast & 1) ? a.x1buf : a.x0buf;
   const double* xsl = xs + (int)(klast & 1) * L.xlen;
-  for (int r = tid; r < nr; r += kCT) xgo[r_begin + r] = xsl[r_begin + r];
+  for (int r = tid; r < nr; r += kCT) xgo[r_begin + r] = xsl[perm<E, 2>(r_begin + r)];
   if (stop && a.x_out)  // finished: X^(iters) straight to the caller's buffer (iters = klast)
-    for (int r = tid; r < nr; r += kCT) a.x_out[r_begin + r] = xsl[r_begin + r];
+    for (int r = tid; r < nr; r += kCT) a.x_out[r_begin + r] = xsl[perm<E, 2>(r_begin + r)];
   if (rank == 0 && tid == 0) {
     if (stop == 1) { st->status = JACOBI_CONVERGED; st->iters = klast; st->done = 1; }
     if (stop == 2) { st->status = JACOBI_MAX_ITER; st->iters = max_iter; st->done = 1; }
