@@ -30,12 +30,12 @@ struct Range {
 // - the persistent grid solver removes the ~8 µs per-sweep floor of the graph of sweep kernels
 //   (fp64 n = 768-3584: 8.6-20.5 -> 5.2-17.3 µs; c2 4096: 21.8 -> 20.9; fp32 up to n = 8192 / 268 MB:
 //   52.0 -> 49.7) and ties or loses beyond (fp64 6144: 53.9 vs 52.9; 12288: 192.6 vs 186.0);
-// - the cluster solver (A in shared memory of 16 SMs, vector smem loads) beats the persistent
-//   solver's ~4 µs floor for small n (cluster vs persistent, JACOBI_CLUSTER_MAXN sweep: fp64 256:
-//   1.72 vs 4.2, 448: 3.58 vs 3.94, 512: 4.11 vs 4.21, 576: 6.06 vs 4.18; fp32 256: 1.84 vs 3.93,
-//   384: 3.42 vs 4.04, 448: 3.93 vs 3.74).
+// - the cluster solver (A in shared memory of 16 SMs, conflict-free vector smem loads) beats the
+//   persistent solver's ~4 µs floor for small n (cluster vs persistent, JACOBI_CLUSTER_MAXN sweep,
+//   profiles/cluster_r01.jsonl: fp64 256: 1.52 vs 4.2, 512: 3.23 vs 4.22, 576: 5.16 vs 4.11; fp32
+//   512: 3.14 vs 3.84, 576: 5.21 vs 3.95 — more than 32 rows per CTA puts 3 rows on a warp).
 constexpr double kPersistMaxBytesF64 = 200e6, kPersistMaxBytesF32 = 300e6;
-constexpr int64_t kClusterPreferMaxN_F64 = 512, kClusterPreferMaxN_F32 = 384;
+constexpr int64_t kClusterPreferMaxN_F64 = 512, kClusterPreferMaxN_F32 = 512;
 
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 }  // namespace

@@ -132,7 +132,7 @@ def test_gridsync_device_borrowed(jb, monkeypatch):
 
 
 @pytest.mark.parametrize("n,f32,path", [(256, False, "cluster"), (512, False, "cluster"), (600, False, "grid"),
-                                        (384, True, "cluster"), (448, True, "grid"), (600, True, "grid"), (3072, False, "grid"),
+                                        (512, True, "cluster"), (576, True, "grid"), (600, True, "grid"), (3072, False, "grid"),
                                         (4096, False, "grid"), (8192, False, "graph")])
 def test_default_path_by_size(jb, n, f32, path, monkeypatch):
     """Default solver path by size (measured crossovers): the cluster solver for small n,
