@@ -239,10 +239,18 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
 #endif
   int stop = 0;  // 1 converged, 2 iteration limit
   int64_t k = k0;
+  // Each barrier phase takes one arrival (with the expected bytes) from thread 0.  The phases of
+  // sweeps k0 and k0 + 1 are armed here, the phase of sweep k + 2 right after sweep k's wait on the
+  // same barrier — off the loop top, where the arrive waited ~350 cycles behind the thread's DSMEM
+  // stores.  No peer can start sweep k + 2 before this CTA has pushed x^(k+1), so the arming always
+  // precedes that phase's bytes.
+  if (tid == 0) {
+    mbar_expect(&s_full[k0 & 1], tx_bytes);
+    mbar_expect(&s_full[(k0 + 1) & 1], tx_bytes);
+  }
   for (; k <= k1; ++k) {
     const int par = (int)(k & 1);
     const double* xo = xs + (1 - par) * L.xlen;
-    if (tid == 0) mbar_expect(&s_full[par], tx_bytes);
     CPROF(8);
     unsigned long long dmax = 0ull;
     for (int r = warp; r < nr; r += kCT / 32) {
@@ -295,15 +303,20 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
     if (lane == 0) s_wmax[warp] = dmax;
     __syncthreads();
     CPROF(4);
-    if (tid < C) {
-      unsigned long long m = 0ull;
+    if (warp == 0) {  // CTA max of the 16 warp maxima (a 16-lane butterfly), lane q pushes it to CTA q
+      static_assert(kCT / 32 == 16 && kMaxC == 16, "16-lane butterflies");
+      unsigned long long m = s_wmax[lane & 15];
 #pragma unroll
-      for (int w = 0; w < kCT / 32; ++w) m = s_wmax[w] > m ? s_wmax[w] : m;
-      st_async_b64(mapa(smem_addr(dsl + par * kMaxC + rank), tid), m, mapa(smem_addr(&s_full[par]), tid));
+      for (int off = 8; off > 0; off >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(kFull, m, off);
+        m = o > m ? o : m;
+      }
+      if (lane < C) st_async_b64(mapa(smem_addr(dsl + par * kMaxC + rank), lane), m, mapa(smem_addr(&s_full[par]), lane));
     }
     CPROF(5);
     mbar_wait_cluster(&s_full[par], (phase >> par) & 1u);  // x^(k), the maxima and dx^2 of every row have landed
     phase ^= 1u << par;
+    if (tid == 0) mbar_expect(&s_full[par], tx_bytes);  // arm this barrier's next phase (sweep k + 2)
     CPROF(6);
 
     double d;
@@ -325,10 +338,10 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) t = __dadd_rn(t, __shfl_xor_sync(kFull, t, off));
       d = __dsqrt_rn(t);
-    } else {  // max of the C slots: one load per lane, then a shuffle max
-      unsigned long long m = lane < C ? dsl[par * kMaxC + lane] : 0ull;
+    } else {  // max of the C slots: one load per lane (both half-warps), then a 16-lane butterfly
+      unsigned long long m = (lane & 15) < C ? dsl[par * kMaxC + (lane & 15)] : 0ull;
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
+      for (int off = 8; off > 0; off >>= 1) {
         const unsigned long long o = __shfl_xor_sync(kFull, m, off);
         m = o > m ? o : m;
       }
