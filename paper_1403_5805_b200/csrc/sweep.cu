@@ -1270,7 +1270,23 @@ static int gridsync_gr(int dtype, int nchunks) {
   }
   return nchunks <= 8 ? 2 : 1;
 }
-static const void* gridsync_fn(int dtype, int gr) {
+// Rows per tile: 8 for fp64; for fp32 8 with few chunks (the half-tile units of 4 rows: 400-sweep
+// solves, R = 4 / 8: n = 1024 5.20 / 4.73 µs, 2048 7.96 / 6.61) and 4 beyond (the R = 8 one-chunk
+// units spill: 4096 14.4 / 17.1, 8192 47.5 / 59.9).  JACOBI_GRID_R = 4 | 8 overrides.
+static int gridsync_r(int dtype, int nchunks) {
+  if (dtype != JACOBI_F32) return 8;
+  if (const char* e = getenv("JACOBI_GRID_R")) return atoi(e) == 8 ? 8 : 4;
+  return gridsync_gr(dtype, nchunks) > 1 ? 8 : 4;
+}
+static const void* gridsync_fn(int dtype, int nchunks) {
+  const int gr = gridsync_gr(dtype, nchunks);
+  if (dtype == JACOBI_F32 && gridsync_r(dtype, nchunks) == 8) {
+    switch (gr) {
+      case 1: return (const void*)k_solve_gridsync<float, 8, 16, true, 1>;
+      case 2: return (const void*)k_solve_gridsync<float, 8, 16, true, 2>;
+      default: return (const void*)k_solve_gridsync<float, 8, 16, true, 4>;
+    }
+  }
   if (dtype == JACOBI_F32) {
     switch (gr) {
       case 1: return (const void*)k_solve_gridsync<float, 4, 16, true, 1>;
@@ -1287,10 +1303,10 @@ static const void* gridsync_fn(int dtype, int gr) {
 }
 
 int gridsync_plan(int dtype, int nchunks, int num_sms, size_t* smem) {
-  const int R = dtype == JACOBI_F32 ? 4 : 8;
+  const int R = gridsync_r(dtype, nchunks);
   *smem = (size_t)kSlots * nchunks * R * 8;
   if (*smem > 200 * 1024) return 0;
-  const void* fn = gridsync_fn(dtype, gridsync_gr(dtype, nchunks));
+  const void* fn = gridsync_fn(dtype, nchunks);
   if (*smem > 48 * 1024 && cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem) != cudaSuccess)
     return 0;
   int per_sm = 0;
@@ -1302,8 +1318,7 @@ cudaError_t launch_solve_gridsync(int dtype, const SweepArgs& a, unsigned long l
                                   int grid, size_t smem, cudaStream_t s) {
   SweepArgs aa = a;
   void* args[] = {&aa, &gbar, &k0, &k1};
-  return cudaLaunchCooperativeKernel(gridsync_fn(dtype, gridsync_gr(dtype, a.nchunks)), dim3(grid), dim3(512), args,
-                                     smem, s);
+  return cudaLaunchCooperativeKernel(gridsync_fn(dtype, a.nchunks), dim3(grid), dim3(512), args, smem, s);
 }
 
 int gridsync_push_plan(int dtype, int nchunks, int num_sms, size_t* smem) {
