@@ -159,6 +159,34 @@ __device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long
   return v;
 }
 
+// Probe build only (-DJACOBI_SM_TIMING): per CTA of the last sweep-kernel launch, its SM id and the
+// %globaltimer at its start and end (jacobi_debug_sm_times) — to see how the static row partition
+// finishes across SMs and dies.
+#ifdef JACOBI_SM_TIMING
+__device__ unsigned long long g_smt[3 * 4096];
+#define SMT_BEGIN()                              \
+  unsigned long long smt0_ = 0;                  \
+  if (threadIdx.x == 0) smt0_ = global_ns()
+#define SMT_END()                                                            \
+  do {                                                                       \
+    __syncthreads();                                                         \
+    if (threadIdx.x == 0 && blockIdx.x < 4096) {                             \
+      unsigned sm_;                                                          \
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_));                      \
+      g_smt[3 * blockIdx.x] = sm_;                                           \
+      g_smt[3 * blockIdx.x + 1] = smt0_;                                     \
+      g_smt[3 * blockIdx.x + 2] = global_ns();                               \
+    }                                                                        \
+  } while (0)
+#else
+#define SMT_BEGIN() \
+  do {              \
+  } while (0)
+#define SMT_END() \
+  do {            \
+  } while (0)
+#endif
+
 __device__ __forceinline__ bool sweep_prologue(const SweepArgs& a, int j, bool leader) {
   State* st = a.st;
   if (*(volatile int32_t*)&st->done || st->nonfinite || *(volatile int32_t*)&st->fault) return false;
@@ -523,6 +551,7 @@ __device__ __forceinline__ unsigned long long cta_sweep(const SweepArgs& a, cons
 
 template <typename T, int R, int NW, int U = 1, int XL = 0, bool PUSH = false, bool POL = false, int GR = 1>
 __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, const int j) {
+  SMT_BEGIN();
   extern __shared__ __align__(16) double s_part[];  // [kSlots][nchunks][R]
   __shared__ __align__(8) uint64_t s_full[kSlots], s_empty[kSlots];
   __shared__ int s_go;
@@ -556,6 +585,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
       for (int p = 0; p < pe->P; ++p) atomicAdd(pe->flags[p] + (k & 1), 1ull);
     }
   }
+  SMT_END();
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -864,6 +894,7 @@ __device__ __forceinline__ void panel_tile_nv(const int nv, const SweepArgs& a, 
 constexpr int kMaxXSN = 16;
 template <typename T, int R, int NW, int U = 1, int XL = 0, bool POL = false, int XSN = 0>
 __global__ void __launch_bounds__(NW * 32, 1) k_sweep_panel(const SweepArgs a, const int j) {
+  SMT_BEGIN();
   static_assert(XSN <= kMaxXSN, "x ring slots");
   extern __shared__ __align__(128) double s_xring[];  // [XSN][chunk] when XSN > 0
   __shared__ __align__(8) uint64_t s_xfull[XSN > 0 ? XSN : 1];
@@ -940,6 +971,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_panel(const SweepArgs a, c
     dmax = o > dmax ? o : dmax;
   }
   if (lane == 0 && dmax) atomicMax(&a.dslot[k & 3], dmax);
+  SMT_END();
 }
 
 
@@ -1229,6 +1261,12 @@ int default_variant(int dtype, int nchunks, int chunk, bool l2_keep) {
 bool variant_uses_l2_keep(int v) { return v == 16 || v == 17 || v == 19 || v == 20; }
 int variant_rows(int v) { return kVariants[v].R; }
 int variant_threads(int v) { return kVariants[v].threads; }
+
+#ifdef JACOBI_SM_TIMING
+extern "C" int jacobi_debug_sm_times(unsigned long long* out, int nctas) {
+  return cudaMemcpyFromSymbol(out, g_smt, sizeof(unsigned long long) * 3 * (size_t)nctas) == cudaSuccess ? 0 : -5;
+}
+#endif
 
 int chunk_for(int64_t n, int dtype) {
   // 8 KB of row data per chunk (1024 fp64 / 2048 fp32 columns) when n has >= 16 such chunks, halved
