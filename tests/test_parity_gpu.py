@@ -417,7 +417,8 @@ def test_dist_plan_single_rank_matches_plain_plan(jb):
 
 
 # ------------------------------------------------------------------ NEXT-3: small-n cluster-resident solver
-@pytest.mark.parametrize("n,f32", [(1, False), (2, False), (37, False), (256, False), (300, True), (600, False)])
+@pytest.mark.parametrize("n,f32", [(1, False), (2, False), (37, False), (129, False), (256, False), (300, True),
+                                   (511, True), (600, False), (640, False)])
 def test_small_n_cluster_path_bitwise(jb, n, f32, monkeypatch):
     """The one-launch cluster solver (A in shared memory, x through DSMEM) must reproduce the sweep
     kernels bit for bit: iterates, histories, stop iterations, both norms, and > 4096-sweep runs."""
