@@ -138,7 +138,20 @@ struct ClusterArgs {
   int64_t max_iter;
   double tol;
   double* hist;
+  HostDone* done;  // non-null (fused start): completion record in mapped host memory, tagged seq
+  unsigned long long seq;
 };
+
+// Rank 0's last act: the completion record, seq after a system fence (every CTA's x_out stores were
+// fenced at system scope before the cluster barrier that precedes this).
+__device__ __forceinline__ void publish_done(HostDone* d, unsigned long long seq, int status, int nonfinite,
+                                             int64_t iters) {
+  d->status = status;
+  d->nonfinite = nonfinite;
+  d->iters = iters;
+  __threadfence_system();
+  *(volatile unsigned long long*)&d->seq = seq;
+}
 
 template <typename T>
 __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, const int64_t k0, const int64_t k1) {
@@ -229,7 +242,10 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
     for (int q = 0; q < C; ++q) any |= *cl.map_shared_rank(&s_bad, q);
     cl.sync();  // no CTA leaves while a peer may still read its flag
     if (any) {
-      if (rank == 0 && tid == 0) st->nonfinite = 1;
+      if (rank == 0 && tid == 0) {
+        st->nonfinite = 1;
+        if (a.done) publish_done(a.done, a.seq, 0, 1, 0);
+      }
       return;
     }
   }
@@ -387,7 +403,10 @@ __global__ void __launch_bounds__(kCT, 1) k_solve_cluster(const ClusterArgs a, c
     if (stop == 2) { st->status = JACOBI_MAX_ITER; st->iters = max_iter; st->done = 1; }
     st->kbase = klast;
   }
+  if (a.done) __threadfence_system();  // this thread's x_out stores, before the barrier below
   cl.sync();  // no CTA leaves while a peer may still write into its shared memory
+  if (a.done && stop && rank == 0 && tid == 0)
+    publish_done(a.done, a.seq, stop == 1 ? JACOBI_CONVERGED : JACOBI_MAX_ITER, 0, stop == 1 ? klast : max_iter);
 }
 
 template <typename T>
@@ -444,8 +463,11 @@ int cluster_plan(int64_t n, int dtype, size_t* smem) {
 cudaError_t launch_solve_cluster(int dtype, int C, size_t smem, const void* A, int64_t lda, int64_t n, int chunk,
                                  int norm, const double* diag, const double* b, double* x0buf, double* x1buf,
                                  State* st, int64_t k0, int64_t k1, cudaStream_t s, const double* x0_src,
-                                 double* x_out, int64_t max_iter, double tol, double* hist) {
+                                 double* x_out, int64_t max_iter, double tol, double* hist, HostDone* done,
+                                 unsigned long long seq) {
   ClusterArgs a;
+  a.done = done;
+  a.seq = seq;
   a.x0_src = x0_src;
   a.x_out = x_out;
   a.max_iter = max_iter;

@@ -23,6 +23,16 @@ struct State {
   int32_t fault;      // fused exchange: a peer's signal did not arrive within kPeerWaitNs (JACOBI_ECUDA)
 };
 
+// Completion record of a one-launch small-n device solve, written by the kernel into mapped pinned
+// host memory (seq last, after a system fence): the host polls it instead of a state copy + stream
+// synchronisation.
+struct HostDone {
+  int32_t status;
+  int32_t nonfinite;
+  int64_t iters;
+  unsigned long long seq;
+};
+
 // NEXT-1 fused exchange: every rank's x buffers, distance slots and arrival counters (peer-mapped
 // pointers over NVLink, or copies on one GPU when P ranks are emulated).  Device-resident.
 enum { kMaxPeers = 8 };
@@ -109,7 +119,7 @@ cudaError_t launch_solve_cluster(int dtype, int C, size_t smem, const void* A, i
                                  int norm, const double* diag, const double* b, double* x0buf, double* x1buf,
                                  State* st, int64_t k0, int64_t k1, cudaStream_t s, const double* x0_src = nullptr,
                                  double* x_out = nullptr, int64_t max_iter = 0, double tol = 0.0,
-                                 double* hist = nullptr);
+                                 double* hist = nullptr, HostDone* done = nullptr, unsigned long long seq = 0);
 enum { kMaxSweepsPerLaunch = 4096 };
 enum { kL2Block = 256 };  // rows per L2 partial sum (P-invariant when it divides the rows per rank)
 cudaError_t launch_l2_partials(const double* sq, int64_t m, double* blk, const State* st, cudaStream_t s);
@@ -183,6 +193,9 @@ struct jacobi_plan {
   unsigned long long* dslot = nullptr;
   jacobi::State* st = nullptr;   // device
   jacobi::State* st_host = nullptr;   // pinned mirror
+  jacobi::HostDone* done_host = nullptr;  // mapped pinned completion record (one-launch small-n solves)
+  jacobi::HostDone* done_dev = nullptr;   // its device address
+  unsigned long long done_seq = 0;
   double* hist_dev = nullptr;    // device history buffer for host-pointer solves
   int64_t hist_cap = 0;
   int* flag_dev = nullptr;       // scratch: non-finite flag / zero-diag min index

@@ -6,6 +6,7 @@
 // pinned memory behind each batch); sweeps after the device's stop decision exit in their prologue.
 // No batch is issued beyond ceil(max_iter / K), so tol = 0 runs never wait on a poll.
 #include "internal.h"
+#include <atomic>
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX: ranges cost nothing unless a tracing tool is attached
 #include <algorithm>
 #include <cmath>
@@ -80,6 +81,7 @@ static int plan_free(jacobi_plan* p) {
   for (size_t i = 0; i < sizeof(dev) / sizeof(dev[0]); ++i)
     if (dev[i]) chk(cudaFree(dev[i]), names[i]);
   if (p->st_host) chk(cudaFreeHost(p->st_host), "cudaFreeHost(state)");
+  if (p->done_host) chk(cudaFreeHost(p->done_host), "cudaFreeHost(done)");
   if (p->own_stream && p->stream) chk(cudaStreamDestroy(p->stream), "cudaStreamDestroy");
   delete p;
   cudaGetLastError();
@@ -192,6 +194,9 @@ int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dty
   JCUDA(cudaMalloc(&p->flag_dev, 16));
   JCUDA(cudaMalloc(&p->zmin_dev, 8));
   JCUDA(cudaMallocHost(&p->st_host, kLookahead * sizeof(jacobi::State)));
+  JCUDA(cudaHostAlloc(&p->done_host, sizeof(jacobi::HostDone), cudaHostAllocMapped));
+  p->done_host->seq = 0;
+  JCUDA(cudaHostGetDevicePointer(&p->done_dev, p->done_host, 0));
   JCUDA(cudaMemsetAsync(p->x[0], 0, (size_t)p->x_len * 8, p->stream));
   JCUDA(cudaMemsetAsync(p->x[1], 0, (size_t)p->x_len * 8, p->stream));
   JCUDA(cudaMemsetAsync(p->cnt, 0, (size_t)a_rows * 4, p->stream));
@@ -841,13 +846,27 @@ static int solve_impl(jacobi_plan* p, const double* b, const double* x0, bool de
     // Small-n device solve in ONE launch: the cluster kernel initialises the stop state, scans b and
     // x0, reads them in place and writes x_out itself; one read-back of the state, one sync.
     Range nvtx_fused("jacobi: sweeps (cluster solver, fused start)");
+    const unsigned long long seq = ++p->done_seq;
     JCUDA(jacobi::launch_solve_cluster(p->dtype, p->cluster_C, p->cluster_smem, p->dA, p->lda, p->n, p->chunk,
                                        p->norm, p->diag, b, p->x[0], p->x[1], p->st, 1, max_iter, p->stream, x0,
-                                       x_out, max_iter, tol, hist_dev));
+                                       x_out, max_iter, tol, hist_dev, p->done_dev, seq));
+    p->sweeps_launched = 1;
+    // Poll the mapped completion record (written after x_out is globally visible); every 256 polls
+    // ask the stream, so a kernel that ended without writing it (an error) is caught by the
+    // synchronising read-back below.
+    volatile jacobi::HostDone* d = p->done_host;
+    for (unsigned i = 1;; ++i) {
+      if (d->seq == seq) {
+        std::atomic_thread_fence(std::memory_order_acquire);
+        if (d->nonfinite) return nonfinite_error();
+        *iters_out = d->iters;
+        return d->status;
+      }
+      if ((i & 255) == 0 && cudaStreamQuery(p->stream) != cudaErrorNotReady) break;
+    }
     JCUDA(cudaMemcpyAsync(&p->st_host[0], p->st, sizeof(jacobi::State), cudaMemcpyDeviceToHost, p->stream));
     JCUDA(cudaStreamSynchronize(p->stream));
     JLAST("solve");
-    p->sweeps_launched = 1;
     if (p->st_host[0].nonfinite) return nonfinite_error();
     if (!p->st_host[0].done) return jacobi_set_error(JACOBI_ECUDA, "internal: small-n solve ended without a stop decision");
     *iters_out = p->st_host[0].iters;
