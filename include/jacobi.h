@@ -48,7 +48,11 @@
  *     (ordered with the legacy default stream, where device inputs written on stream 0 — torch's
  *     default stream — are complete before the plan reads them).  Device inputs written on any
  *     other stream must be complete, or ordered before the call on cuda_stream, by the caller.
- *     Functions return after the work they enqueue has completed (they synchronize that stream).
+ *     Functions return after the work they enqueue has completed: its results are written and
+ *     visible to the host and to any stream.  They synchronize the stream, except a small-n device
+ *     solve (one cluster launch), which returns when the kernel's completion record — written after
+ *     every result store, behind a system-scope fence — reaches host memory (the kernel may still be
+ *     retiring; later work on the stream is ordered after it as usual).
  */
 #ifndef JACOBI_H
 #define JACOBI_H
