@@ -171,6 +171,18 @@ int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dty
     JCUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, p->device));
     const double a_bytes = (double)a_rows * (double)a_cols * (dtype == JACOBI_F32 ? 4.0 : 8.0);
     if (l2 > 0 && a_bytes <= 4.0 * l2) p->l2_keep_pm = (int)std::min(1000.0, 1000.0 * 0.59 * l2 / a_bytes);
+    // fp64: the kernels keep whole 8-row tiles of each CTA's rows (one CTA per SM), tile t when
+    // t*8*1000 < rows*keep.  A per-mille share just above a tile boundary keeps one tile too many on
+    // every CTA and the kept set no longer fits (c2: 580 ‰ of 28 rows keeps 24 rows — 10 % L2 hits —
+    // where 16 rows give 53 %, profiles/l2keep_grid_r01.md).  So the budget — 78 % of the L2, the
+    // measured best with whole tiles (kept share of the L2 vs µs per sweep, profiles/l2keep_tiles_r01.md:
+    // n = 3584 0.77 best; 4096 0.59 best, 0.88 thrashes; 4608 0.66 best; 6144 0.44 best, 0.88 worse) —
+    // is rounded down to whole tiles T per CTA, and keep is placed where every CTA keeps exactly T.
+    if (dtype == JACOBI_F64 && p->l2_keep_pm > 0 && p->l2_keep_pm < 1000 && p->num_sms > 0 && a_rows >= p->num_sms) {
+      const int64_t G = p->num_sms, rmax = (a_rows + G - 1) / G;
+      const int64_t T = (int64_t)(0.78 * l2 / (a_cols * 8.0 * G) / 8.0);
+      p->l2_keep_pm = T >= 1 ? (int)std::min<int64_t>(1000, T * 8 * 1000 / rmax) : 0;
+    }
     if (const char* e = getenv("JACOBI_L2_KEEP")) p->l2_keep_pm = std::max(0, std::min(1000, atoi(e)));
   }
   choose_variant(p, a_cols, &p->variant, &p->grid);
