@@ -1313,14 +1313,14 @@ static int gridsync_gr(int dtype, int nchunks) {
 // units spill: 4096 14.4 / 17.1, 8192 47.5 / 59.9).  JACOBI_GRID_R = 4 | 8 overrides.
 static int gridsync_r(int dtype, int nchunks) {
   if (dtype != JACOBI_F32) return 8;
+  if (gridsync_gr(dtype, nchunks) == 1) return 4;  // no fp32 R = 8 one-chunk-unit instance (it spills)
   if (const char* e = getenv("JACOBI_GRID_R")) return atoi(e) == 8 ? 8 : 4;
-  return gridsync_gr(dtype, nchunks) > 1 ? 8 : 4;
+  return 8;
 }
 static const void* gridsync_fn(int dtype, int nchunks) {
   const int gr = gridsync_gr(dtype, nchunks);
   if (dtype == JACOBI_F32 && gridsync_r(dtype, nchunks) == 8) {
     switch (gr) {
-      case 1: return (const void*)k_solve_gridsync<float, 8, 16, true, 1>;
       case 2: return (const void*)k_solve_gridsync<float, 8, 16, true, 2>;
       default: return (const void*)k_solve_gridsync<float, 8, 16, true, 4>;
     }
