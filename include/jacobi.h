@@ -132,6 +132,9 @@ typedef struct {
                                    this many CTAs (all sweeps of a launch, grid barrier between
                                    sweeps; same bits); JACOBI_PERSIST=0/1 disables / forces it
                                    where it applies (1 GPU, row blocks, max norm)                 */
+  int l2_keep_permille;         /* share of each CTA's rows loaded with L2::evict_last (kept in L2
+                                   across sweeps; whole 8-row tiles for fp64); 0: A streams with
+                                   evict_first.  Changes no result bit.  JACOBI_L2_KEEP overrides  */
 } jacobi_plan_info_t;
 int jacobi_plan_info(const jacobi_plan* plan, jacobi_plan_info_t* info);
 

@@ -62,7 +62,7 @@ class PlanInfo(ctypes.Structure):
                 ("grid_ctas", ctypes.c_int), ("threads_per_cta", ctypes.c_int), ("a_borrowed", ctypes.c_int),
                 ("sweeps_launched", ctypes.c_int64), ("bytes_per_sweep", ctypes.c_double),
                 ("variant", ctypes.c_int), ("num_variants", ctypes.c_int), ("cluster_ctas", ctypes.c_int),
-                ("persistent_ctas", ctypes.c_int)]
+                ("persistent_ctas", ctypes.c_int), ("l2_keep_permille", ctypes.c_int)]
 
 
 def _load():

@@ -474,6 +474,7 @@ extern "C" int jacobi_plan_info(const jacobi_plan* p, jacobi_plan_info_t* info) 
   info->num_variants = jacobi::num_variants();
   info->cluster_ctas = use_cluster(p) ? p->cluster_C : 0;
   info->persistent_ctas = use_grid(p) ? p->grid_G : (use_grid_push(p) ? p->num_sms : 0);
+  info->l2_keep_permille = p->l2_keep_pm;
   return 0;
 }
 

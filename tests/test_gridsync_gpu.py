@@ -131,6 +131,30 @@ def test_gridsync_device_borrowed(jb, monkeypatch):
     assert r.iters == q.iters == 60 and np.array_equal(xo.cpu().numpy(), q.x)
 
 
+@pytest.mark.parametrize("n,tiles", [(2048, None), (3584, 3), (4096, 2), (4608, 2), (6144, 1), (16384, 0)])
+def test_l2_keep_whole_tiles(jb, n, tiles, monkeypatch):
+    """fp64 L2-kept share (profiles/l2keep_tiles_r01.md): whole 8-row tiles per CTA
+    within 0.78 x L2, every CTA (rows_min or rows_max) keeping the same number of tiles; A that fits
+    the budget entirely is kept whole; A > 4 x L2 streams (0)."""
+    import torch
+    monkeypatch.delenv("JACOBI_L2_KEEP", raising=False)
+    G = torch.cuda.get_device_properties(0).multi_processor_count
+    dA = torch.eye(n, dtype=torch.float64, device="cuda") * 2.0
+    with jb.Plan(dA, n=n) as p:
+        keep = p.info.l2_keep_permille
+    if tiles is None:
+        assert keep == 1000
+        return
+    if tiles == 0:
+        assert keep == 0
+        return
+    for rows in (n // G, -(-n // G)):  # the kernels keep tile t of a CTA when t*8*1000 < rows*keep
+        kept = sum(1 for t in range(-(-rows // 8)) if t * 8 * 1000 < rows * keep)
+        assert kept == tiles, (n, rows, keep, kept)
+    L2 = torch.cuda.get_device_properties(0).L2_cache_size
+    assert tiles * 8 * n * 8 * G <= 0.78 * L2 < (tiles + 1) * 8 * n * 8 * G
+
+
 @pytest.mark.parametrize("n,f32,path", [(256, False, "cluster"), (512, False, "cluster"), (600, False, "grid"),
                                         (512, True, "cluster"), (576, True, "grid"), (600, True, "grid"), (3072, False, "grid"),
                                         (4096, False, "grid"), (8192, False, "graph")])
