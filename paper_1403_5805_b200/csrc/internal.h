@@ -59,6 +59,8 @@ struct SweepArgs {
   double* x1buf;
   double* part;             // partial row sums, part[c * m + r]
   unsigned* cnt;            // per row-tile arrival counters (reset by the finalizing warp)
+  unsigned* dyn;            // dynamic tile assignment (variants with DYN): sweep k takes tiles from
+                            // dyn[k & 3]; zeroed by k_prepare and, one sweep ahead, by CTA 0
   unsigned long long* dslot;// 4-slot ring of max|dx| bit patterns; sweep k uses slot k & 3
   State* st;
   int64_t col0, cend;       // column range of A held here: [0, n) row-wise; a slab column-wise (NEXT-4)
@@ -97,7 +99,7 @@ cudaError_t launch_copy_pitched(int dtype, const void* src, int64_t src_ld, void
                                 int64_t rows, int64_t n, cudaStream_t s);
 int num_variants();
 const char* variant_name(int variant);
-int default_variant(int dtype, int nchunks, int chunk, bool l2_keep);
+int default_variant(int dtype, int nchunks, int chunk, bool l2_keep, int64_t rows, int num_sms);
 bool variant_uses_l2_keep(int variant);
 bool variant_is_cta(int variant);
 bool variant_is_push(int variant);

@@ -105,7 +105,8 @@ static int check_last(const char* what) {
 // JACOBI_SWEEP_VARIANT override is honoured when the variant can tile the chunking).
 static void choose_variant(const jacobi_plan* p, int64_t ncols, int* variant, int* grid) {
   const int nch = (int)((ncols + p->chunk - 1) / p->chunk);
-  int v = jacobi::default_variant(p->dtype, nch, p->chunk, p->l2_keep_pm > 0);
+  int v = jacobi::default_variant(p->dtype, nch, p->chunk, p->l2_keep_pm > 0, p->colwise ? p->n : p->m / p->nblocks,
+                                  p->num_sms);
   if (const char* e = getenv("JACOBI_SWEEP_VARIANT")) {  // tuning override (all variants: same bits)
     const int vi = atoi(e);
     if (vi >= 0 && vi < jacobi::num_variants() && !jacobi::variant_is_push(vi) &&
@@ -194,7 +195,7 @@ int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dty
   JCUDA(cudaMalloc(&p->x[0], (size_t)p->x_len * 8));
   JCUDA(cudaMalloc(&p->x[1], (size_t)p->x_len * 8));
   JCUDA(cudaMalloc(&p->part, (size_t)(nchunks * a_rows) * 8));
-  JCUDA(cudaMalloc(&p->cnt, (size_t)a_rows * 4));
+  JCUDA(cudaMalloc(&p->cnt, (size_t)a_rows * 4 * 5));  // + 4 dynamic-tile counters per row block
   p->nblk = (m + jacobi::kL2Block - 1) / jacobi::kL2Block;
   JCUDA(cudaMalloc(&p->sq, (size_t)m * 2 * 8));  // two halves: the persistent solver double-buffers dx^2
   JCUDA(cudaMalloc(&p->blk, (size_t)p->nblk * 8));
@@ -211,7 +212,7 @@ int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dty
   JCUDA(cudaHostGetDevicePointer(&p->done_dev, p->done_host, 0));
   JCUDA(cudaMemsetAsync(p->x[0], 0, (size_t)p->x_len * 8, p->stream));
   JCUDA(cudaMemsetAsync(p->x[1], 0, (size_t)p->x_len * 8, p->stream));
-  JCUDA(cudaMemsetAsync(p->cnt, 0, (size_t)a_rows * 4, p->stream));
+  JCUDA(cudaMemsetAsync(p->cnt, 0, (size_t)a_rows * 4 * 5, p->stream));
   JLAST("plan buffers");
   return 0;
 }
@@ -493,6 +494,7 @@ static jacobi::SweepArgs sweep_args(const jacobi_plan* p, int blk) {
   a.x1buf = p->x[1];
   a.part = p->part;
   a.cnt = p->cnt;
+  a.dyn = p->cnt + p->a_rows + 4 * blk;
   a.dslot = p->dslot;
   a.st = p->st;
   a.col0 = 0;
@@ -645,7 +647,7 @@ static int solve_prepare(jacobi_plan* p, const double* b, const double* x0, bool
     JCUDA(cudaMemcpyAsync(p->x[0], x0, (size_t)p->n * 8, cudaMemcpyHostToDevice, p->stream));
   }
   JCUDA(cudaMemsetAsync(p->st, 0, sizeof(jacobi::State), p->stream));
-  JCUDA(jacobi::launch_prepare(p->st, max_iter, tol, hist_dev, p->dslot, p->cnt, p->a_rows, p->b, dev ? b : nullptr,
+  JCUDA(jacobi::launch_prepare(p->st, max_iter, tol, hist_dev, p->dslot, p->cnt, p->a_rows * 5, p->b, dev ? b : nullptr,
                                p->m, p->x[0], dev ? x0 : nullptr, p->n, p->p2p ? p->flags : nullptr, p->gbar,
                                p->stream));
   if (p->p2p_emul) {  // virtual ranks 1..P-1: their x^(0), slots and counters

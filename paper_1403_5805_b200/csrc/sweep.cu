@@ -435,24 +435,31 @@ __device__ __forceinline__ unsigned long long cta_max_bits(unsigned long long wm
 // GR > 1: a work unit is (chunk, group of R/GR rows of the tile) instead of (chunk, tile): with
 // nchunks not a multiple of the warp count, nchunks x GR units balance the warps (24 chunks: 1.5
 // chunks per warp per tile — warps 0-7 do two — become 3 units each).  Same per-row order.
-template <typename T, int R, int NW, int U, int XL, bool PUSH, bool POL, int GR = 1, bool PIN = false>
+// DYN: tiles are taken from a launch-wide counter (a.dyn[0]) instead of a static row range, so SMs
+// that stream faster take more tiles (the static partition leaves a fixed minority of slower SMs
+// finishing last: profiles/sm_tail_r01.jsonl).  Sequence t's tile index sits in s_tile[t & 7]:
+// thread 0 claims the tile of sequence t + kSlots when it starts sequence t (the atomic's latency
+// hides behind its unit) and publishes it before its arrival on s_full of t; a warp reads it only
+// after s_empty of that slot, which orders the publication before the read.  -1 = no tiles left.
+template <typename T, int R, int NW, int U, int XL, bool PUSH, bool POL, int GR = 1, bool PIN = false,
+          bool DYN = false>
 __device__ __forceinline__ unsigned long long cta_sweep(const SweepArgs& a, const int64_t k, const int64_t tbase,
                                                         double* s_part, uint64_t* s_full, uint64_t* s_empty,
-                                                        const int cta, const int ncta) {
+                                                        const int cta, const int ncta, volatile int* s_tile = nullptr) {
   const double* __restrict__ xo = (k & 1) ? a.x0buf : a.x1buf;  // x^(k-1)
   double* __restrict__ xn = (k & 1) ? a.x1buf : a.x0buf;        // x^(k)
   const T* __restrict__ A = static_cast<const T*>(a.A);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int nch = a.nchunks;
-  const int64_t rb = (int64_t)cta * a.m / ncta;  // this CTA's rows of the launch (rank)
-  const int64_t re = (int64_t)(cta + 1) * a.m / ncta;
+  const int64_t rb = DYN ? 0 : (int64_t)cta * a.m / ncta;  // this CTA's rows of the launch (rank)
+  const int64_t re = DYN ? a.m : (int64_t)(cta + 1) * a.m / ncta;
   const int ntile = (int)((re - rb + R - 1) / R);
   unsigned long long dmax = 0ull;
 
   auto finalize = [&](int t) {
     const int64_t tt = tbase + t;
     const int q = (int)(tt % kSlots);
-    const int64_t r0 = rb + (int64_t)t * R;
+    const int64_t r0 = DYN ? (int64_t)s_tile[t & 7] * R : rb + (int64_t)t * R;
     const int nv = (int)min((int64_t)R, re - r0);
     // The epilogue's own operands (b_i, a_ii, x_i^(k-1)) do not depend on the partial sums: load
     // them before waiting for the tile, so their latency hides behind the other warps' work.
@@ -490,12 +497,23 @@ __device__ __forceinline__ unsigned long long cta_sweep(const SweepArgs& a, cons
     if (lane == 0) mbar_arrive(&s_empty[q]);
   };
 
-  for (int t = 0; t < ntile; ++t) {
+  unsigned pend = 0u;  // DYN: thread 0's claim for sequence t + kSlots
+  int t = 0;
+  for (;; ++t) {
+    if (!DYN && t >= ntile) break;
     const int64_t tt = tbase + t;
     const int q = (int)(tt % kSlots);
-    const int64_t r0 = rb + (int64_t)t * R;
-    const int nv = (int)min((int64_t)R, re - r0);
     if (tt >= kSlots) mbar_wait(&s_empty[q], (unsigned)(((tt / kSlots) - 1) & 1));
+    int64_t r0;
+    if constexpr (DYN) {
+      const int tile = s_tile[t & 7];
+      if (tile < 0) break;
+      r0 = (int64_t)tile * R;
+      if (threadIdx.x == 0) pend = atomicAdd(a.dyn, 1u);
+    } else {
+      r0 = rb + (int64_t)t * R;
+    }
+    const int nv = (int)min((int64_t)R, re - r0);
     const T* rowp[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) rowp[r] = A + (r0 + min(r, nv - 1)) * a.lda - a.col0;  // global columns
@@ -537,10 +555,17 @@ __device__ __forceinline__ unsigned long long cta_sweep(const SweepArgs& a, cons
       }
     }
     __syncwarp();
+    if constexpr (DYN)
+      if (threadIdx.x == 0) s_tile[(t + kSlots) & 7] = pend < (unsigned)a.tiles ? (int)pend : -1;
     if (lane == 0) mbar_arrive(&s_full[q]);
     if (t >= 1 && (t - 1) % NW == w) finalize(t - 1);
   }
-  if (ntile >= 1 && (ntile - 1) % NW == w) finalize(ntile - 1);
+  if (t >= 1 && (t - 1) % NW == w) finalize(t - 1);  // t = tiles processed
+  if constexpr (DYN)  // the launch's last CTA resets the counters for the next launch (all claims are done)
+    if (threadIdx.x == 0 && atomicAdd(a.dyn + 1, 1u) == (unsigned)ncta - 1u) {
+      a.dyn[0] = 0u;
+      a.dyn[1] = 0u;
+    }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     const unsigned long long o = __shfl_xor_sync(kFull, dmax, off);
@@ -549,14 +574,20 @@ __device__ __forceinline__ unsigned long long cta_sweep(const SweepArgs& a, cons
   return dmax;
 }
 
-template <typename T, int R, int NW, int U = 1, int XL = 0, bool PUSH = false, bool POL = false, int GR = 1>
+template <typename T, int R, int NW, int U = 1, int XL = 0, bool PUSH = false, bool POL = false, int GR = 1,
+          bool DYN = false>
 __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, const int j) {
   SMT_BEGIN();
   extern __shared__ __align__(16) double s_part[];  // [kSlots][nchunks][R]
   __shared__ __align__(8) uint64_t s_full[kSlots], s_empty[kSlots];
   __shared__ int s_go;
+  __shared__ int s_tile[8];  // DYN: tile of sequence t at [t & 7]
   if (threadIdx.x == 0) {
     s_go = sweep_prologue(a, j, blockIdx.x == 0);
+    if (DYN && s_go) {  // the tiles of sequences 0 .. kSlots-1
+      const unsigned base = atomicAdd(a.dyn, (unsigned)kSlots);
+      for (int q = 0; q < kSlots; ++q) s_tile[q] = base + q < (unsigned)a.tiles ? (int)(base + q) : -1;
+    }
     for (int q = 0; q < kSlots; ++q) {
       mbar_init(&s_full[q], NW);
       mbar_init(&s_empty[q], 1);
@@ -569,7 +600,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
   const int64_t k = a.st->kbase + j + 1;
   __shared__ unsigned long long s_wmax[NW];
   const unsigned long long dmax =
-      cta_sweep<T, R, NW, U, XL, PUSH, POL, GR>(a, k, 0, s_part, s_full, s_empty, blockIdx.x, gridDim.x);
+      cta_sweep<T, R, NW, U, XL, PUSH, POL, GR, false, DYN>(a, k, 0, s_part, s_full, s_empty, blockIdx.x, gridDim.x,
+                                                           s_tile);
   if constexpr (!PUSH) {
     if ((threadIdx.x & 31) == 0 && dmax) atomicMax(&a.dslot[k & 3], dmax);  // local L2: one per warp is fine
   } else {
@@ -1196,6 +1228,8 @@ const Variant kVariants[] = {
     // CTA kernel R8 L2-policy with (chunk, row group) units: balanced when nchunks is not a multiple of 16
     {"k_sweep_cta R8 U1 L2-policy rows/2", 8, 512, 1, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, false, true, 2>, k_sweep_cta<float, 4, 16, 1, 0, false, true, 2>},
     {"k_sweep_cta R8 U1 L2-policy rows/4", 8, 512, 1, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, false, true, 4>, k_sweep_cta<float, 4, 16, 1, 0, false, true, 4>},
+    // CTA kernel with dynamic tile assignment (a launch-wide counter) instead of static row ranges
+    {"k_sweep_cta R8 U1 L2-policy dynamic", 8, 512, 1, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, false, true, 1, true>, k_sweep_cta<float, 4, 16, 1, 0, false, true, 1, true>},
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
@@ -1249,9 +1283,15 @@ int variant_rows_dt(int v, int dtype) { return dtype == JACOBI_F32 ? kVariants[v
 //   tile: +50 % of the A bytes with fp32 A).  For fp64 A the shared-memory ring measured 1-2.5 %
 //   slower than the CTA kernel (c4 7092 / 7076, c3 6564 / 6676), so fp64 keeps the CTA kernel;
 // - fewer chunks: the item kernel R=8,U=1 (fp64) or R=4,U=1 (fp32).
-int default_variant(int dtype, int nchunks, int chunk, bool l2_keep) {
+int default_variant(int dtype, int nchunks, int chunk, bool l2_keep, int64_t rows, int num_sms) {
   if (dtype == JACOBI_F32 && nchunks >= 16) return variant_fits(18, nchunks, dtype, chunk) ? 18 : 12;
-  (void)l2_keep;  // the POL instance streams A with evict_first when no share is kept (l2_keep_pm = 0)
+  // Dynamic tiles (24) once a CTA has >= 40 tiles of 8 rows: the expected idle of dynamic assignment,
+  // about half a tile, then undercuts the static partition's tail (a fixed minority of slower SMs):
+  // c4 (55 tiles per CTA) 4704 -> 4670 µs per sweep; c3 (14) 302.6 -> 306.8 and n = 6144 (5) 47.8 ->
+  // 48.9 lose.
+  if (dtype == JACOBI_F64 && !l2_keep && nchunks >= 32 && num_sms > 0 && rows >= (int64_t)40 * 8 * num_sms &&
+      variant_fits(24, nchunks, dtype, chunk))
+    return 24;
   // 16 < nchunks < 32, not a multiple of 16: (chunk, half-tile) units balance the 16 warps (n = 12288 /
   // 20000 / 24576: +3 / +4 / +2 %; from 40 chunks on, and for multiples of 16, whole-tile units win).
   const int big = (dtype == JACOBI_F64 && nchunks > 16 && nchunks < 32 && nchunks % 16 != 0) ? 22 : 20;
