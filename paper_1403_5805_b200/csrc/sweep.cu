@@ -1230,6 +1230,8 @@ const Variant kVariants[] = {
     {"k_sweep_cta R8 U1 L2-policy rows/4", 8, 512, 1, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, false, true, 4>, k_sweep_cta<float, 4, 16, 1, 0, false, true, 4>},
     // CTA kernel with dynamic tile assignment (a launch-wide counter) instead of static row ranges
     {"k_sweep_cta R8 U1 L2-policy dynamic", 8, 512, 1, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, false, true, 1, true>, k_sweep_cta<float, 4, 16, 1, 0, false, true, 1, true>},
+    {"k_sweep_cta R4 U1 L2-policy dynamic", 4, 512, 1, 4, 1, 1, k_sweep_cta<double, 4, 16, 1, 0, false, true, 1, true>, k_sweep_cta<float, 4, 16, 1, 0, false, true, 1, true>},
+    {"k_sweep_cta R4 U2 L2-policy dynamic", 4, 512, 1, 4, 2, 2, k_sweep_cta<double, 4, 16, 2, 0, false, true, 1, true>, k_sweep_cta<float, 4, 16, 2, 0, false, true, 1, true>},
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
@@ -1285,13 +1287,14 @@ int variant_rows_dt(int v, int dtype) { return dtype == JACOBI_F32 ? kVariants[v
 // - fewer chunks: the item kernel R=8,U=1 (fp64) or R=4,U=1 (fp32).
 int default_variant(int dtype, int nchunks, int chunk, bool l2_keep, int64_t rows, int num_sms) {
   if (dtype == JACOBI_F32 && nchunks >= 16) return variant_fits(18, nchunks, dtype, chunk) ? 18 : 12;
-  // Dynamic tiles (24) once a CTA has >= 40 tiles of 8 rows: the expected idle of dynamic assignment,
-  // about half a tile, then undercuts the static partition's tail (a fixed minority of slower SMs):
-  // c4 (55 tiles per CTA) 4704 -> 4670 µs per sweep; c3 (14) 302.6 -> 306.8 and n = 6144 (5) 47.8 ->
-  // 48.9 lose.
-  if (dtype == JACOBI_F64 && !l2_keep && nchunks >= 32 && num_sms > 0 && rows >= (int64_t)40 * 8 * num_sms &&
-      variant_fits(24, nchunks, dtype, chunk))
-    return 24;
+  // Dynamic tiles of 4 rows, two column steps in flight (26) once a CTA has >= 32 such tiles: the
+  // expected idle of dynamic assignment, about half a tile, then undercuts the static partition's
+  // tail (a fixed minority of slower SMs).  µs per sweep, static default / 26 (R8 dynamic, 24, in
+  // between): n = 20000 491 / 485, 24576 688 / 681, 32768 1186 / 1188, 49152 2667 / 2631, 65536
+  // 4704 / 4668; below the threshold it loses (16384: 302 / 305; 12288: 178 / 180).
+  if (dtype == JACOBI_F64 && !l2_keep && nchunks >= 16 && num_sms > 0 && rows >= (int64_t)32 * 4 * num_sms &&
+      variant_fits(26, nchunks, dtype, chunk))
+    return 26;
   // 16 < nchunks < 32, not a multiple of 16: (chunk, half-tile) units balance the 16 warps (n = 12288 /
   // 20000 / 24576: +3 / +4 / +2 %; from 40 chunks on, and for multiples of 16, whole-tile units win).
   const int big = (dtype == JACOBI_F64 && nchunks > 16 && nchunks < 32 && nchunks % 16 != 0) ? 22 : 20;

@@ -27,7 +27,7 @@ QUICK = "--quick" in sys.argv  # one graph-path case (checker self-test)
 CASES = ((1, False, [None], ["0"]), (37, False, [None], ["0"]), (300, True, [None], ["0"]),
          (700, False, [None], ["1", "0"]), (3001, False, [None, "7", "12", "18"], ["1", "0"]),
          (2049, True, [None, "18"], ["1", "0"]),
-         (8190, False, [None, "1", "6", "9", "10", "16", "19", "20", "24"], ["0"]),
+         (8190, False, [None, "1", "6", "9", "10", "16", "19", "20", "24", "26"], ["0"]),
          (8190, True, [None, "12", "18"], ["0"]))
 for n, f32, variants, modes in (((3001, False, [None], ["0"]),) if QUICK else CASES):
     A, b = dominant(n, n, f32)

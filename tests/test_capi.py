@@ -113,6 +113,6 @@ def test_default_variant_indices_keep_their_names(jb):
     expect = {1: "k_sweep R8 U1", 6: "k_sweep_cta R8 U1", 7: "k_sweep_cta R4 U1", 12: "k_sweep_panel R4 U1",
               18: "k_sweep_panel R4 U1 x-smem", 20: "k_sweep_cta R8 U1 L2-policy",
               21: "k_sweep_cta R8 U1 fused-exchange", 22: "k_sweep_cta R8 U1 L2-policy rows/2",
-              24: "k_sweep_cta R8 U1 L2-policy dynamic"}
+              24: "k_sweep_cta R8 U1 L2-policy dynamic", 26: "k_sweep_cta R4 U2 L2-policy dynamic"}
     for v, name in expect.items():
         assert jb.variant_name(v) == name, (v, jb.variant_name(v))
