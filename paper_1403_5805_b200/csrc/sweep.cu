@@ -7,10 +7,12 @@
 //   k_sweep       (item kernel, n with < 16 chunks): work item = (tile of R rows, column chunk),
 //                 round-robin over a persistent grid; chunk partials in global memory, the last
 //                 warp to arrive on a tile's counter finalizes it;
-//   k_sweep_cta   (fp64 default): CTA b owns rows [b*m/G, (b+1)*m/G); warp w streams chunks
+//   k_sweep_cta   (fp64 default): CTA b owns rows [b*m/G, (b+1)*m/G) — or, with DYN (large row
+//                 blocks, c4), takes tiles from a launch-wide counter; warp w streams chunks
 //                 w, w+16, ... of each tile; partials meet in a shared-memory ring (mbarriers) and a
 //                 finalizer warp per tile applies the epilogue; also the L2-keep (POL) and the
-//                 fused-exchange (PUSH, NEXT-1) instances;
+//                 fused-exchange (PUSH, NEXT-1) instances; its body is each sweep of the persistent
+//                 grid solver (k_solve_gridsync, mid-size n);
 //   k_sweep_panel (fp32-A default): each warp owns whole rows and walks all chunks in order;
 //                 optionally x^(k-1) staged in shared memory by a TMA chunk ring (XSN).
 //
