@@ -291,3 +291,43 @@ def test_distinct_plans_on_distinct_threads(jb, monkeypatch):
     assert not errs, errs
     for i in range(len(systems)):
         assert np.array_equal(out[i], alone[i]), i
+
+
+def test_dynamic_tile_plans_concurrently(jb, monkeypatch):
+    """Dynamic tile assignment (variant 26; DESIGN.md §6 tail paragraph): each plan owns its tile
+    counters, so two plans claiming tiles at once on different streams give the bits each gives
+    alone, and the counters reset themselves between launches (many sweeps, several solves)."""
+    import threading
+    monkeypatch.delenv("JACOBI_PERSIST", raising=False)
+    monkeypatch.setenv("JACOBI_PERSIST", "0")
+    monkeypatch.setenv("JACOBI_SWEEP_VARIANT", "26")
+    systems = [dominant(n, 700 + n, scale=1.05) for n in (4096, 6000)]
+    alone = []
+    for A, b, _ in systems:
+        with jb.Plan(A) as p:
+            assert jb.variant_name(p.info.variant) == "k_sweep_cta R4 U2 L2-policy dynamic"
+            alone.append(p.solve(b, None, 45, 0.0).x)
+    monkeypatch.delenv("JACOBI_SWEEP_VARIANT")
+    with jb.Plan(systems[0][0]) as p:  # the static default of this size: same bits
+        assert np.array_equal(p.solve(systems[0][1], None, 45, 0.0).x, alone[0])
+    monkeypatch.setenv("JACOBI_SWEEP_VARIANT", "26")
+    plans = [jb.Plan(A) for A, _, _ in systems]
+    out, errs = [None] * len(systems), []
+
+    def run(i):
+        try:
+            for _ in range(3):
+                out[i] = plans[i].solve(systems[i][1], None, 45, 0.0).x
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(len(systems))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for p in plans:
+        p.close()
+    assert not errs, errs
+    for i in range(len(systems)):
+        assert np.array_equal(out[i], alone[i]), i
