@@ -4,6 +4,8 @@
 //   1: red.release.gpu.global.add + ld.acquire.gpu spin
 //   2: cooperative_groups::this_grid().sync()
 //   3: variant 0 plus a dependent L2 read after the barrier (the solver's stop-test read)
+//   4: two-level: 8 group counters, each group's last arriver adds to a top counter that all poll
+//   5: per-CTA epoch flags (st.release), warp 0 of every CTA polls all flags (ld.acquire) with a vote
 // Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o probes/gridbar_probe probes/gridbar_probe.cu
 #include <cooperative_groups.h>
 #include <cstdio>
@@ -17,12 +19,44 @@ __device__ __forceinline__ unsigned long long ld_acq(const unsigned long long* p
   return v;
 }
 
+__device__ __forceinline__ void st_rel(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 template <int V>
 __global__ void __launch_bounds__(512, 1) k(unsigned long long* ctr, double* slot, int iters, double* out) {
   double acc = 0.0;
   for (int it = 1; it <= iters; ++it) {
     if constexpr (V == 2) {
       cg::this_grid().sync();
+    } else if constexpr (V == 4) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const unsigned G = gridDim.x, grp = blockIdx.x & 7u;
+        const unsigned gsize = G / 8u + (grp < (G & 7u) ? 1u : 0u);
+        __threadfence();
+        const unsigned long long old = atomicAdd(ctr + 16 + 16 * grp, 1ull);
+        if (old == (unsigned long long)gsize * it - 1ull) atomicAdd(ctr, 1ull);
+        const unsigned long long target = 8ull * it;
+        while (ld_acq(ctr) < target) {
+        }
+      }
+      __syncthreads();
+    } else if constexpr (V == 5) {
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        if (threadIdx.x == 0) {
+          __threadfence();
+          st_rel(ctr + 256 + blockIdx.x, (unsigned long long)it);
+        }
+        bool done = false;
+        while (!done) {
+          bool mine = true;
+          for (unsigned b = threadIdx.x; b < gridDim.x; b += 32) mine &= ld_acq(ctr + 256 + b) >= (unsigned long long)it;
+          done = __all_sync(0xffffffffu, mine);
+        }
+      }
+      __syncthreads();
     } else {
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -48,15 +82,15 @@ int main() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   unsigned long long* ctr;
   double *slot, *out;
-  cudaMalloc(&ctr, 8);
+  cudaMalloc(&ctr, 8 * 1024);
   cudaMalloc(&slot, 8);
   cudaMalloc(&out, 8);
   const int iters = 20000;
-  void (*fns[])(unsigned long long*, double*, int, double*) = {k<0>, k<1>, k<2>, k<3>};
-  for (int v = 0; v < 4; ++v) {
+  void (*fns[])(unsigned long long*, double*, int, double*) = {k<0>, k<1>, k<2>, k<3>, k<4>, k<5>};
+  for (int v = 0; v < 6; ++v) {
     float best = 1e30f;
     for (int r = 0; r < 3; ++r) {
-      cudaMemset(ctr, 0, 8);
+      cudaMemset(ctr, 0, 8 * 1024);
       cudaEvent_t e0, e1;
       cudaEventCreate(&e0);
       cudaEventCreate(&e1);
