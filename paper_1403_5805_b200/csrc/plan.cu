@@ -35,7 +35,9 @@ struct Range {
 //   persistent solver's ~4 µs floor for small n (cluster vs persistent, JACOBI_CLUSTER_MAXN sweep,
 //   profiles/cluster_r01.jsonl: fp64 256: 1.52 vs 4.2, 512: 3.23 vs 4.22, 576: 5.16 vs 4.11; fp32
 //   512: 3.14 vs 3.84, 576: 5.21 vs 3.95 — more than 32 rows per CTA puts 3 rows on a warp).
-constexpr double kPersistMaxBytesF64 = 200e6, kPersistMaxBytesF32 = 300e6;
+// fp64 limit re-measured with the whole-tile L2 keep (persistent / graph µs per sweep): n = 4224 (143 MB)
+// 24.2 / 25.5, 4352 (152 MB) 28.5 / 28.0, 4608 (170 MB) 30.5 / 29.5.
+constexpr double kPersistMaxBytesF64 = 148e6, kPersistMaxBytesF32 = 300e6;
 constexpr int64_t kClusterPreferMaxN_F64 = 512, kClusterPreferMaxN_F32 = 512;
 
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
