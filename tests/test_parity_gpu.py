@@ -564,3 +564,21 @@ def test_enomem_on_oversized_plan_then_healthy(jb):
     A, b, _ = dominant(512, 3, scale=1.05)
     with jb.Plan(A) as p:
         assert p.solve(b, None, 10, 0.0).iters == 10
+
+
+@pytest.mark.parametrize("n,seed,max_iter,tol", [(18950, 1, 6, 0.0), (20001, 2, 40, 1e-9), (24575, 3, 5, 0.0)])
+def test_dynamic_tile_default_sizes_vs_oracle(jb, n, seed, max_iter, tol):
+    """Ragged sizes where the default sweep kernel takes its tiles dynamically: same
+    status and iteration count as the oracle, relative L-inf error <= 1e-10."""
+    rng = np.random.default_rng(seed)
+    A = rng.uniform(-1, 1, (n, n))
+    np.fill_diagonal(A, 0.0)
+    np.fill_diagonal(A, np.abs(A).sum(1) * 1.05 * rng.choice([-1.0, 1.0], n))
+    b = rng.uniform(-1, 1, n)
+    x0 = rng.uniform(-1, 1, n)
+    st_o, x_o, it_o = oracle.jacobi(A, b, x0, max_iter, tol, nthreads=16)
+    with jb.Plan(A) as p:
+        assert jb.variant_name(p.info.variant) == "k_sweep_cta R4 U2 L2-policy dynamic"
+        r = p.solve(b, x0, max_iter, tol)
+    assert (r.status, r.iters) == (st_o, it_o)
+    assert rel_linf(r.x, x_o) <= TOL64
