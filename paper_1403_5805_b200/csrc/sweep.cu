@@ -819,7 +819,8 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync_push(const SweepA
     __syncthreads();
     if (!s_go) break;
     const unsigned long long dmax =
-        cta_sweep<T, R, NW, 1, 2, true, true>(a, k, (k - k0) * ntile, s_part, s_full, s_empty, blockIdx.x - c0, c1 - c0);
+        cta_sweep<T, R, NW, 1, 2, true, true, 1, true>(a, k, (k - k0) * ntile, s_part, s_full, s_empty, blockIdx.x - c0,
+                                                   c1 - c0);
     __threadfence_system();  // this thread's x pushes, before the arrivals below
     const unsigned long long m = cta_max_bits<NW>(dmax, s_wmax);
     if (threadIdx.x == 0) {
