@@ -5,20 +5,27 @@ GB/s, % of peak) on the headline workload c4: n = 65536 dense fp64 (34.4 GB), fi
 One STEP = one jacobi_plan_solve of the workload (100 sweeps, tol = 0, the whole hot path:
 sweep + fused update + max|dx| + device stop test; + allgather/allreduce when N > 1).
   value : iterations/s with A, b, x0 resident in HBM (device-pointer solve), CUDA events on the
-          plan's stream, max over ranks.  A (34 GB) >> L2 (126 MB): every sweep streams A from HBM,
-          so no L2 flush is needed between steps.
-  e2e   : the same metric through the C-ABI one-shot call jacobi_solve() with HOST (pinned) buffers:
-          the H2D copy of A, b, x0, plan setup, 100 sweeps and the D2H copy of x are inside the
-          timed region every step (N = 1; under torchrun the distributed plan is created per step
-          from host rows).
-  --impl reference : the CPU oracle (oracle/), as it stands, on the box's host cores, on a bounded
-          row sample of the same workload per step; it/s extrapolated to whole sweeps.
+          plan's stream, max over ranks.  A (34 GB, or 34/N GB per GPU) >> L2 (126 MB): every sweep
+          streams A from HBM, so no L2 flush is needed between steps.
+  e2e   : the same metric through the C-ABI with HOST (pinned) buffers: N = 1 the one-shot
+          jacobi_solve() (H2D of A, b, x0, plan setup, 100 sweeps, D2H of x inside the timed region
+          every step); N > 1 every rank creates its distributed plan from its host row block per step.
+  cpu_baseline : the CPU oracle (oracle/), as it stands, on the host cores of rank 0: oracle.jacobi
+          over the WHOLE c4 system for a bounded number of its 100 sweeps (all cores), plus one-thread
+          per-sweep times of c1-c3.
+  --impl reference : the same oracle timing as the reference arm (rank 0 only under torchrun).
 
-Launch: python bench.py [--gpus N --steps K --warmup W]; N > 1 under torchrun (one rank per GPU).
+Multi-GPU: ``python bench.py --gpus N`` re-launches itself with N ranks (torch.distributed.run,
+127.0.0.1) when WORLD_SIZE is unset; under torchrun (the driver's form) it runs as one rank per GPU.
+Row blocks (§3) with the NCCL allgather of x + one-scalar max allreduce per sweep
+(the north star's exchange) is the headline; the fused NVLink push exchange (NEXT-1)
+is timed after it as a separate field (``fused_exchange``), bounded by a watchdog so a failure there
+can never cost the headline line.
 """
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -49,14 +56,61 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU oracle sample budget per run")
-    ap.add_argument("--exchange", choices=["auto", "nccl", "p2p", "cols"], default="auto",
-                    help="N > 1: fused NVLink push (NEXT-1, 'p2p'), NCCL row-wise, or column-wise (NEXT-4); "
-                         "auto = p2p when every GPU pair has peer access (agreed by all ranks), else nccl")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="CPU oracle budget: sweeps of the full system timed for about this long")
+    ap.add_argument("--ref-sweeps", type=int, default=5,
+                    help="--impl reference: oracle sweeps of the full system per step")
+    ap.add_argument("--exchange", choices=["nccl", "p2p", "cols"], default="nccl",
+                    help="N > 1 headline exchange: NCCL row-wise (north star, default), fused NVLink push "
+                         "(NEXT-1) or column-wise reduce-scatter (NEXT-4)")
+    ap.add_argument("--no-fused", action="store_true", help="N > 1: skip the fused-exchange side measurement")
+    ap.add_argument("--fused-timeout", type=float, default=180.0,
+                    help="watchdog (s) of the fused-exchange side measurement")
+    ap.add_argument("--launcher-dry-run", action="store_true",
+                    help="spawn the ranks (gloo, no GPU work) and report what was spawned: tests the launcher")
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the per-config rates of the other BASELINE.json configs (N = 1 only)")
     return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- self-launch (N > 1)
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def launch_ranks(args):
+    """`bench.py --gpus N` without WORLD_SIZE: re-run this script as N ranks (one per GPU) under
+    torch.distributed.run on 127.0.0.1.  Fails loudly if fewer than N GPUs are visible."""
+    if not args.launcher_dry_run:
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) are visible", file=sys.stderr)
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def launcher_dry_run(world, rank):
+    """Each spawned rank joins a gloo group and reports itself; rank 0 prints one JSON line."""
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo")
+    got = [None] * world
+    dist.all_gather_object(got, {"rank": rank, "local_rank": int(os.environ.get("LOCAL_RANK", "0")),
+                                 "pid": os.getpid()})
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "world_size": dist.get_world_size(),
+                          "ranks": [g["rank"] for g in got], "local_ranks": [g["local_rank"] for g in got],
+                          "distinct_pids": len({g["pid"] for g in got}), "torch": torch.__version__}), flush=True)
+    dist.destroy_process_group()
+    return 0
 
 
 # ----------------------------------------------------------------------------- clocks sampling
@@ -127,45 +181,99 @@ def ncu_traffic(name):
 
 
 # ----------------------------------------------------------------------------- CPU oracle timing
-def cpu_oracle_rate(wname, seconds, steps=None):
-    """Oracle (oracle.sweep_rows) on a bounded row sample of the workload, on all host
-    cores (rows split over threads; ctypes releases the GIL).  Returns (it/s, cores, sample)."""
+def cpu_oracle_full(wname, seconds, A=None, b=None, sweeps=None):
+    """The oracle as it stands (oracle.jacobi, its own row-parallel threads) over the
+    WHOLE system of the workload, on all host cores of this process.  Runs `sweeps` sweeps (or as many
+    of the workload's sweeps as fit in about `seconds`, sized by a first 1-sweep call).  A, b: the host
+    system if the caller already holds it (the e2e leg does); else it is generated here.
+    Returns a dict: it/s of the whole oracle call (validation pass included), the per-sweep time net of
+    that pass (oracle.jacobi with max_iter = 0 is the validation alone), cores and the sample."""
     import jacobi_gen as g
     import oracle
     cfg = g.CONFIGS[WORKLOADS[wname][0]]
-    n = cfg.n
+    total_sweeps = WORKLOADS[wname][1]
     cores = len(os.sched_getaffinity(0))
-    rows = min(n, max(cores * 64, 4096 if n >= 65536 else n))
-    A, b = g.host_rows(cfg, 0, rows)
-    x = g.host_xstar(cfg) * 0.5  # any x^(k-1); the work per row is data independent
-    chunks = np.array_split(np.arange(rows), cores)
-
-    def one_pass():
-        out = [None] * len(chunks)
-
-        def run(t):
-            idx = chunks[t]
-            if len(idx):
-                out[t] = oracle.sweep_rows(A[idx[0]: idx[-1] + 1], int(idx[0]), b[idx[0]: idx[-1] + 1], x)
-
-        th = [threading.Thread(target=run, args=(t,)) for t in range(len(chunks))]
-        for t in th:
-            t.start()
-        for t in th:
-            t.join()
-
-    one_pass()  # warm
+    t_gen = 0.0
+    if A is None:
+        t0 = time.perf_counter()
+        A, b = g.host_rows(cfg, 0, cfg.n)
+        t_gen = time.perf_counter() - t0
     t0 = time.perf_counter()
-    passes = 0
-    while True:
-        one_pass()
-        passes += 1
+    oracle.jacobi(A, b, None, 0, 0.0, nthreads=cores)  # validation pass alone (EZERODIAG/ENONFINITE scan)
+    t_val = time.perf_counter() - t0
+    if sweeps is None:
+        t0 = time.perf_counter()
+        oracle.jacobi(A, b, None, 1, 0.0, nthreads=cores)
+        t1 = time.perf_counter() - t0
+        sweeps = int(max(1, min(total_sweeps, seconds // max(t1, 1e-6))))
+    t0 = time.perf_counter()
+    st, x, it = oracle.jacobi(A, b, None, sweeps, 0.0, nthreads=cores)
+    el = time.perf_counter() - t0
+    assert it == sweeps, (st, it)
+    per_sweep = max(el - t_val, 1e-9) / sweeps
+    return {"value": sweeps / el, "unit": "it/s", "cores": cores, "kind": "oracle",
+            "sample": (f"oracle.jacobi(nthreads={cores}) on the whole {wname} system (n={cfg.n}), {sweeps} of its "
+                       f"{total_sweeps} fixed sweeps in {el:.2f} s (validation pass {t_val:.2f} s included); "
+                       f"it/s = sweeps / time"),
+            "per_sweep_s": per_sweep, "sweeps": sweeps, "seconds": el, "validation_s": t_val,
+            "gen_s": t_gen if t_gen else None}
+
+
+def cpu_oracle_t1(configs=("c1", "c2", "c3"), seconds=2.0):
+    """One-thread oracle per-sweep time of the small configs (T = 1 for c1-c3)."""
+    import jacobi_gen as g
+    import oracle
+    out = {}
+    for name in configs:
+        cfg = g.CONFIGS[name]
+        A, b = g.host_rows(cfg, 0, cfg.n)
+        t0 = time.perf_counter()
+        oracle.jacobi(A, b, None, 1, 0.0, nthreads=1)
+        t1 = time.perf_counter() - t0
+        k = int(max(1, min(200, seconds // max(t1, 1e-6))))
+        t0 = time.perf_counter()
+        oracle.jacobi(A, b, None, k, 0.0, nthreads=1)
         el = time.perf_counter() - t0
-        if (steps is not None and passes >= steps) or (steps is None and el >= seconds):
-            break
-    rate = passes * rows / n / el
-    sample = f"oracle.sweep_rows over rows [0,{rows}) of {n} x {passes} passes in {el:.2f}s; it/s = passes*rows/n/t"
-    return rate, cores, sample, el
+        out[name] = {"n": cfg.n, "sweeps": k, "seconds": el, "per_sweep_s": el / k, "it_per_s": k / el,
+                     "threads": 1}
+        del A
+    return out
+
+
+def reference_arm(args, rank):
+    """--impl reference: the CPU oracle as it stands on the host cores (rank 0 only under torchrun);
+    each step = args.ref_sweeps sweeps of oracle.jacobi over the WHOLE workload system."""
+    if rank != 0:
+        return 0
+    import jacobi_gen as g
+    gname, sweeps, tol, desc = WORKLOADS[args.workload]
+    cfg = g.CONFIGS[gname]
+    t0 = time.perf_counter()
+    A, b = g.host_rows(cfg, 0, cfg.n)
+    t_gen = time.perf_counter() - t0
+    for _ in range(args.warmup):
+        cpu_oracle_full(args.workload, 0, A, b, sweeps=args.ref_sweeps)
+    els = []
+    cb = None
+    for _ in range(args.steps):
+        cb = cpu_oracle_full(args.workload, 0, A, b, sweeps=args.ref_sweeps)
+        els.append(cb["seconds"])
+    el = sum(els)
+    rate = args.steps * args.ref_sweeps / el
+    cb.update(value=rate, seconds=el, gen_s=t_gen,
+              sample=(f"{args.steps} steps x oracle.jacobi(nthreads={cb['cores']}) over the whole {gname} system "
+                      f"(n={cfg.n}), {args.ref_sweeps} of its {sweeps} sweeps per step (validation pass each call)"))
+    line = {"impl": "reference", "metric": "Jacobi iterations/s", "value": rate, "unit": "it/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded counter-based generator, host)",
+            "config": {"workload": desc, "n": cfg.n, "sweeps_per_step": args.ref_sweeps,
+                       "note": "reference step = a bounded sample of the workload's sweeps (the GPU arm's step is "
+                               "all of them); it/s is the comparable quantity"},
+            "cpu_baseline": cb,
+            "e2e": {"value": rate, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
 
 
 # ----------------------------------------------------------------------------- other configs (N = 1)
@@ -214,32 +322,105 @@ def other_configs(jb, g, torch, stream):
     return out
 
 
+# ----------------------------------------------------------------------------- fused exchange (N > 1 side leg)
+def fused_exchange_leg(jb, torch, dist, dA, db, dx0, dxo, n, sh, stream, sweeps, steps, K, rank, world,
+                       planted_ok):
+    """Times the fused NVLink push exchange (NEXT-1) on the same row blocks.
+    Every stage that can fail on one rank alone ends in a vote (MIN all-reduce of an ok flag) that every
+    rank reaches, so a failure becomes a reported error, not a hang; hangs inside NCCL are covered by
+    the caller's watchdog.  Returns a dict for the JSON line."""
+    from paper_1403_5805_b200.dist import bootstrap
+
+    def vote(ok):
+        f = torch.tensor([1 if ok else 0], device="cuda")
+        dist.all_reduce(f, op=dist.ReduceOp.MIN)
+        return bool(int(f.item()))
+
+    plan = None
+    try:
+        uid, _, _, _, _ = bootstrap(n)  # torch.distributed broadcast: every rank enters
+        err = None
+        try:
+            plan = jb.Plan(dA, n=n, stream=sh, dist=(uid, rank, world))
+        except Exception as ex:  # noqa: BLE001
+            err = f"plan: {ex}"
+        if not vote(err is None):
+            return {"error": err or "plan creation failed on another rank"}
+        mine = None
+        try:
+            mine = plan.ipc_export()
+        except Exception as ex:  # noqa: BLE001
+            err = f"ipc_export: {ex}"
+        allh = [None] * world
+        dist.all_gather_object(allh, mine)
+        if err is None and any(h is None for h in allh):
+            err = "ipc_export failed on another rank"
+        if err is None:
+            try:
+                plan.ipc_attach(b"".join(allh))
+                plan.set_batch(K)
+            except Exception as ex:  # noqa: BLE001
+                err = f"ipc_attach: {ex}"
+        if not vote(err is None):
+            return {"error": err or "ipc attach failed on another rank"}
+        for i in range(3):  # warm-up solves, one vote after each (every rank enters every solve)
+            ok = True
+            try:
+                r = plan.solve_device(db, dx0, dxo, sweeps, 0.0)
+                ok = r.iters == sweeps and r.status == jb.MAX_ITER and planted_ok()
+            except Exception as ex:  # noqa: BLE001
+                err, ok = f"warm-up solve: {ex}", False
+            if not vote(ok):
+                return {"error": err or "warm-up solve failed or wrong on some rank"}
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        ok = True
+        try:
+            for _ in range(steps):
+                plan.solve_device(db, dx0, dxo, sweeps, 0.0)
+        except Exception as ex:  # noqa: BLE001
+            err, ok = f"timed solve: {ex}", False
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if not vote(ok):
+            return {"error": err or "timed solve failed on some rank"}
+        t = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        inf = plan.info
+        its = steps * sweeps / (ms * 1e-3)
+        return {"value": its, "unit": "it/s", "ms_per_step": ms / steps, "steps": steps,
+                "effective_gbs_per_gpu": inf.bytes_per_sweep * its / 1e9,
+                "kernel": jb.variant_name(inf.variant),
+                "what": "row blocks, the sweep kernel pushes x_i^(k) into every rank's buffer over NVLink and "
+                        "signals arrival counters (no NCCL per sweep); planted-solution check passed"}
+    finally:
+        if plan is not None:
+            try:
+                plan.close()
+            except Exception:  # noqa: BLE001
+                pass
+
+
 # ----------------------------------------------------------------------------- main (GPU arm)
 def main():
     args = parse()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None and args.gpus > 1 and args.impl == "cuda":
+        return launch_ranks(args)
+    world = int(world_env or "1")
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    gname, sweeps, tol, desc = WORKLOADS[args.workload]
-
+    if args.launcher_dry_run:
+        return launcher_dry_run(world, rank)
     if args.impl == "reference":
-        if rank != 0:
-            return 0
-        per_step = []
-        rate, cores, sample, el = cpu_oracle_rate(args.workload, None, steps=1)  # warm-up + sizing
-        for _ in range(args.warmup):
-            cpu_oracle_rate(args.workload, None, steps=1)
-        t0 = time.perf_counter()
-        rate, cores, sample, el = cpu_oracle_rate(args.workload, None, steps=args.steps)
-        line = {"impl": "reference", "metric": "Jacobi iterations/s", "value": rate, "unit": "it/s",
-                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": desc, "n": 65536 if gname == "c4" else None, "sweeps_per_step": sweeps},
-                "cpu_baseline": {"value": rate, "unit": "it/s", "cores": cores, "kind": "oracle", "sample": sample},
-                "e2e": {"value": rate, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
-        return 0
+        return reference_arm(args, rank)
+    if world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+        return 2
+    gname, sweeps, tol, desc = WORKLOADS[args.workload]
 
     import torch
     import torch.distributed as dist
@@ -247,6 +428,9 @@ def main():
     import jacobi_gen as g
     import paper_1403_5805_b200 as jb
 
+    if torch.cuda.device_count() <= local:
+        print(f"bench.py: rank {rank} needs CUDA device {local}; {torch.cuda.device_count()} visible", file=sys.stderr)
+        return 2
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -261,11 +445,6 @@ def main():
     row0, m = jb.partition(n, world, rank)
 
     # ---- resident inputs (device twin of the generator; identical bits to the host generator)
-    if world > 1 and args.exchange == "auto":
-        ok = all(torch.cuda.can_device_access_peer(local, q) for q in range(world) if q != local)
-        flag = torch.tensor([1 if ok else 0], device="cuda")
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)  # every rank takes the same decision
-        args.exchange = "p2p" if int(flag.item()) else "nccl"
     cols = world > 1 and args.exchange == "cols"
     db = torch.empty(m, dtype=torch.float64, device="cuda")
     if cols:  # column slab [row0, row0 + m) of all n rows: generate all rows, keep the slab
@@ -275,29 +454,24 @@ def main():
         for r in range(0, n, 4096):
             g.device_rows(cfg, r, min(n, r + 4096), tmp.data_ptr(), n, tb.data_ptr(), sh)
             dA[r:r + 4096].copy_(tmp[: min(4096, n - r), row0:row0 + m])
-            if row0 <= r < row0 + m or r <= row0 < r + 4096:
-                lo, hi = max(r, row0), min(r + 4096, row0 + m)
-                if lo < hi:
-                    db[lo - row0:hi - row0].copy_(tb[lo - r:hi - r])
+            lo, hi = max(r, row0), min(r + 4096, row0 + m)
+            if lo < hi:
+                db[lo - row0:hi - row0].copy_(tb[lo - r:hi - r])
         del tmp, tb
     else:
         dA = torch.empty((m, n), dtype=dt, device="cuda")
         g.device_rows(cfg, row0, row0 + m, dA.data_ptr(), n, db.data_ptr(), sh)
     dx0 = torch.zeros(n, dtype=torch.float64, device="cuda")
     dxo = torch.empty(n, dtype=torch.float64, device="cuda")
+    xs_dev = torch.empty(n, dtype=torch.float64, device="cuda")
+    g.device_xstar(cfg, xs_dev.data_ptr(), sh)
     torch.cuda.synchronize()
     K = 20 if sweeps % 20 == 0 else 4  # 100 sweeps = 5 graph batches exactly: no no-op overshoot launches
-    plan = None
-
-    def step():
-        return plan.solve_device(db, dx0, dxo, sweeps, tol)
 
     def local_planted_error():
-        """max |x - x*| on this rank after the warm-up solves (BASELINE.json: b = A x*, so the
-        fixed-iteration configs end at x* to ~1e-16): a cheap end-to-end check of the exchange."""
-        xs = torch.empty(n, dtype=torch.float64, device="cuda")
-        g.device_xstar(cfg, xs.data_ptr(), sh)
-        return float((dxo - xs).abs().max().item())
+        """max |x - x*| on this rank after a solve (BASELINE.json: b = A x*, so the fixed-iteration
+        configs end at x* to ~1e-16): a cheap end-to-end check of the exchange."""
+        return float((dxo - xs_dev).abs().max().item())
 
     def planted_error():  # max over ranks
         e = torch.tensor([local_planted_error()], dtype=torch.float64, device="cuda")
@@ -305,41 +479,18 @@ def main():
             dist.all_reduce(e, op=dist.ReduceOp.MAX)
         return float(e.item())
 
-    if world > 1 and args.exchange == "p2p":
-        # The fused exchange is validated with emulated ranks only: any error on any rank (IPC attach,
-        # a bounded peer wait that faulted) or a wrong result (planted-solution check) makes every rank
-        # fall back to the NCCL exchange together.  No collective runs between here and the vote.
+    if world > 1:
         from paper_1403_5805_b200.dist import dist_plan
-        ok = 1
-        try:
-            plan = dist_plan(dA, n, stream=sh, p2p=True)
-            plan.set_batch(K)
-            for _ in range(max(3, args.warmup)):
-                r = step()
-            ok = int(r.iters == sweeps and r.status == jb.MAX_ITER and (tol != 0.0 or local_planted_error() <= 1e-10))
-        except Exception as ex:  # noqa: BLE001 - any failure of the opt-in path means "fall back"
-            print(f"bench: rank {rank}: fused exchange failed ({ex})", file=sys.stderr)
-            ok = 0
-        flag = torch.tensor([ok], device="cuda")
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-        if not int(flag.item()):
-            print("bench: fused exchange unusable on some rank; using the NCCL exchange", file=sys.stderr)
-            if plan is not None:
-                try:
-                    plan.close()
-                except Exception:  # noqa: BLE001
-                    pass
-            plan = None
-            args.exchange = "nccl"
-    if plan is None:
-        if world > 1:
-            from paper_1403_5805_b200.dist import dist_plan
-            plan = dist_plan(dA, n, stream=sh, layout="cols" if cols else "rows")
-        else:
-            plan = jb.Plan(dA, n=n, stream=sh)
-        plan.set_batch(K)
-        for _ in range(max(3, args.warmup)):
-            r = step()
+        plan = dist_plan(dA, n, stream=sh, layout="cols" if cols else "rows", p2p=args.exchange == "p2p")
+    else:
+        plan = jb.Plan(dA, n=n, stream=sh)
+    plan.set_batch(K)
+
+    def step():
+        return plan.solve_device(db, dx0, dxo, sweeps, tol)
+
+    for _ in range(max(3, args.warmup)):
+        r = step()
     assert r.iters == sweeps and r.status == jb.MAX_ITER
     planted = planted_error() if tol == 0.0 else None  # reported: the solve reached x*
     info = plan.info
@@ -372,22 +523,76 @@ def main():
     # per-kernel timing (untimed cross-check: events around each sweep kernel alone)
     kms = plan.time_sweeps(db, dx0, min(sweeps, 20))
     kernel_ms = float(np.median(kms[1:])) if len(kms) > 1 else float(kms[0])
+    if world > 1:
+        t = torch.tensor([kernel_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        kernel_ms = float(t.item())
 
     ceiling = None
     if rank == 0:
         try:
             ceiling = jb.bwprobe(min(32 << 30, int(bytes_sweep)), 5)
-        except Exception:
+        except Exception:  # noqa: BLE001
             ceiling = None
-
     plan.close()
+
+    line = {
+        "metric": "Jacobi iterations/s", "value": its, "unit": "it/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded counter-based generator, BASELINE.json recipe; device twin)",
+        "config": {"workload": desc, "n": n, "sweeps_per_step": sweeps, "tol": tol,
+                   "parallelism": (f"row-block x{world}" if not cols else f"column-slab x{world}") + (
+                       {"nccl": " + NCCL allgather/allreduce", "p2p": " + fused NVLink push exchange (NEXT-1)",
+                        "cols": " + NCCL reduce-scatter/allreduce (NEXT-4)"}[args.exchange] if world > 1 else ""),
+                   "l2": "A per GPU >> 126 MB L2; each sweep streams A from HBM (no flush needed)",
+                   "graph_batch": K, "chunk_cols": info.chunk_cols, "rows_per_warp": info.rows_per_warp,
+                   "grid": f"{info.grid_ctas}x{info.threads_per_cta}"},
+        "effective_gbs_per_gpu": achieved, "effective_gbs_aggregate": achieved * world,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": ncu_traffic(args.workload),
+                     "peak_source": peak_src,
+                     "kernel": f"{jb.variant_name(info.variant)} ({'fp64' if dt == torch.float64 else 'fp32'} A)",
+                     "bytes_per_launch": bytes_sweep, "avg_launch_ms": sweep_ms,
+                     "kernel_only_ms": kernel_ms, "kernel_only_gbs": bytes_sweep / (kernel_ms * 1e-3) / 1e9,
+                     "read_ceiling_gbs": ceiling,
+                     "frac_of_read_ceiling": (achieved / ceiling) if ceiling else None,
+                     "frac_of_8tbs": achieved / 8000.0},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "cpu_baseline": None,
+        "e2e": None,
+        "other_configs": None,
+        "check": {"planted_max_abs_err": planted,
+                  "what": "max_i |x_i - x*_i| after the warm-up solves (b = A x*), max over ranks"},
+    }
+
+    # ---- N > 1: the fused NVLink exchange as a side measurement, under a watchdog
+    if world > 1 and args.exchange == "nccl" and not args.no_fused and not cols:
+        done = threading.Event()
+
+        def watchdog():
+            if not done.wait(args.fused_timeout):
+                if rank == 0:
+                    line["fused_exchange"] = {"error": f"watchdog: no result within {args.fused_timeout:.0f} s"}
+                    print(json.dumps(line), flush=True)
+                os._exit(0)
+
+        threading.Thread(target=watchdog, daemon=True).start()
+        try:
+            line["fused_exchange"] = fused_exchange_leg(
+                jb, torch, dist, dA, db, dx0, dxo, n, sh, stream, sweeps, args.steps, K, rank, world,
+                lambda: local_planted_error() <= 1e-10)
+        except Exception as ex:  # noqa: BLE001
+            line["fused_exchange"] = {"error": str(ex)}
+        done.set()
     del dA, db
     torch.cuda.empty_cache()
 
     # ---- e2e through the public C-ABI with host buffers (pinned), copies inside the timed region.
     # N = 1: the one-shot jacobi_solve (north-star signature).  N > 1: per step every rank creates a
     # distributed plan from its host row block (H2D inside), solves from host b / x0 and reads x back.
-    e2e = None
+    hA = None
     if not args.no_e2e and args.e2e_steps > 0:
         import ctypes
         hA = torch.empty((m, n), dtype=dt, pin_memory=True)
@@ -423,60 +628,35 @@ def main():
             t = torch.tensor([el], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
-        e2e = {"value": args.e2e_steps * sweeps / el, "unit": "it/s",
-               "h2d_bytes_per_step": int(world * (hA.numel() * hA.element_size() + 8 * m + 8 * n)),
-               "d2h_bytes_per_step": int(world * (8 * n + 48)), "steps": args.e2e_steps,
-               "api": ("jacobi_solve (C-ABI one-shot, host pinned buffers: plan setup + H2D + sweeps + D2H per step)"
-                       if world == 1 else
-                       "jacobi_dist_plan_create + jacobi_plan_solve per step on every rank (host row block, H2D, "
-                       "NCCL comm init, sweeps, D2H); wall time, max over ranks")}
-        del hA
+        line["e2e"] = {"value": args.e2e_steps * sweeps / el, "unit": "it/s",
+                       "h2d_bytes_per_step": int(world * (hA.numel() * hA.element_size() + 8 * m + 8 * n)),
+                       "d2h_bytes_per_step": int(world * (8 * n + 48)), "steps": args.e2e_steps,
+                       "api": ("jacobi_solve (C-ABI one-shot, host pinned buffers: plan setup + H2D + sweeps + D2H "
+                               "per step)" if world == 1 else
+                               "jacobi_dist_plan_create + jacobi_plan_solve per step on every rank (host row block, "
+                               "H2D, NCCL comm init, sweeps, D2H); wall time, max over ranks")}
 
-    configs = None
     if world == 1 and not args.no_configs:
-        configs = other_configs(jb, g, torch, stream)
+        line["other_configs"] = other_configs(jb, g, torch, stream)
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, cores, sample, _ = cpu_oracle_rate(args.workload, args.cpu_seconds)
-        cpu = {"value": rate, "unit": "it/s", "cores": cores, "kind": "oracle", "sample": sample}
+    # ---- CPU oracle on rank 0's host cores (every N); reuses the e2e host A when it is the whole system
+    if rank == 0 and not args.no_cpu_baseline:
+        whole = hA is not None and m == n
+        cb = cpu_oracle_full(args.workload, args.cpu_seconds, hA.numpy() if whole else None,
+                             g.host_diag_b(cfg, 0, n)[1] if whole else None)
+        hA = None
+        cb["t1"] = cpu_oracle_t1()
+        line["cpu_baseline"] = cb
+    hA = None
 
     if rank == 0:
-        line = {
-            "metric": "Jacobi iterations/s", "value": its, "unit": "it/s", "n_gpus": world,
-            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded counter-based generator, BASELINE.json recipe; device twin)",
-            "config": {"workload": desc, "n": n, "sweeps_per_step": sweeps, "tol": tol,
-                       "parallelism": (f"row-block x{world}" if not cols else f"column-slab x{world}") + (
-                           {"nccl": " + NCCL allgather/allreduce", "p2p": " + fused NVLink push exchange (NEXT-1)",
-                            "cols": " + NCCL reduce-scatter/allreduce (NEXT-4)"}[args.exchange] if world > 1 else ""),
-                       "l2": "A per GPU >> 126 MB L2; each sweep streams A from HBM (no flush needed)",
-                       "graph_batch": K, "chunk_cols": info.chunk_cols, "rows_per_warp": info.rows_per_warp,
-                       "grid": f"{info.grid_ctas}x{info.threads_per_cta}"},
-            "effective_gbs_per_gpu": achieved, "effective_gbs_aggregate": achieved * world,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(args.workload),
-                         "peak_source": peak_src, "kernel": f"{jb.variant_name(info.variant)} ({'fp64' if dt == torch.float64 else 'fp32'} A)",
-                         "bytes_per_launch": bytes_sweep, "avg_launch_ms": sweep_ms,
-                         "kernel_only_ms": kernel_ms, "kernel_only_gbs": bytes_sweep / (kernel_ms * 1e-3) / 1e9,
-                         "read_ceiling_gbs": ceiling,
-                         "frac_of_read_ceiling": (achieved / ceiling) if ceiling else None,
-                         "frac_of_8tbs": achieved / 8000.0},
-            "gpu_launches": int(launches),
-            "clocks": clk.summary(),
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "other_configs": configs,
-            "check": {"planted_max_abs_err": planted,
-                      "what": "max_i |x_i - x*_i| after the warm-up solves (b = A x*), max over ranks"},
-        }
         s = json.dumps(line)
         print(s, flush=True)
         if args.out:
             with open(args.out, "a") as f:
                 f.write(s + "\n")
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
     return 0
 

@@ -19,7 +19,7 @@
  *       rows into every peer's buffer over NVLink and signals their arrival counters (§3.3 one-sided
  *       puts; overlapping transfer and compute).
  *   Single-GPU solver path (chosen per plan from measured crossovers, same results bit for bit):
- *       small n: one thread-block-cluster launch with A in shared memory; mid-size A (<= 200 MB
+ *       small n: one thread-block-cluster launch with A in shared memory; mid-size A (<= 148 MB
  *       fp64 / 300 MB fp32): persistent cooperative launches with a grid barrier per sweep; larger
  *       A: CUDA graphs of sweep kernels.  jacobi_plan_info reports which.
  *
@@ -33,7 +33,9 @@
  *     (it is copied only when its pointer is not 32-byte aligned or lda is not a multiple of 8).
  *     The library owns its own device allocations and frees them in jacobi_plan_destroy (or before
  *     jacobi_solve returns).
- *   - Outputs (x_out, iters_out, dist_hist) are written only when the status is >= 0.
+ *   - Outputs (x_out, iters_out, dist_hist) are written only when the status is >= 0 — except the
+ *     DEVICE history of jacobi_plan_solve_device, which the kernels fill while the solve runs
+ *     (d_dist_hist[k-1] once d_k is known), so a failed device solve may leave it partly written.
  *   - Validation order: JACOBI_EINVAL (n < 1, NULL pointer, lda < n, max_iter < 0, tol < 0 or NaN,
  *     bad dtype) before any CUDA call; then JACOBI_EINDIVISIBLE (distributed, P does not divide n);
  *     then JACOBI_EZERODIAG (lowest i, across ranks); then JACOBI_ENONFINITE (any non-finite value
@@ -100,7 +102,9 @@ int jacobi_plan_create(jacobi_plan** out, int64_t n, int dtype, const void* A, i
 int jacobi_plan_solve(jacobi_plan* plan, const double* b, const double* x0, int64_t max_iter, double tol,
                       double* x_out, int64_t* iters_out, double* dist_hist);
 /* Same contract with DEVICE pointers (b, x0, x_out, dist_hist on the plan's device); only the
- * 48-byte stop state crosses PCIe.  x_out may alias x0. */
+ * 48-byte stop state crosses PCIe.  x_out may alias x0.  d_dist_hist (nullable) must hold max_iter
+ * doubles — the library cannot check a device pointer's extent (the Python binding does) — and is
+ * written by the kernels during the solve (see Outputs above). */
 int jacobi_plan_solve_device(jacobi_plan* plan, const double* d_b, const double* d_x0, int64_t max_iter,
                              double tol, double* d_x_out, int64_t* iters_out, double* d_dist_hist);
 void jacobi_plan_destroy(jacobi_plan* plan);

@@ -266,7 +266,12 @@ class Plan:
         return SolveResult(st, x, it.value, hist[: it.value] if history else None)
 
     def solve_device(self, b, x0, x_out, max_iter=100, tol=0.0, hist=None):
-        """Device-pointer solve on torch CUDA tensors (results written into x_out / hist)."""
+        """Device-pointer solve on torch CUDA tensors (results written into x_out / hist).  hist
+        (optional) needs max(max_iter, 1) float64 elements: the kernels write d_k into it while the
+        solve runs (jacobi.h), so a short tensor would be written past its end."""
+        if hist is not None and (not _is_torch_cuda(hist) or hist.numel() < max(int(max_iter), 1)):
+            raise ValueError(f"hist must be a CUDA tensor with at least max(max_iter, 1) = {max(int(max_iter), 1)} "
+                             "elements")
         it = ctypes.c_int64(-1)
         st = _check(_lib.jacobi_plan_solve_device(
             self._h, _dev_ptr(b, self._rows, "b"), _dev_ptr(x0, self.n, "x0"), int(max_iter), float(tol),

@@ -59,8 +59,13 @@ struct SweepArgs {
   double* x1buf;
   double* part;             // partial row sums, part[c * m + r]
   unsigned* cnt;            // per row-tile arrival counters (reset by the finalizing warp)
-  unsigned* dyn;            // dynamic tile assignment (variants with DYN): sweep k takes tiles from
-                            // dyn[k & 3]; zeroed by k_prepare and, one sweep ahead, by CTA 0
+  unsigned* dyn;            // dynamic tile assignment (variants with DYN): dyn[0] is the launch's
+                            // tile-claim counter, dyn[1] counts CTAs that finished their claims; the
+                            // last CTA to finish resets both for the next launch (k_prepare zeroes
+                            // them per solve).  This needs every CTA of a launch to reach the end of
+                            // cta_sweep, i.e. all CTAs agree on s_go (they read the same stop state:
+                            // the bounds-checked build checks, in the last CTA, that the claims
+                            // add up to ncta * 4 + tiles, i.e. the launch began from zero)
   unsigned long long* dslot;// 4-slot ring of max|dx| bit patterns; sweep k uses slot k & 3
   State* st;
   int64_t col0, cend;       // column range of A held here: [0, n) row-wise; a slab column-wise (NEXT-4)
@@ -100,7 +105,6 @@ cudaError_t launch_copy_pitched(int dtype, const void* src, int64_t src_ld, void
 int num_variants();
 const char* variant_name(int variant);
 int default_variant(int dtype, int nchunks, int chunk, bool l2_keep, int64_t rows, int num_sms);
-bool variant_uses_l2_keep(int variant);
 bool variant_is_cta(int variant);
 bool variant_is_push(int variant);
 int push_variant();

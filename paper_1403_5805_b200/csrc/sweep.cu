@@ -563,11 +563,18 @@ __device__ __forceinline__ unsigned long long cta_sweep(const SweepArgs& a, cons
     if (t >= 1 && (t - 1) % NW == w) finalize(t - 1);
   }
   if (t >= 1 && (t - 1) % NW == w) finalize(t - 1);  // t = tiles processed
-  if constexpr (DYN)  // the launch's last CTA resets the counters for the next launch (all claims are done)
+  if constexpr (DYN) {  // the launch's last CTA resets the counters for the next launch (all claims are done)
+#ifdef JACOBI_BOUNDS_CHECK
+    if (threadIdx.x == 0) __threadfence();  // this CTA's claims before its finish count (checked build)
+#endif
     if (threadIdx.x == 0 && atomicAdd(a.dyn + 1, 1u) == (unsigned)ncta - 1u) {
+      // Every CTA claimed kSlots tiles up front and one more per tile it processed, so a launch that
+      // started from a zero counter and dealt every tile once ends at ncta * kSlots + tiles (bit 6).
+      JB_CHECK(atomicAdd(a.dyn, 0u) == (unsigned)ncta * kSlots + (unsigned)a.tiles, 6);
       a.dyn[0] = 0u;
       a.dyn[1] = 0u;
     }
+  }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     const unsigned long long o = __shfl_xor_sync(kFull, dmax, off);
@@ -1212,8 +1219,11 @@ const Variant kVariants[] = {
     {"k_sweep_cta R4 U2", 4, 512, 1, 4, 2, 2, k_sweep_cta<double, 4, 16, 2>, k_sweep_cta<float, 4, 16, 2>},
     {"k_sweep_cta R2 U4", 2, 512, 1, 2, 4, 2, k_sweep_cta<double, 2, 16, 4>, k_sweep_cta<float, 2, 16, 2>},
     // fused-exchange (NEXT-1) instances of the defaults; selected only by jacobi_plan_ipc_attach /
-    // jacobi_plan_set_p2p_emulation (they need SweepArgs.peers)
-    {"k_sweep_cta R4 U1 fused-exchange", 4, 512, 2, 4, 1, 1, k_sweep_cta<double, 4, 16, 1, 0, true>, k_sweep_cta<float, 4, 16, 1, 0, true>},
+    // jacobi_plan_set_p2p_emulation (they need SweepArgs.peers).  x^(k-1) is read with weak
+    // (L1-cacheable) loads, XL = 3, never ld.global.nc: peers store into it over NVLink while this
+    // kernel may already be resident (spinning in sweep_prologue); the prologue's ld.acquire.sys of
+    // the arrival counter plus the CTA barrier order those stores before every load of the sweep.
+    {"k_sweep_cta R4 U1 fused-exchange", 4, 512, 2, 4, 1, 1, k_sweep_cta<double, 4, 16, 1, 3, true>, k_sweep_cta<float, 4, 16, 1, 3, true>},
     // row-panel kernel (cta = 3): warps own whole rows, x chunks shared through L1
     {"k_sweep_panel R4 U1", 4, 512, 3, 4, 1, 1, k_sweep_panel<double, 4, 16>, k_sweep_panel<float, 4, 16>},
     {"k_sweep_panel R4 U1 x-evict_last", 4, 512, 3, 4, 1, 1, k_sweep_panel<double, 4, 16, 1, 1>, k_sweep_panel<float, 4, 16, 1, 1>},
@@ -1227,7 +1237,7 @@ const Variant kVariants[] = {
     {"k_sweep_panel R4 U1 x-smem L2-keep", 4, 512, 4, 4, 1, 1, k_sweep_panel<double, 4, 16, 1, 0, true, 8>, k_sweep_panel<float, 4, 16, 1, 0, true, 8>},
     // CTA kernel R = 8 (fp64; the fp32 instances keep R = 4, R = 8 spills): L2-keep and fused exchange
     {"k_sweep_cta R8 U1 L2-policy", 8, 512, 1, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, false, true>, k_sweep_cta<float, 4, 16, 1, 0, false, true>},
-    {"k_sweep_cta R8 U1 fused-exchange", 8, 512, 2, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, true, true>, k_sweep_cta<float, 4, 16, 1, 0, true>},
+    {"k_sweep_cta R8 U1 fused-exchange", 8, 512, 2, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 3, true, true>, k_sweep_cta<float, 4, 16, 1, 3, true>},
     // CTA kernel R8 L2-policy with (chunk, row group) units: balanced when nchunks is not a multiple of 16
     {"k_sweep_cta R8 U1 L2-policy rows/2", 8, 512, 1, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, false, true, 2>, k_sweep_cta<float, 4, 16, 1, 0, false, true, 2>},
     {"k_sweep_cta R8 U1 L2-policy rows/4", 8, 512, 1, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, false, true, 4>, k_sweep_cta<float, 4, 16, 1, 0, false, true, 4>},
@@ -1304,7 +1314,6 @@ int default_variant(int dtype, int nchunks, int chunk, bool l2_keep, int64_t row
   if (variant_fits(big, nchunks, dtype, chunk)) return big;
   return dtype == JACOBI_F32 ? 0 : 1;  // U = 1: fits every chunk
 }
-bool variant_uses_l2_keep(int v) { return v == 16 || v == 17 || v == 19 || v == 20; }
 int variant_rows(int v) { return kVariants[v].R; }
 int variant_threads(int v) { return kVariants[v].threads; }
 

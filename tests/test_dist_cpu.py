@@ -49,6 +49,38 @@ def _worker(rank, world, port, q):
         except jb.JacobiError as e:
             out["indiv"] = e.status
 
+        # the library's distributed plan entry points, world_size 2 (no GPU here): argument validation
+        # before any CUDA call, EINDIVISIBLE on every rank, and ECUDA — never a CPU fallback — once the
+        # arguments are valid (paper_1403_5805_b200.dist.dist_plan -> jacobi_dist_plan_create)
+        import ctypes
+        from paper_1403_5805_b200.dist import dist_plan
+        blk = np.eye(96)[row0:row0 + rows] * 2.0
+        try:
+            dist_plan(np.zeros((rows + 1, 96)), 96)
+            out["shape"] = None
+        except ValueError as e:
+            out["shape"] = "ValueError" if "rows" in str(e) else str(e)
+        try:
+            dist_plan(np.eye(97)[:48], 97)
+            out["dp_indiv"] = None
+        except jb.JacobiError as e:
+            out["dp_indiv"] = e.status
+        try:
+            dist_plan(blk, 96)
+            out["dp_nogpu"] = None
+        except jb.JacobiError as e:
+            out["dp_nogpu"] = e.status
+        h = ctypes.c_void_p()
+        ub = ctypes.create_string_buffer(bytes(uid), 128)
+        out["einval"] = [
+            jb._lib.jacobi_dist_plan_create(ctypes.byref(h), ub, 2, 2, 96, jb.F64, blk.ctypes.data, 96, 0, None),
+            jb._lib.jacobi_dist_plan_create(ctypes.byref(h), None, r, w, 96, jb.F64, blk.ctypes.data, 96, 0, None),
+            jb._lib.jacobi_dist_plan_create(ctypes.byref(h), ub, r, w, 96, 7, blk.ctypes.data, 96, 0, None),
+            jb._lib.jacobi_dist_plan_create(ctypes.byref(h), ub, r, w, 96, jb.F64, blk.ctypes.data, 95, 0, None),
+            jb._lib.jacobi_dist_plan_create_colwise(ctypes.byref(h), ub, r, w, 100, jb.F64, blk.ctypes.data, 100, 0,
+                                                    None),
+        ]
+
         # distributed Jacobi protocol with the oracle as the per-rank compute
         rng = np.random.default_rng(5)
         n = 96
@@ -119,6 +151,22 @@ def test_bootstrap_uid_and_partition(results):
     assert results[0]["uid"] == results[1]["uid"] and len(results[0]["uid"]) == 128
     assert results[0]["part"] == (0, 2, 0, 48) and results[1]["part"] == (1, 2, 48, 48)
     assert results[0]["indiv"] == results[1]["indiv"] == jb.EINDIVISIBLE
+
+
+def test_library_dist_plan_validation_world2(results):
+    """jacobi_dist_plan_create through the binding on 2 gloo ranks without a GPU: a wrong block shape is
+    refused by the binding, P not dividing n is EINDIVISIBLE on both ranks, bad arguments
+    are EINVAL before any CUDA call, and valid arguments end in ECUDA (there is no CPU fallback)."""
+    import paper_1403_5805_b200 as jb
+    for r in (0, 1):
+        o = results[r]
+        assert o["shape"] == "ValueError"
+        assert o["dp_indiv"] == jb.EINDIVISIBLE
+        assert o["dp_nogpu"] == jb.ECUDA
+        # rank out of range, NULL uid, bad dtype, lda < n -> EINVAL; column slabs of 50 columns -> EINVAL
+        # (a multiple of 8 is required), or EINDIVISIBLE first when P does not divide n
+        assert o["einval"][:4] == [jb.EINVAL] * 4
+        assert o["einval"][4] == jb.EINVAL
 
 
 def test_exchange_protocol_matches_serial_oracle_bitwise(results):

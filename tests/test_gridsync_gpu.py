@@ -46,6 +46,21 @@ def solve_both(jb, monkeypatch, A, b, max_iter, tol, x0=None):
     return out["1"], out["0"]
 
 
+def rel_linf(x, ref):
+    den = np.max(np.abs(ref))
+    err = np.max(np.abs(np.asarray(x) - ref))
+    return err / den if den > 0 else err
+
+
+def match_oracle(r, orc, tol=1e-10):
+    """Status, iteration count, x (relative L-inf <= 1e-10) and the d_k history against the oracle."""
+    st_o, x_o, it_o, h_o = orc
+    assert (r.status, r.iters) == (st_o, it_o), (r.status, r.iters, st_o, it_o)
+    assert rel_linf(r.x, x_o) <= tol
+    if r.hist is not None:
+        np.testing.assert_allclose(r.hist, h_o, rtol=1e-9, atol=1e-14)
+
+
 def same(r, q):
     return ((r.status, r.iters) == (q.status, q.iters) and np.array_equal(r.x, q.x)
             and np.array_equal(r.hist, q.hist, equal_nan=True))
@@ -227,6 +242,8 @@ def test_persistent_fused_exchange_emulated_ranks_bitwise(jb, monkeypatch):
     for n, scale in ((8192, 1.05), (4096, 1.02)):  # >= 16 column chunks (the fused-exchange plans need it)
         A, b, _ = dominant(n, 211 + n, scale=scale)
         x0 = np.random.default_rng(n).uniform(-1, 1, n)
+        orc = oracle.jacobi(A, b, x0, 40, 0.0, nthreads=16, history=True)
+        orc2 = oracle.jacobi(A, b, x0, 3000, 1e-11, nthreads=16, history=True)
         monkeypatch.setenv("JACOBI_PERSIST", "0")
         with jb.Plan(A) as p:
             ref = p.solve(b, x0, 40, 0.0, history=True)
@@ -238,14 +255,17 @@ def test_persistent_fused_exchange_emulated_ranks_bitwise(jb, monkeypatch):
                 p.set_p2p_emulation(P)
                 assert p.info.persistent_ctas > 0
                 r = p.solve(b, x0, 40, 0.0, history=True)
+                match_oracle(r, orc)
                 assert r.iters == 40 and np.array_equal(r.x, ref.x) and np.array_equal(r.hist, ref.hist), (n, P)
                 r2 = p.solve(b, x0, 3000, 1e-11, history=True)
+                match_oracle(r2, orc2)
                 assert (r2.status, r2.iters) == (ref2.status, ref2.iters) and np.array_equal(r2.x, ref2.x), (n, P)
                 assert np.array_equal(r2.hist, ref2.hist)
                 if P in (1, 8):
                     r3 = p.solve(b, x0, 4200, 0.0)  # two launch segments
                     assert r3.iters == 4200 and np.array_equal(r3.x, ref3.x), (n, P)
     A, b, _ = dominant(8192, 5, scale=1.05)
+    orc = oracle.jacobi(A, b, None, 3000, 1e-11, nthreads=16, history=True)
     monkeypatch.setenv("JACOBI_PERSIST", "0")
     with jb.Plan(A) as p0:
         ref = p0.solve(b, None, 3000, 1e-11, history=True)
@@ -255,6 +275,7 @@ def test_persistent_fused_exchange_emulated_ranks_bitwise(jb, monkeypatch):
         p.ipc_attach(p.ipc_export())
         assert p.info.persistent_ctas > 0
         r = p.solve(b, None, 3000, 1e-11, history=True)
+        match_oracle(r, orc)
         assert (r.status, r.iters) == (ref.status, ref.iters) and np.array_equal(r.x, ref.x)
         assert np.array_equal(r.hist, ref.hist)
 
