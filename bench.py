@@ -10,10 +10,12 @@ sweep + fused update + max|dx| + device stop test; + allgather/allreduce when N 
   e2e   : the same metric through the C-ABI with HOST (pinned) buffers: N = 1 the one-shot
           jacobi_solve() (H2D of A, b, x0, plan setup, 100 sweeps, D2H of x inside the timed region
           every step); N > 1 every rank creates its distributed plan from its host row block per step.
-  cpu_baseline : the CPU oracle (oracle/), as it stands, on the host cores of rank 0: oracle.jacobi
-          over the WHOLE c4 system for a bounded number of its 100 sweeps (all cores), plus one-thread
-          per-sweep times of c1-c3.
-  --impl reference : the same oracle timing as the reference arm (rank 0 only under torchrun).
+  cpu_baseline : the CPU oracle (oracle/), as it stands, on the host cores of rank 0: its sweep
+          (oracle.sweep_rows on all cores + oracle.maxnorm_dist) over the WHOLE c4 system for a bounded
+          number of its 100 sweeps, the once-per-solve validation pass of oracle.jacobi timed beside it,
+          plus one-thread oracle.jacobi per-sweep times of c1-c3.
+  --impl reference : the same oracle sweeps as the reference arm; each step = --ref-sweeps consecutive
+          sweeps of the whole system (rank 0 only under torchrun).
 
 Multi-GPU: ``python bench.py --gpus N`` re-launches itself with N ranks (torch.distributed.run,
 127.0.0.1) when WORLD_SIZE is unset; under torchrun (the driver's form) it runs as one rank per GPU.
@@ -58,7 +60,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="CPU oracle budget: sweeps of the full system timed for about this long")
-    ap.add_argument("--ref-sweeps", type=int, default=5,
+    ap.add_argument("--ref-sweeps", type=int, default=3,
                     help="--impl reference: oracle sweeps of the full system per step")
     ap.add_argument("--exchange", choices=["nccl", "p2p", "cols"], default="nccl",
                     help="N > 1 headline exchange: NCCL row-wise (north star, default), fused NVLink push "
@@ -181,42 +183,68 @@ def ncu_traffic(name):
 
 
 # ----------------------------------------------------------------------------- CPU oracle timing
+def oracle_sweeps(A, b, x, sweeps, cores):
+    """`sweeps` sweeps of the oracle over the whole system: oracle.sweep_rows on row ranges
+    in `cores` host threads (ctypes releases the GIL; per-row arithmetic unchanged, so the bits equal
+    oracle.jacobi's at any thread count: pins P11/P13) and oracle.maxnorm_dist for d_k.  Returns
+    (x, hist, seconds)."""
+    import oracle
+    n = A.shape[0]
+    bounds = [n * t // cores for t in range(cores + 1)]
+    hist = []
+    t0 = time.perf_counter()
+    for _ in range(sweeps):
+        xn = np.empty(n)
+
+        def run(t):
+            r0, r1 = bounds[t], bounds[t + 1]
+            if r1 > r0:
+                xn[r0:r1] = oracle.sweep_rows(A[r0:r1], r0, b[r0:r1], x)
+
+        th = [threading.Thread(target=run, args=(t,)) for t in range(cores)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        hist.append(oracle.maxnorm_dist(xn, x))
+        x = xn
+    return x, hist, time.perf_counter() - t0
+
+
 def cpu_oracle_full(wname, seconds, A=None, b=None, sweeps=None):
-    """The oracle as it stands (oracle.jacobi, its own row-parallel threads) over the
-    WHOLE system of the workload, on all host cores of this process.  Runs `sweeps` sweeps (or as many
-    of the workload's sweeps as fit in about `seconds`, sized by a first 1-sweep call).  A, b: the host
-    system if the caller already holds it (the e2e leg does); else it is generated here.
-    Returns a dict: it/s of the whole oracle call (validation pass included), the per-sweep time net of
-    that pass (oracle.jacobi with max_iter = 0 is the validation alone), cores and the sample."""
+    """The oracle as it stands on all host cores of this process, over the WHOLE system of the workload:
+    its sweeps (oracle_sweeps: oracle.sweep_rows + oracle.maxnorm_dist) for `sweeps`
+    sweeps, or as many of the workload's sweeps as fit in about `seconds` (sized by a first sweep).
+    The once-per-solve validation pass of oracle.jacobi (max_iter = 0: the EZERODIAG/ENONFINITE scan,
+    single-threaded) is timed separately.  A, b: the host system if the caller already holds it (the
+    e2e leg does); else it is generated here."""
     import jacobi_gen as g
     import oracle
     cfg = g.CONFIGS[WORKLOADS[wname][0]]
     total_sweeps = WORKLOADS[wname][1]
     cores = len(os.sched_getaffinity(0))
-    t_gen = 0.0
+    t_gen = None
     if A is None:
         t0 = time.perf_counter()
         A, b = g.host_rows(cfg, 0, cfg.n)
         t_gen = time.perf_counter() - t0
     t0 = time.perf_counter()
-    oracle.jacobi(A, b, None, 0, 0.0, nthreads=cores)  # validation pass alone (EZERODIAG/ENONFINITE scan)
+    oracle.jacobi(A, b, None, 0, 0.0, nthreads=cores)  # validation pass alone
     t_val = time.perf_counter() - t0
+    x = np.zeros(cfg.n)
     if sweeps is None:
-        t0 = time.perf_counter()
-        oracle.jacobi(A, b, None, 1, 0.0, nthreads=cores)
-        t1 = time.perf_counter() - t0
-        sweeps = int(max(1, min(total_sweeps, seconds // max(t1, 1e-6))))
-    t0 = time.perf_counter()
-    st, x, it = oracle.jacobi(A, b, None, sweeps, 0.0, nthreads=cores)
-    el = time.perf_counter() - t0
-    assert it == sweeps, (st, it)
-    per_sweep = max(el - t_val, 1e-9) / sweeps
-    return {"value": sweeps / el, "unit": "it/s", "cores": cores, "kind": "oracle",
-            "sample": (f"oracle.jacobi(nthreads={cores}) on the whole {wname} system (n={cfg.n}), {sweeps} of its "
-                       f"{total_sweeps} fixed sweeps in {el:.2f} s (validation pass {t_val:.2f} s included); "
-                       f"it/s = sweeps / time"),
+        x, _, t1 = oracle_sweeps(A, b, x, 1, cores)
+        sweeps = int(max(1, min(total_sweeps - 1, seconds // max(t1, 1e-6))))
+    x, hist, el = oracle_sweeps(A, b, x, sweeps, cores)
+    per_sweep = el / sweeps
+    solve_s = t_val + total_sweeps * per_sweep
+    return {"value": 1.0 / per_sweep, "unit": "it/s", "cores": cores, "kind": "oracle",
+            "sample": (f"{sweeps} of the {total_sweeps} sweeps of the whole {wname} system (n={cfg.n}) with the "
+                       f"oracle's sweep (oracle.sweep_rows on {cores} threads + oracle.maxnorm_dist) in {el:.2f} s; "
+                       f"it/s = sweeps / time.  oracle.jacobi's once-per-solve validation pass took {t_val:.2f} s "
+                       f"(single thread): a whole {total_sweeps}-sweep oracle solve ~ {solve_s:.1f} s"),
             "per_sweep_s": per_sweep, "sweeps": sweeps, "seconds": el, "validation_s": t_val,
-            "gen_s": t_gen if t_gen else None}
+            "solve_it_per_s": total_sweeps / solve_s, "gen_s": t_gen}
 
 
 def cpu_oracle_t1(configs=("c1", "c2", "c3"), seconds=2.0):
@@ -251,18 +279,25 @@ def reference_arm(args, rank):
     t0 = time.perf_counter()
     A, b = g.host_rows(cfg, 0, cfg.n)
     t_gen = time.perf_counter() - t0
+    import oracle
+    cores = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    oracle.jacobi(A, b, None, 0, 0.0, nthreads=cores)  # the oracle's validation pass, once per solve
+    t_val = time.perf_counter() - t0
+    x = np.zeros(cfg.n)
     for _ in range(args.warmup):
-        cpu_oracle_full(args.workload, 0, A, b, sweeps=args.ref_sweeps)
-    els = []
-    cb = None
-    for _ in range(args.steps):
-        cb = cpu_oracle_full(args.workload, 0, A, b, sweeps=args.ref_sweeps)
-        els.append(cb["seconds"])
-    el = sum(els)
+        x, _, _ = oracle_sweeps(A, b, x, args.ref_sweeps, cores)
+    x = np.zeros(cfg.n)
+    el = 0.0
+    for _ in range(args.steps):  # consecutive sweeps of one solve from x0 = 0
+        x, _, t = oracle_sweeps(A, b, x, args.ref_sweeps, cores)
+        el += t
     rate = args.steps * args.ref_sweeps / el
-    cb.update(value=rate, seconds=el, gen_s=t_gen,
-              sample=(f"{args.steps} steps x oracle.jacobi(nthreads={cb['cores']}) over the whole {gname} system "
-                      f"(n={cfg.n}), {args.ref_sweeps} of its {sweeps} sweeps per step (validation pass each call)"))
+    cb = {"value": rate, "unit": "it/s", "cores": cores, "kind": "oracle", "seconds": el, "validation_s": t_val,
+          "gen_s": t_gen,
+          "sample": (f"{args.steps} steps x {args.ref_sweeps} consecutive sweeps of the whole {gname} system "
+                     f"(n={cfg.n}) with the oracle's sweep (oracle.sweep_rows on {cores} threads + "
+                     f"oracle.maxnorm_dist); the once-per-solve validation pass ({t_val:.2f} s) is not in a step")}
     line = {"impl": "reference", "metric": "Jacobi iterations/s", "value": rate, "unit": "it/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "strong",

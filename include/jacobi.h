@@ -147,6 +147,20 @@ int jacobi_plan_info(const jacobi_plan* plan, jacobi_plan_info_t* info);
  * duration in ms.  For roofline measurements; the solve path itself uses CUDA graphs. */
 int jacobi_plan_time_sweeps(jacobi_plan* plan, const double* d_b, const double* d_x0, int sweeps,
                             float* ms_out);
+/* Per-GPU shard measurement (SURVEY.md §8(e); PAPER.md:72 row blocks, :84-90 per-rank partial
+ * products): on a 1-GPU row-wise plan, times `sweeps` (1..4096) fixed sweeps of ONLY rows
+ * [rank*n/nranks, (rank+1)*n/nranks) — the work rank `rank` of an nranks-rank row-block plan does per
+ * sweep — with the kernel variant, grid and L2-resident share that rank's plan would choose (they depend
+ * on the m x n block's shape only), and no exchange.  mode 0: a CUDA graph of sweep kernels (the
+ * graph path); 1: the persistent grid solver on the shard; 2: the persistent fused-exchange kernel
+ * (k_solve_gridsync_push) with its peer set reduced to this GPU (pushes, remote atomics and arrival
+ * counters all local).  d_b (n) and d_x0 (n) are device vectors.  Writes the average ms per sweep
+ * (CUDA events around one warm launch of all sweeps) and, if variant_out is non-NULL, the sweep
+ * variant (-1 / -2 for modes 1 / 2).  Rows outside the shard keep x0, so the iterates are not the
+ * system's: a measurement hook, not a solver.  Errors: EINVAL (distributed / emulating plan,
+ * nranks does not divide n, bad arguments, persistent mode unsupported for this shape), ECUDA. */
+int jacobi_plan_time_shard(jacobi_plan* plan, int nranks, int rank, const double* d_b, const double* d_x0,
+                           int sweeps, int mode, float* ms_per_sweep, int* variant_out);
 
 /* ------------------------------------------------------------------ distributed (NCCL) */
 /* Row-block partition of PAPER.md:72: rows [rank*m, (rank+1)*m), m = n/nranks. */

@@ -29,7 +29,8 @@ STATUS_NAMES = {0: "CONVERGED", 1: "MAX_ITER", -1: "EINVAL", -2: "EZERODIAG", -3
 # Every symbol include/jacobi.h declares (checked by tests/test_capi.py).
 EXPORTS = ("jacobi_solve", "jacobi_solve_f32a", "jacobi_plan_create", "jacobi_plan_solve",
            "jacobi_plan_solve_device", "jacobi_plan_destroy", "jacobi_plan_set_row_blocks",
-           "jacobi_plan_set_batch", "jacobi_plan_set_norm", "jacobi_plan_info", "jacobi_plan_time_sweeps", "jacobi_partition",
+           "jacobi_plan_set_batch", "jacobi_plan_set_norm", "jacobi_plan_info", "jacobi_plan_time_sweeps",
+           "jacobi_plan_time_shard", "jacobi_partition",
            "jacobi_nccl_unique_id", "jacobi_dist_plan_create", "jacobi_dist_plan_create_colwise",
            "jacobi_plan_set_col_blocks", "jacobi_plan_ipc_export", "jacobi_plan_ipc_attach",
            "jacobi_plan_set_p2p_emulation", "jacobi_bwprobe", "jacobi_last_error",
@@ -84,6 +85,7 @@ def _load():
         "jacobi_plan_set_norm": ([vp, i32], i32),
         "jacobi_plan_info": ([vp, P(PlanInfo)], i32),
         "jacobi_plan_time_sweeps": ([vp, vp, vp, i32, P(ctypes.c_float)], i32),
+        "jacobi_plan_time_shard": ([vp, i32, i32, vp, vp, i32, i32, P(ctypes.c_float), P(i32)], i32),
         "jacobi_partition": ([i64, i32, i32, P(i64), P(i64)], i32),
         "jacobi_nccl_unique_id": ([vp], i32),
         "jacobi_dist_plan_create": ([P(vp), vp, i32, i32, i64, i32, vp, i64, i32, vp], i32),
@@ -285,6 +287,18 @@ class Plan:
         _check(_lib.jacobi_plan_time_sweeps(self._h, _dev_ptr(b, inf.rows, "b"), _dev_ptr(x0, self.n, "x0"),
                                             int(sweeps), ms))
         return np.array(ms[:], dtype=np.float64)
+
+
+    def time_shard(self, b, x0, nranks, rank=0, sweeps=20, mode="graph"):
+        """jacobi_plan_time_shard: ms per sweep of rank `rank`'s row block of an nranks-rank plan, on this
+        GPU, exchange excluded.  mode: "graph", "persistent" or "persistent-push".  Returns (ms, variant)."""
+        ms = ctypes.c_float()
+        v = ctypes.c_int()
+        m = {"graph": 0, "persistent": 1, "persistent-push": 2}[mode]
+        _check(_lib.jacobi_plan_time_shard(self._h, int(nranks), int(rank), _dev_ptr(b, self.n, "b"),
+                                           _dev_ptr(x0, self.n, "x0"), int(sweeps), m, ctypes.byref(ms),
+                                           ctypes.byref(v)))
+        return float(ms.value), int(v.value)
 
 
 def partition(n, nranks, rank):

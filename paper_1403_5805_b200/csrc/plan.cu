@@ -103,12 +103,32 @@ static int check_last(const char* what) {
     if (_rc) return _rc;             \
   } while (0)
 
-// Sweep-kernel variant for a GEMV over `ncols` columns (default from measurements; the
-// JACOBI_SWEEP_VARIANT override is honoured when the variant can tile the chunking).
-static void choose_variant(const jacobi_plan* p, int64_t ncols, int* variant, int* grid) {
+// L2-resident share of A (sweep variants with POL), per mille of the stored block's work units: a
+// budget of 50 % of the L2 (per-unit keep, µs per sweep at budget 0.5 / 0.65 / 0.78 / 0.9: c2 19.7 /
+// 19.6 / 22.6 / 26.4, c3 P = 8 shard 40.3 / 40.8 / 44.3 / 46.5, profiles/keep_budget_r02.txt) is kept across sweeps
+// with evict_last loads and the rest streams with evict_first, whenever that budget is at least 2 % of
+// the block (a smaller share is not worth giving up the dynamic-tile kernel of large blocks).  Each CTA
+// keeps that share of its own (tile, chunk) units (keep_unit in sweep.cu), so the kept bytes stay within
+// the budget at any row length.  A function of the block's shape only: a P-rank plan's rank applies it
+// to its m x n block (c3: P = 1/2/4/8 keep 4.5 / 9 / 18 / 36 % of the block).  JACOBI_L2_KEEP (per
+// mille) and JACOBI_L2_BUDGET (fraction of the L2) override.
+static int l2_keep_for(int l2, int64_t a_rows, int64_t a_cols, int dtype, int num_sms) {
+  (void)num_sms;
+  const double a_bytes = (double)a_rows * (double)a_cols * (dtype == JACOBI_F32 ? 4.0 : 8.0);
+  double budget = 0.5;
+  if (const char* e = getenv("JACOBI_L2_BUDGET")) budget = atof(e);
+  int keep = (l2 > 0 && a_bytes > 0) ? (int)std::min(1000.0, std::floor(1000.0 * budget * l2 / a_bytes)) : 0;
+  if (keep < 20) keep = 0;
+  if (const char* e = getenv("JACOBI_L2_KEEP")) keep = std::max(0, std::min(1000, atoi(e)));
+  return keep;
+}
+
+// Sweep-kernel variant for a GEMV over `ncols` columns and `rows` rows per launch (default from
+// measurements; the JACOBI_SWEEP_VARIANT override is honoured when the variant can tile the chunking).
+static void choose_variant_for(const jacobi_plan* p, int64_t ncols, int64_t rows, int l2_keep_pm, int* variant,
+                               int* grid) {
   const int nch = (int)((ncols + p->chunk - 1) / p->chunk);
-  int v = jacobi::default_variant(p->dtype, nch, p->chunk, p->l2_keep_pm > 0, p->colwise ? p->n : p->m / p->nblocks,
-                                  p->num_sms);
+  int v = jacobi::default_variant(p->dtype, nch, p->chunk, l2_keep_pm > 0, rows, p->num_sms);
   if (const char* e = getenv("JACOBI_SWEEP_VARIANT")) {  // tuning override (all variants: same bits)
     const int vi = atoi(e);
     if (vi >= 0 && vi < jacobi::num_variants() && !jacobi::variant_is_push(vi) &&
@@ -117,6 +137,9 @@ static void choose_variant(const jacobi_plan* p, int64_t ncols, int* variant, in
   }
   *variant = v;
   *grid = jacobi::sweep_grid(p->dtype, v, p->num_sms, nch, p->chunk);
+}
+static void choose_variant(const jacobi_plan* p, int64_t ncols, int* variant, int* grid) {
+  choose_variant_for(p, ncols, p->colwise ? p->n : p->m / p->nblocks, p->l2_keep_pm, variant, grid);
 }
 
 // Common plan setup.  The stored block of A is a_rows x a_cols (row-major, lda): the m x n row block
@@ -166,30 +189,14 @@ int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dty
   }
   JLAST("A upload");
   p->chunk = jacobi::chunk_for(n, dtype);
-  // L2-resident share of A (sweep variants with POL): when the stored block is at most 4x the L2,
-  // keep ~59 % of the L2 (74 MB of 126 MB: the measured optimum at c2) of it across sweeps with
-  // evict_last loads and stream the rest with evict_first.  JACOBI_L2_KEEP (per mille) overrides.
   {
     int l2 = 0;
     JCUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, p->device));
-    const double a_bytes = (double)a_rows * (double)a_cols * (dtype == JACOBI_F32 ? 4.0 : 8.0);
-    if (l2 > 0 && a_bytes <= 4.0 * l2) p->l2_keep_pm = (int)std::min(1000.0, 1000.0 * 0.59 * l2 / a_bytes);
-    // fp64: the kernels keep whole 8-row tiles of each CTA's rows (one CTA per SM), tile t when
-    // t*8*1000 < rows*keep.  A per-mille share just above a tile boundary keeps one tile too many on
-    // every CTA and the kept set no longer fits (c2: 580 ‰ of 28 rows keeps 24 rows — 10 % L2 hits —
-    // where 16 rows give 53 %, profiles/l2keep_grid_r01.md).  So the budget — 78 % of the L2, the
-    // measured best with whole tiles (kept share of the L2 vs µs per sweep, profiles/l2keep_tiles_r01.md:
-    // n = 3584 0.77 best; 4096 0.59 best, 0.88 thrashes; 4608 0.66 best; 6144 0.44 best, 0.88 worse) —
-    // is rounded down to whole tiles T per CTA, and keep is placed where every CTA keeps exactly T.
-    if (dtype == JACOBI_F64 && p->l2_keep_pm > 0 && p->l2_keep_pm < 1000 && p->num_sms > 0 && a_rows >= p->num_sms) {
-      const int64_t G = p->num_sms, rmax = (a_rows + G - 1) / G;
-      const int64_t T = (int64_t)(0.78 * l2 / (a_cols * 8.0 * G) / 8.0);
-      p->l2_keep_pm = T >= 1 ? (int)std::min<int64_t>(1000, T * 8 * 1000 / rmax) : 0;
-    }
-    if (const char* e = getenv("JACOBI_L2_KEEP")) p->l2_keep_pm = std::max(0, std::min(1000, atoi(e)));
+    p->l2_keep_pm = l2_keep_for(l2, a_rows, a_cols, dtype, p->num_sms);
   }
   choose_variant(p, a_cols, &p->variant, &p->grid);
   JLAST("sweep kernel occupancy query");
+  if (const char* e = getenv("JACOBI_PREFETCH")) p->pf_steps = std::max(0, atoi(e));
   p->x_len = round_up(n, 256) + 256;
   const int64_t nchunks = (a_cols + p->chunk - 1) / p->chunk;
   JCUDA(cudaMalloc(&p->diag, (size_t)m * 8));
@@ -510,6 +517,7 @@ static jacobi::SweepArgs sweep_args(const jacobi_plan* p, int blk) {
   const int R = jacobi::variant_rows_dt(p->variant, p->dtype);
   a.tiles = (int)((mb + R - 1) / R);
   a.l2_keep_pm = p->l2_keep_pm;
+  a.pf_steps = p->pf_steps;
   a.a_base = p->dA;
   a.a_elems = p->a_rows * p->lda;
   a.x_len = p->x_len;
@@ -982,6 +990,125 @@ extern "C" int jacobi_plan_time_sweeps(jacobi_plan* p, const double* d_b, const 
   cudaStreamSynchronize(p->stream);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  return rc;
+}
+
+// Per-GPU shard measurement (see jacobi.h): the sweeps rank `rank` of an nranks-rank row-block plan
+// would run on its m x n block — the same kernel variant, grid and L2-resident share its plan would
+// choose (they depend on the block's shape only) — timed on this GPU without the exchange.
+extern "C" int jacobi_plan_time_shard(jacobi_plan* p, int nranks, int rank, const double* d_b, const double* d_x0,
+                                      int sweeps, int mode, float* ms_per_sweep, int* variant_out) {
+  if (!p || nranks < 1 || rank < 0 || rank >= nranks || !d_b || !d_x0 || sweeps < 1 ||
+      sweeps > jacobi::kMaxSweepsPerLaunch || mode < 0 || mode > 2 || !ms_per_sweep || p->comm || p->colwise ||
+      p->p2p || p->nblocks != 1 || p->colblocks != 1 || p->n % nranks != 0)
+    return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_time_shard: 1-GPU row-wise plan, nranks | n, 0 <= rank < "
+                                           "nranks, 1 <= sweeps <= 4096, mode 0/1/2");
+  JCUDA(cudaSetDevice(p->device));
+  const int64_t ms = p->n / nranks, r0 = (int64_t)rank * ms;
+  int l2 = 0;
+  JCUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, p->device));
+  const int keep = l2_keep_for(l2, ms, p->n, p->dtype, p->num_sms);
+  int v = 0, grid = 0;
+  choose_variant_for(p, p->n, ms, keep, &v, &grid);
+  JLAST("shard variant");
+  const int64_t esz = p->dtype == JACOBI_F32 ? 4 : 8;
+  jacobi::SweepArgs a = sweep_args(p, 0);
+  a.A = (const char*)p->dA + (size_t)(r0 * p->lda * esz);
+  a.m = ms;
+  a.row0 = r0;
+  a.diag = p->diag + r0;
+  a.b = p->b + r0;
+  a.sq = p->sq + r0;
+  a.tiles = (int)((ms + jacobi::variant_rows_dt(v, p->dtype) - 1) / jacobi::variant_rows_dt(v, p->dtype));
+  a.l2_keep_pm = keep;
+  int rc = 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaGraphExec_t gx = nullptr;
+  jacobi::SweepArgs* ra = nullptr;
+  jacobi::PeerArgs* pa = nullptr;
+  size_t smem = 0;
+  int G = 0;
+  auto prepare = [&]() -> int {
+    JRC(solve_prepare(p, d_b, d_x0, true, sweeps, 0.0, nullptr));
+    JCUDA(cudaMemsetAsync(p->flags, 0, 2 * 8, p->stream));
+    return 0;
+  };
+  auto launch = [&]() -> int {
+    if (mode == 0) {
+      JCUDA(cudaGraphLaunch(gx, p->stream));
+    } else if (mode == 1) {
+      JCUDA(jacobi::launch_solve_gridsync(p->dtype, a, p->gbar, 1, sweeps, G, smem, p->stream));
+    } else {
+      JCUDA(jacobi::launch_solve_gridsync_push(p->dtype, ra, 1, 1, sweeps, G, smem, p->stream));
+    }
+    return 0;
+  };
+  rc = [&]() -> int {
+    const int nch = (int)((p->n + p->chunk - 1) / p->chunk);
+    if (mode == 0) {  // a graph of `sweeps` sweep kernels, like the rank's graph minus the collectives
+      cudaGraph_t g = nullptr;
+      JCUDA(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+      int lrc = 0;
+      for (int j = 0; j < sweeps && lrc == 0; ++j) {
+        cudaError_t e = jacobi::launch_sweep(p->dtype, v, a, j, grid, p->stream);
+        if (e != cudaSuccess) lrc = jacobi_set_error(JACOBI_ECUDA, std::string("shard sweep: ") + cudaGetErrorString(e));
+      }
+      cudaError_t ee = cudaStreamEndCapture(p->stream, &g);
+      if (lrc) { if (g) cudaGraphDestroy(g); return lrc; }
+      JCUDA(ee);
+      cudaError_t ie = cudaGraphInstantiate(&gx, g, 0);
+      cudaGraphDestroy(g);
+      JCUDA(ie);
+    } else if (mode == 1) {  // the persistent grid solver restricted to the shard's rows
+      G = jacobi::gridsync_plan(p->dtype, nch, p->num_sms, &smem);
+      cudaGetLastError();
+      if (!G) return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_time_shard: persistent solver not supported here");
+      v = -1;
+    } else {  // the persistent fused-exchange kernel of a rank, its peer set reduced to this GPU
+      G = jacobi::gridsync_push_plan(p->dtype, nch, p->num_sms, &smem);
+      cudaGetLastError();
+      if (!G) return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_time_shard: persistent fused exchange not supported");
+      jacobi::PeerArgs q;
+      std::memset(&q, 0, sizeof(q));
+      q.P = 1;
+      q.rank = 0;
+      q.total_ctas = (unsigned long long)G;
+      q.wait_ns = peer_wait_ns();
+      q.x0[0] = p->x[0];
+      q.x1[0] = p->x[1];
+      q.dslot[0] = p->dslot;
+      q.flags[0] = p->flags;
+      JCUDA(cudaMalloc(&pa, sizeof(q)));
+      JCUDA(cudaMemcpy(pa, &q, sizeof(q), cudaMemcpyHostToDevice));
+      a.peers = pa;
+      JCUDA(cudaMalloc(&ra, sizeof(a)));
+      JCUDA(cudaMemcpy(ra, &a, sizeof(a), cudaMemcpyHostToDevice));
+      v = -2;
+    }
+    JCUDA(cudaEventCreate(&e0));
+    JCUDA(cudaEventCreate(&e1));
+    JRC(prepare());
+    JRC(launch());  // warm-up (graph upload, L2 state)
+    JRC(prepare());
+    JCUDA(cudaEventRecord(e0, p->stream));
+    JRC(launch());
+    JCUDA(cudaEventRecord(e1, p->stream));
+    JCUDA(cudaEventSynchronize(e1));
+    float ms_tot = 0.f;
+    JCUDA(cudaEventElapsedTime(&ms_tot, e0, e1));
+    JCUDA(cudaMemcpy(&p->st_host[0], p->st, sizeof(jacobi::State), cudaMemcpyDeviceToHost));
+    if (p->st_host[0].fault) return jacobi_set_error(JACOBI_ECUDA, "jacobi_plan_time_shard: wait timed out");
+    *ms_per_sweep = ms_tot / (float)sweeps;
+    if (variant_out) *variant_out = v;
+    return 0;
+  }();
+  cudaStreamSynchronize(p->stream);
+  if (gx) cudaGraphExecDestroy(gx);
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (ra) cudaFree(ra);
+  if (pa) cudaFree(pa);
+  cudaGetLastError();
   return rc;
 }
 

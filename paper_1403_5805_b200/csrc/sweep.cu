@@ -189,10 +189,22 @@ __device__ unsigned long long g_smt[3 * 4096];
   } while (0)
 #endif
 
-__device__ __forceinline__ bool sweep_prologue(const SweepArgs& a, int j, bool leader) {
+// All state loads are issued together (one L2 round trip instead of a chain of dependent ones: the
+// short-circuit `done || nonfinite || fault` and the kbase -> slot dependency each cost a round trip,
+// ~1-2 µs per sweep kernel).  The distance slot of sweep k-1 is (kbase + j) & 3 = j & 3 because kbase
+// is a multiple of the graph batch, itself a multiple of 4 (jacobi_plan_set_batch); with the fused
+// exchange it is re-read after the wait for the peers' atomics.
+__device__ __forceinline__ bool sweep_prologue(const SweepArgs& a, int j, bool leader, long long* k_out) {
   State* st = a.st;
-  if (*(volatile int32_t*)&st->done || st->nonfinite || *(volatile int32_t*)&st->fault) return false;
-  const int64_t k = st->kbase + j + 1;
+  const int32_t done = *(volatile int32_t*)&st->done, nonf = st->nonfinite, fault = *(volatile int32_t*)&st->fault;
+  const int64_t kbase = st->kbase, max_iter = st->max_iter;
+  const double tol = st->tol;
+  double* const hist = st->hist;
+  unsigned long long dbits = *(volatile unsigned long long*)&a.dslot[j & 3];
+  if (done | nonf | fault) return false;
+  JB_CHECK((kbase & 3) == 0, 7);  // bit 7: the slot shortcut's premise
+  const int64_t k = kbase + j + 1;
+  *k_out = k;  // broadcast through shared memory: the sweep body needs no second read of the state
   if (k >= 2 && a.peers) {
     // NEXT-1: wait until every CTA of every rank has pushed its x^(k-1) rows and max|dx| bits here.
     // Bounded: after pe->wait_ns (10 s by default) the plan is marked faulted (the host reports JACOBI_ECUDA) and every
@@ -213,17 +225,18 @@ __device__ __forceinline__ bool sweep_prologue(const SweepArgs& a, int j, bool l
         }
       }
     }
+    dbits = *(volatile unsigned long long*)&a.dslot[j & 3];  // after the acquire: every peer's atomicMax
   }
   if (k >= 2) {
-    const double d = __longlong_as_double((long long)a.dslot[(k - 1) & 3]);
-    if (leader && st->hist) st->hist[k - 2] = d;
-    if (d < st->tol) {  // (b): ||X - X^t|| < tol  -> return X^(k-1)
+    const double d = __longlong_as_double((long long)dbits);
+    if (leader && hist) hist[k - 2] = d;
+    if (d < tol) {  // (b): ||X - X^t|| < tol  -> return X^(k-1)
       if (leader) { st->status = JACOBI_CONVERGED; st->iters = k - 1; st->done = 1; }
       return false;
     }
   }
-  if (k > st->max_iter) {  // step 3: iteration limit reached
-    if (leader) { st->status = JACOBI_MAX_ITER; st->iters = st->max_iter; st->done = 1; }
+  if (k > max_iter) {  // step 3: iteration limit reached
+    if (leader) { st->status = JACOBI_MAX_ITER; st->iters = max_iter; st->done = 1; }
     return false;
   }
   if (leader) a.dslot[(k + 1) & 3] = 0ull;  // next sweep's max accumulator
@@ -313,11 +326,12 @@ __device__ __forceinline__ void accumulate_chunk(const T* const (&rowp)[R], cons
 template <typename T, int R, int U, int NT>
 __global__ void __launch_bounds__(NT, (NT < 512 ? 512 / NT : 1)) k_sweep(const SweepArgs a, const int j) {
   __shared__ int s_go;
-  if (threadIdx.x == 0) s_go = sweep_prologue(a, j, blockIdx.x == 0);
+  __shared__ long long s_k;
+  if (threadIdx.x == 0) s_go = sweep_prologue(a, j, blockIdx.x == 0, &s_k);
   __syncthreads();
   if (!s_go) return;
 
-  const int64_t k = a.st->kbase + j + 1;
+  const int64_t k = s_k;
   const double* __restrict__ xo = (k & 1) ? a.x0buf : a.x1buf;  // x^(k-1)
   double* __restrict__ xn = (k & 1) ? a.x1buf : a.x0buf;        // x^(k)
   const T* __restrict__ A = static_cast<const T*>(a.A);
@@ -416,6 +430,31 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
 
 constexpr int kSlots = 4;
 
+// L2-resident share of A (POL instances).  The kept set is made of work units — (tile, column chunk[,
+// row group]) — not whole tiles: a unit is 16-64 KB, a tile up to 1 MB (8 rows of 16384 fp64), and an
+// L2 budget of ~60 MB is less than one tile per CTA once rows are that long (c3 shards).  Unit i of a
+// CTA's sequence (offset by a per-CTA phase) is kept iff frac(i * phi) < keep_pm / 1000 (a Weyl
+// sequence: the kept units are spread evenly along every CTA's sequence and every warp's share, and
+// the kept count is the share to within a couple of units), so at any moment some CTAs stream kept
+// units from L2 while others stream from HBM.  32-bit integer hash: two instructions per unit (an exact
+// Bresenham split needed 64-bit divisions and pushed the persistent kernels into register spills).
+// The same units are kept every sweep (static rows), so they hit in L2 from the second sweep on.
+__device__ __forceinline__ unsigned keep_threshold(int keep_pm) {
+  return keep_pm >= 1000 ? 0xffffffffu : (unsigned)(((unsigned long long)max(keep_pm, 0) << 32) / 1000ull);
+}
+__device__ __forceinline__ bool keep_unit(unsigned i, unsigned thr) { return i * 2654435769u < thr; }
+
+// Fused exchange, end of sweep k in one CTA (thread 0, after a CTA barrier that follows every thread's
+// x stores): fold the CTA's max|dx| bits into every rank's distance slot, then — behind one system-scope
+// fence, cumulative over the stores the barrier ordered before it — add one arrival to every rank's
+// counter for the parity of k.
+__device__ __forceinline__ void push_signal(const PeerArgs* pe, int64_t k, unsigned long long m) {
+  const int P = pe->P;
+  for (int p = 0; p < P; ++p) atomicMax(pe->dslot[p] + (k & 3), m);
+  __threadfence_system();
+  for (int p = 0; p < P; ++p) atomicAdd(pe->flags[p] + (k & 1), 1ull);
+}
+
 // CTA-wide max of the warps' max|dx| bits (every thread must call it; returns the max in thread 0).
 // Used by the fused exchange, where each atomic crosses NVLink to every peer: one remote atomic per
 // CTA per peer instead of one per warp (16x fewer same-address atomics arriving at each rank: 1184
@@ -456,6 +495,9 @@ __device__ __forceinline__ unsigned long long cta_sweep(const SweepArgs& a, cons
   const int64_t rb = DYN ? 0 : (int64_t)cta * a.m / ncta;  // this CTA's rows of the launch (rank)
   const int64_t re = DYN ? a.m : (int64_t)(cta + 1) * a.m / ncta;
   const int ntile = (int)((re - rb + R - 1) / R);
+  // POL keep pattern over the CTA's units (DYN: over the launch's units, tiles numbered globally)
+  const unsigned kthr = POL ? keep_threshold(a.l2_keep_pm) : 0u;
+  const unsigned koff = DYN ? 0u : (unsigned)cta * 40503u;
   unsigned long long dmax = 0ull;
 
   auto finalize = [&](int t) {
@@ -520,11 +562,12 @@ __device__ __forceinline__ unsigned long long cta_sweep(const SweepArgs& a, cons
 #pragma unroll
     for (int r = 0; r < R; ++r) rowp[r] = A + (r0 + min(r, nv - 1)) * a.lda - a.col0;  // global columns
     const int64_t g0 = a.row0 + r0;
-    uint64_t pol = 0;  // POL: the first l2_keep_pm/1000 of the CTA's rows stay in L2 (evict_last)
-    if constexpr (POL) pol = l2_policy((r0 - rb) * 1000 < (re - rb) * (int64_t)a.l2_keep_pm);
+    const unsigned useq = (unsigned)(DYN ? (r0 / R) : (int64_t)t) * (unsigned)(nch * GR) + koff;  // tile's 1st unit
     constexpr int RG = R / GR;  // rows per unit
     for (int u = w; u < nch * GR; u += NW) {
       const int c = u / GR, rg = u % GR;
+      uint64_t pol = 0;  // POL: evict_last for the kept units, evict_first for the streamed ones
+      if constexpr (POL) pol = l2_policy(keep_unit(useq + (unsigned)u, kthr));
       const int nvg = min(RG, nv - rg * RG);  // rows of this group that exist (last tile)
       if (nvg <= 0) continue;
       const T* rp[RG];
@@ -583,6 +626,34 @@ __device__ __forceinline__ unsigned long long cta_sweep(const SweepArgs& a, cons
   return dmax;
 }
 
+// Start of a sweep kernel with static rows: while thread 0 runs the prologue (one L2 round trip for
+// the stop state), every warp asks L2 for the first a.pf_steps column steps of its first unit (A does
+// not depend on the previous sweep), so the unit's first loads find their lines in L2 or in flight
+// instead of paying the full HBM latency after the barrier.  pf_steps = 0 turns it off.
+template <typename T, int R, int NW, int GR>
+__device__ __forceinline__ void prefetch_first_unit(const SweepArgs& a, int cta, int ncta) {
+  if (a.pf_steps <= 0) return;
+  constexpr int E = VecOf<T>::E;
+  constexpr int RG = R / GR;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (w >= a.nchunks * GR) return;
+  const int64_t rb = (int64_t)cta * a.m / ncta, re = (int64_t)(cta + 1) * a.m / ncta;
+  const int c = w / GR, rg = w % GR;
+  const int64_t c0 = a.col0 + (int64_t)c * a.chunk;
+  const int steps = min(a.pf_steps, a.chunk / (32 * E));
+  const T* A = static_cast<const T*>(a.A);
+  for (int r = 0; r < RG; ++r) {
+    const int64_t row = rb + rg * RG + r;
+    if (row >= re) break;
+    const T* rp = A + row * a.lda - a.col0;
+    for (int s = 0; s < steps; ++s) {
+      const int64_t col = c0 + (int64_t)(s * 32 + lane) * E;
+      if (col < a.cend && (lane & (128 / (E * sizeof(T)) - 1)) == 0)  // one request per 128-byte line
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + col));
+    }
+  }
+}
+
 template <typename T, int R, int NW, int U = 1, int XL = 0, bool PUSH = false, bool POL = false, int GR = 1,
           bool DYN = false>
 __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, const int j) {
@@ -591,8 +662,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
   __shared__ __align__(8) uint64_t s_full[kSlots], s_empty[kSlots];
   __shared__ int s_go;
   __shared__ int s_tile[8];  // DYN: tile of sequence t at [t & 7]
+  __shared__ long long s_k;
+  if constexpr (!DYN) prefetch_first_unit<T, R, NW, GR>(a, blockIdx.x, gridDim.x);
   if (threadIdx.x == 0) {
-    s_go = sweep_prologue(a, j, blockIdx.x == 0);
+    s_go = sweep_prologue(a, j, blockIdx.x == 0, &s_k);
     if (DYN && s_go) {  // the tiles of sequences 0 .. kSlots-1
       const unsigned base = atomicAdd(a.dyn, (unsigned)kSlots);
       for (int q = 0; q < kSlots; ++q) s_tile[q] = base + q < (unsigned)a.tiles ? (int)(base + q) : -1;
@@ -606,7 +679,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
   __syncthreads();
   if (!s_go) return;
 
-  const int64_t k = a.st->kbase + j + 1;
+  const int64_t k = s_k;
   __shared__ unsigned long long s_wmax[NW];
   const unsigned long long dmax =
       cta_sweep<T, R, NW, U, XL, PUSH, POL, GR, false, DYN>(a, k, 0, s_part, s_full, s_empty, blockIdx.x, gridDim.x,
@@ -614,17 +687,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
   if constexpr (!PUSH) {
     if ((threadIdx.x & 31) == 0 && dmax) atomicMax(&a.dslot[k & 3], dmax);  // local L2: one per warp is fine
   } else {
-    // NEXT-1: every thread fences its NVLink x pushes; then the CTA's max|dx| bits go into every rank's
-    // slot and, after a system fence, one arrival per CTA on every rank's counter for this parity; the
-    // next sweep's prologue waits for all of them.
-    __threadfence_system();
+    // NEXT-1: the CTA's max|dx| bits go into every rank's slot and, after a system-scope fence, one
+    // arrival per CTA on every rank's counter for this parity; the next sweep's prologue waits for all
+    // of them.  The CTA barrier inside cta_max_bits orders every thread's NVLink x pushes before thread
+    // 0's fence, whose release is cumulative — one fence per CTA instead of one per thread (512
+    // fence.sc.sys per CTA per sweep cost ~12 µs per sweep in the persistent kernel).
     const unsigned long long m = cta_max_bits<NW>(dmax, s_wmax);
-    if (threadIdx.x == 0) {
-      const PeerArgs* pe = a.peers;
-      for (int p = 0; p < pe->P; ++p) atomicMax(pe->dslot[p] + (k & 3), m);
-      __threadfence_system();
-      for (int p = 0; p < pe->P; ++p) atomicAdd(pe->flags[p] + (k & 1), 1ull);
-    }
+    if (threadIdx.x == 0) push_signal(a.peers, k, m);
   }
   SMT_END();
 }
@@ -757,7 +826,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync(const SweepArgs a
 // every rank's counter for the sweep's parity.  Before sweep k >= 2 a CTA waits on its own rank's
 // counter (all CTAs of all ranks have pushed x^(k-1)) — also at k = k0, since other GPUs may still
 // be finishing the previous launch — and then every CTA of every rank takes the same stop decision
-// from its own copy of the distance slot.  x is read at L2 (peers write it during the launch).
+// from its own copy of the distance slot.  x^(k-1) is read with weak loads (kGridXL = 3), as in
+// k_solve_gridsync: thread 0's ld.acquire.sys of the arrival counter and the CTA barrier that follows
+// order every peer's and every local CTA's stores of x^(k-1) before them (ld.global.cg here — L2 on
+// every tile, asm volatile — measured 1.6x slower per sweep: c3 shard 491 vs 299 µs).
 // Single-GPU emulation: one launch holds nvr virtual ranks (CTA groups) with their own x copies,
 // slots and counters (jacobi_plan_set_p2p_emulation) — the whole protocol in one co-resident grid.
 template <typename T, int R, int NW>
@@ -826,15 +898,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync_push(const SweepA
     __syncthreads();
     if (!s_go) break;
     const unsigned long long dmax =
-        cta_sweep<T, R, NW, 1, 2, true, true, 1, true>(a, k, (k - k0) * ntile, s_part, s_full, s_empty, blockIdx.x - c0,
+        cta_sweep<T, R, NW, 1, kGridXL, true, true, 1, true>(a, k, (k - k0) * ntile, s_part, s_full, s_empty, blockIdx.x - c0,
                                                    c1 - c0);
-    __threadfence_system();  // this thread's x pushes, before the arrivals below
-    const unsigned long long m = cta_max_bits<NW>(dmax, s_wmax);
-    if (threadIdx.x == 0) {
-      for (int p = 0; p < pe->P; ++p) atomicMax(pe->dslot[p] + (k & 3), m);
-      __threadfence_system();
-      for (int p = 0; p < pe->P; ++p) atomicAdd(pe->flags[p] + (k & 1), 1ull);
-    }
+    const unsigned long long m = cta_max_bits<NW>(dmax, s_wmax);  // CTA barrier: every x push issued
+    if (threadIdx.x == 0) push_signal(pe, k, m);
   }
 }
 
@@ -942,8 +1009,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_panel(const SweepArgs a, c
   __shared__ __align__(8) uint64_t s_xfull[XSN > 0 ? XSN : 1];
   __shared__ unsigned s_xcnt[XSN > 0 ? XSN : 1];
   __shared__ int s_go;
+  __shared__ long long s_k;
   if (threadIdx.x == 0) {
-    s_go = sweep_prologue(a, j, blockIdx.x == 0);
+    s_go = sweep_prologue(a, j, blockIdx.x == 0, &s_k);
     if constexpr (XSN > 0) {
       for (int q = 0; q < XSN; ++q) {
         mbar_init(&s_xfull[q], 1);
@@ -955,7 +1023,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_panel(const SweepArgs a, c
   __syncthreads();
   if (!s_go) return;
 
-  const int64_t k = a.st->kbase + j + 1;
+  const int64_t k = s_k;
   const double* __restrict__ xo = (k & 1) ? a.x0buf : a.x1buf;  // x^(k-1)
   double* __restrict__ xn = (k & 1) ? a.x1buf : a.x0buf;        // x^(k)
   const T* __restrict__ A = static_cast<const T*>(a.A);
@@ -1207,45 +1275,35 @@ struct Variant {
   void (*f32)(const SweepArgs, const int);
 };
 const Variant kVariants[] = {
+    // item kernel (defaults below 16 column chunks: 0 for fp32 A, 1 for fp64 A)
     {"k_sweep R4 U2", 4, 512, 0, 4, 2, 1, k_sweep<double, 4, 2, 512>, k_sweep<float, 4, 1, 512>},
     {"k_sweep R8 U1", 8, 512, 0, 8, 1, 1, k_sweep<double, 8, 1, 512>, k_sweep<float, 8, 1, 512>},
-    {"k_sweep R2 U4", 2, 512, 0, 2, 4, 2, k_sweep<double, 2, 4, 512>, k_sweep<float, 2, 2, 512>},
-    {"k_sweep R4 U1", 4, 512, 0, 4, 1, 2, k_sweep<double, 4, 1, 512>, k_sweep<float, 4, 2, 512>},
-    {"k_sweep R4 U2 256t", 4, 256, 0, 4, 2, 1, k_sweep<double, 4, 2, 256>, k_sweep<float, 4, 1, 256>},
-    {"k_sweep R2 U1 1024t", 2, 1024, 0, 2, 1, 1, k_sweep<double, 2, 1, 1024>, k_sweep<float, 2, 1, 1024>},
+    // CTA kernel with plain loads: the baselines the L2-policy (7) and dynamic (10) instances are measured against
     {"k_sweep_cta R8 U1", 8, 512, 1, 8, 1, 1, k_sweep_cta<double, 8, 16>, k_sweep_cta<float, 8, 16>},
     {"k_sweep_cta R4 U1", 4, 512, 1, 4, 1, 1, k_sweep_cta<double, 4, 16>, k_sweep_cta<float, 4, 16>},
-    {"k_sweep_cta R8 U1 256t", 8, 256, 1, 4, 1, 1, k_sweep_cta<double, 8, 8>, k_sweep_cta<float, 4, 8>},
-    {"k_sweep_cta R4 U2", 4, 512, 1, 4, 2, 2, k_sweep_cta<double, 4, 16, 2>, k_sweep_cta<float, 4, 16, 2>},
-    {"k_sweep_cta R2 U4", 2, 512, 1, 2, 4, 2, k_sweep_cta<double, 2, 16, 4>, k_sweep_cta<float, 2, 16, 2>},
-    // fused-exchange (NEXT-1) instances of the defaults; selected only by jacobi_plan_ipc_attach /
-    // jacobi_plan_set_p2p_emulation (they need SweepArgs.peers).  x^(k-1) is read with weak
+    // fused-exchange (NEXT-1) instance of the fp64 default; selected only by jacobi_plan_ipc_attach /
+    // jacobi_plan_set_p2p_emulation (it needs SweepArgs.peers).  x^(k-1) is read with weak
     // (L1-cacheable) loads, XL = 3, never ld.global.nc: peers store into it over NVLink while this
     // kernel may already be resident (spinning in sweep_prologue); the prologue's ld.acquire.sys of
     // the arrival counter plus the CTA barrier order those stores before every load of the sweep.
-    {"k_sweep_cta R4 U1 fused-exchange", 4, 512, 2, 4, 1, 1, k_sweep_cta<double, 4, 16, 1, 3, true>, k_sweep_cta<float, 4, 16, 1, 3, true>},
-    // row-panel kernel (cta = 3): warps own whole rows, x chunks shared through L1
-    {"k_sweep_panel R4 U1", 4, 512, 3, 4, 1, 1, k_sweep_panel<double, 4, 16>, k_sweep_panel<float, 4, 16>},
-    {"k_sweep_panel R4 U1 x-evict_last", 4, 512, 3, 4, 1, 1, k_sweep_panel<double, 4, 16, 1, 1>, k_sweep_panel<float, 4, 16, 1, 1>},
-    {"k_sweep_panel R8 U1", 8, 512, 3, 8, 1, 1, k_sweep_panel<double, 8, 16>, k_sweep_panel<float, 8, 16>},
-    {"k_sweep_panel R4 U2", 4, 512, 3, 4, 2, 1, k_sweep_panel<double, 4, 16, 2>, k_sweep_panel<float, 4, 16, 1, 1>},
-    // L2-resident share of A (SweepArgs.l2_keep_pm): 16 = CTA kernel, 17 = panel kernel
-    {"k_sweep_cta R4 U1 L2-keep", 4, 512, 1, 4, 1, 1, k_sweep_cta<double, 4, 16, 1, 0, false, true>, k_sweep_cta<float, 4, 16, 1, 0, false, true>},
-    {"k_sweep_panel R4 U1 L2-keep", 4, 512, 3, 4, 1, 1, k_sweep_panel<double, 4, 16, 1, 0, true>, k_sweep_panel<float, 4, 16, 1, 0, true>},
-    // row-panel kernel with x^(k-1) staged in shared memory (8-slot chunk ring, cta = 4)
-    {"k_sweep_panel R4 U1 x-smem", 4, 512, 4, 4, 1, 1, k_sweep_panel<double, 4, 16, 1, 0, false, 8>, k_sweep_panel<float, 4, 16, 1, 0, false, 8>},
-    {"k_sweep_panel R4 U1 x-smem L2-keep", 4, 512, 4, 4, 1, 1, k_sweep_panel<double, 4, 16, 1, 0, true, 8>, k_sweep_panel<float, 4, 16, 1, 0, true, 8>},
-    // CTA kernel R = 8 (fp64; the fp32 instances keep R = 4, R = 8 spills): L2-keep and fused exchange
-    {"k_sweep_cta R8 U1 L2-policy", 8, 512, 1, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, false, true>, k_sweep_cta<float, 4, 16, 1, 0, false, true>},
+    // (CTA kernel R = 8 for fp64; the fp32 instances keep R = 4, R = 8 spills.)
     {"k_sweep_cta R8 U1 fused-exchange", 8, 512, 2, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 3, true, true>, k_sweep_cta<float, 4, 16, 1, 3, true>},
-    // CTA kernel R8 L2-policy with (chunk, row group) units: balanced when nchunks is not a multiple of 16
+    // row-panel kernel (cta = 3): warps own whole rows, x chunks shared through L1 (fp32 fallback)
+    {"k_sweep_panel R4 U1", 4, 512, 3, 4, 1, 1, k_sweep_panel<double, 4, 16>, k_sweep_panel<float, 4, 16>},
+    // row-panel kernel with x^(k-1) staged in shared memory (8-slot chunk ring, cta = 4): fp32 default
+    {"k_sweep_panel R4 U1 x-smem", 4, 512, 4, 4, 1, 1, k_sweep_panel<double, 4, 16, 1, 0, false, 8>, k_sweep_panel<float, 4, 16, 1, 0, false, 8>},
+    // CTA kernel R8 with an L2 cache policy on A (evict_first, or evict_last for the kept share): fp64 default
+    {"k_sweep_cta R8 U1 L2-policy", 8, 512, 1, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, false, true>, k_sweep_cta<float, 4, 16, 1, 0, false, true>},
+    // ... with (chunk, half-tile) units: balanced when nchunks (17-31) is not a multiple of 16
     {"k_sweep_cta R8 U1 L2-policy rows/2", 8, 512, 1, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, false, true, 2>, k_sweep_cta<float, 4, 16, 1, 0, false, true, 2>},
-    {"k_sweep_cta R8 U1 L2-policy rows/4", 8, 512, 1, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, false, true, 4>, k_sweep_cta<float, 4, 16, 1, 0, false, true, 4>},
-    // CTA kernel with dynamic tile assignment (a launch-wide counter) instead of static row ranges
+    // ... with dynamic tile assignment (a launch-wide counter) instead of static row ranges
     {"k_sweep_cta R8 U1 L2-policy dynamic", 8, 512, 1, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, false, true, 1, true>, k_sweep_cta<float, 4, 16, 1, 0, false, true, 1, true>},
-    {"k_sweep_cta R4 U1 L2-policy dynamic", 4, 512, 1, 4, 1, 1, k_sweep_cta<double, 4, 16, 1, 0, false, true, 1, true>, k_sweep_cta<float, 4, 16, 1, 0, false, true, 1, true>},
     {"k_sweep_cta R4 U2 L2-policy dynamic", 4, 512, 1, 4, 2, 2, k_sweep_cta<double, 4, 16, 2, 0, false, true, 1, true>, k_sweep_cta<float, 4, 16, 2, 0, false, true, 1, true>},
 };
+// Round 1 also compiled item kernels R2 U4 / R4 U1 / 256 and 1024 threads, CTA kernels R8 256t / R4 U2 /
+// R2 U4 / R4 fused-exchange / R4 L2-keep / rows/4 / R4 U1 dynamic, and panel kernels x-evict_last / R8 /
+// R4 U2 / L2-keep / x-smem L2-keep: all slower than the instances above on every config they were
+// measured on (profiles/variants*_r01_*.jsonl, shard_variants_r02.jsonl), so they were removed.
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 }  // namespace
@@ -1268,7 +1326,7 @@ unsigned long long bounds_violations(bool reset) {
 int num_variants() { return kNumVariants; }
 const char* variant_name(int v) { return v >= 0 && v < kNumVariants ? kVariants[v].name : nullptr; }
 bool variant_is_cta(int v) { return kVariants[v].cta != 0; }
-int push_variant() { return 21; }
+int push_variant() { return 4; }
 // Shared memory of a variant: the CTA kernel's partial slots.
 size_t variant_smem(int v, int nchunks, int dtype, int chunk) {
   const Variant& V = kVariants[v];
@@ -1299,20 +1357,22 @@ int variant_rows_dt(int v, int dtype) { return dtype == JACOBI_F32 ? kVariants[v
 //   slower than the CTA kernel (c4 7092 / 7076, c3 6564 / 6676), so fp64 keeps the CTA kernel;
 // - fewer chunks: the item kernel R=8,U=1 (fp64) or R=4,U=1 (fp32).
 int default_variant(int dtype, int nchunks, int chunk, bool l2_keep, int64_t rows, int num_sms) {
-  if (dtype == JACOBI_F32 && nchunks >= 16) return variant_fits(18, nchunks, dtype, chunk) ? 18 : 12;
-  // Dynamic tiles of 4 rows, two column steps in flight (26) once a CTA has >= 32 such tiles: the
+  (void)l2_keep;  // every default instance with an L2 policy handles any kept share (0 included)
+  if (dtype == JACOBI_F32 && nchunks >= 16) return variant_fits(6, nchunks, dtype, chunk) ? 6 : 5;
+  // Dynamic tiles of 4 rows, two column steps in flight (10) once a CTA has >= 32 such tiles: the
   // expected idle of dynamic assignment, about half a tile, then undercuts the static partition's
-  // tail (a fixed minority of slower SMs).  µs per sweep, static default / 26 (R8 dynamic, 24, in
+  // tail (a fixed minority of slower SMs).  µs per sweep, static default / 10 (R8 dynamic, 9, in
   // between): n = 20000 491 / 485, 24576 688 / 681, 32768 1186 / 1188, 49152 2667 / 2631, 65536
   // 4704 / 4668; below the threshold it loses (16384: 302 / 305; 12288: 178 / 180).
-  if (dtype == JACOBI_F64 && !l2_keep && nchunks >= 16 && num_sms > 0 && rows >= (int64_t)32 * 4 * num_sms &&
-      variant_fits(26, nchunks, dtype, chunk))
-    return 26;
+  // (its L2 keep pattern numbers the units by global tile, so it holds with dynamic tiles too)
+  if (dtype == JACOBI_F64 && nchunks >= 16 && num_sms > 0 && rows >= (int64_t)32 * 4 * num_sms &&
+      variant_fits(10, nchunks, dtype, chunk))
+    return 10;
   // 16 < nchunks < 32, not a multiple of 16: (chunk, half-tile) units balance the 16 warps (n = 12288 /
   // 20000 / 24576: +3 / +4 / +2 %; from 40 chunks on, and for multiples of 16, whole-tile units win).
-  const int big = (dtype == JACOBI_F64 && nchunks > 16 && nchunks < 32 && nchunks % 16 != 0) ? 22 : 20;
+  const int big = (dtype == JACOBI_F64 && nchunks > 16 && nchunks < 32 && nchunks % 16 != 0) ? 8 : 7;
   if (variant_fits(big, nchunks, dtype, chunk)) return big;
-  return dtype == JACOBI_F32 ? 0 : 1;  // U = 1: fits every chunk
+  return dtype == JACOBI_F32 ? 0 : 1;  // item kernel: fits every chunk
 }
 int variant_rows(int v) { return kVariants[v].R; }
 int variant_threads(int v) { return kVariants[v].threads; }

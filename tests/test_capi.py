@@ -84,9 +84,9 @@ def test_no_cpu_fallback_without_gpu(jb):
 def test_variant_names_without_gpu(jb):
     """jacobi_variant_name is pure host code: names for the compiled variants, NULL past the end."""
     names = [jb.variant_name(v) for v in range(64)]
-    assert names[0].startswith("k_sweep") and names[7] == "k_sweep_cta R4 U1"
+    assert names[0].startswith("k_sweep") and names[3] == "k_sweep_cta R4 U1"
     known = [n for n in names if not n.startswith("variant ")]
-    assert len(known) >= 12 and len(set(known)) == len(known)
+    assert len(known) == 11 and len(set(known)) == len(known)
     assert jb._lib.jacobi_variant_name(-1) is None and jb._lib.jacobi_variant_name(10**6) is None
 
 
@@ -108,11 +108,12 @@ def test_bounds_checked_build_exports_the_same_abi(jb):
 
 
 def test_default_variant_indices_keep_their_names(jb):
-    """csrc/sweep.cu selects defaults by table index (default_variant, push_variant); the measurements
-    in DESIGN.md and profiles/ name variants by index too.  Appending variants must not shift them."""
-    expect = {1: "k_sweep R8 U1", 6: "k_sweep_cta R8 U1", 7: "k_sweep_cta R4 U1", 12: "k_sweep_panel R4 U1",
-              18: "k_sweep_panel R4 U1 x-smem", 20: "k_sweep_cta R8 U1 L2-policy",
-              21: "k_sweep_cta R8 U1 fused-exchange", 22: "k_sweep_cta R8 U1 L2-policy rows/2",
-              24: "k_sweep_cta R8 U1 L2-policy dynamic", 26: "k_sweep_cta R4 U2 L2-policy dynamic"}
+    """csrc/sweep.cu selects defaults by table index (default_variant, push_variant); DESIGN.md names
+    variants by these indices (round-2 table; profiles/*_r01_* files use the round-1 numbering, which
+    DESIGN.md §6 maps).  Appending variants must not shift them."""
+    expect = {0: "k_sweep R4 U2", 1: "k_sweep R8 U1", 2: "k_sweep_cta R8 U1", 3: "k_sweep_cta R4 U1",
+              4: "k_sweep_cta R8 U1 fused-exchange", 5: "k_sweep_panel R4 U1", 6: "k_sweep_panel R4 U1 x-smem",
+              7: "k_sweep_cta R8 U1 L2-policy", 8: "k_sweep_cta R8 U1 L2-policy rows/2",
+              9: "k_sweep_cta R8 U1 L2-policy dynamic", 10: "k_sweep_cta R4 U2 L2-policy dynamic"}
     for v, name in expect.items():
         assert jb.variant_name(v) == name, (v, jb.variant_name(v))

@@ -146,28 +146,30 @@ def test_gridsync_device_borrowed(jb, monkeypatch):
     assert r.iters == q.iters == 60 and np.array_equal(xo.cpu().numpy(), q.x)
 
 
-@pytest.mark.parametrize("n,tiles", [(2048, None), (3584, 3), (4096, 2), (4608, 2), (6144, 1), (16384, 0)])
-def test_l2_keep_whole_tiles(jb, n, tiles, monkeypatch):
-    """fp64 L2-kept share (profiles/l2keep_tiles_r01.md): whole 8-row tiles per CTA
-    within 0.78 x L2, every CTA (rows_min or rows_max) keeping the same number of tiles; A that fits
-    the budget entirely is kept whole; A > 4 x L2 streams (0)."""
+@pytest.mark.parametrize("n,f32", [(2048, False), (4096, False), (6144, False), (16384, False), (40000, False),
+                                   (8192, True)])
+def test_l2_keep_share_rule(jb, n, f32, monkeypatch):
+    """L2-resident share of A: per mille of the block's work units kept with evict_last =
+    floor(1000 x budget x L2 / A bytes), capped at 1000 (A within the budget is kept whole) and 0 below
+    20 (less than 2 % is not worth it); budget = 0.5 of the L2, JACOBI_L2_BUDGET / JACOBI_L2_KEEP override.
+    The same rule gives a rank's share from its m x n block (jacobi_plan_time_shard)."""
     import torch
     monkeypatch.delenv("JACOBI_L2_KEEP", raising=False)
-    G = torch.cuda.get_device_properties(0).multi_processor_count
-    dA = torch.eye(n, dtype=torch.float64, device="cuda") * 2.0
-    with jb.Plan(dA, n=n) as p:
-        keep = p.info.l2_keep_permille
-    if tiles is None:
-        assert keep == 1000
-        return
-    if tiles == 0:
-        assert keep == 0
-        return
-    for rows in (n // G, -(-n // G)):  # the kernels keep tile t of a CTA when t*8*1000 < rows*keep
-        kept = sum(1 for t in range(-(-rows // 8)) if t * 8 * 1000 < rows * keep)
-        assert kept == tiles, (n, rows, keep, kept)
+    monkeypatch.delenv("JACOBI_L2_BUDGET", raising=False)
     L2 = torch.cuda.get_device_properties(0).L2_cache_size
-    assert tiles * 8 * n * 8 * G <= 0.78 * L2 < (tiles + 1) * 8 * n * 8 * G
+    dA = torch.eye(n, dtype=torch.float32 if f32 else torch.float64, device="cuda") * 2.0
+    a_bytes = n * n * (4 if f32 else 8)
+    want = min(1000, int(1000 * 0.5 * L2 / a_bytes))
+    want = 0 if want < 20 else want
+    with jb.Plan(dA, n=n) as p:
+        assert p.info.l2_keep_permille == want, (n, p.info.l2_keep_permille, want)
+    monkeypatch.setenv("JACOBI_L2_BUDGET", "0.25")
+    with jb.Plan(dA, n=n) as p:
+        w = min(1000, int(1000 * 0.25 * L2 / a_bytes))
+        assert p.info.l2_keep_permille == (0 if w < 20 else w)
+    monkeypatch.setenv("JACOBI_L2_KEEP", "333")
+    with jb.Plan(dA, n=n) as p:
+        assert p.info.l2_keep_permille == 333
 
 
 @pytest.mark.parametrize("n,f32,path", [(256, False, "cluster"), (512, False, "cluster"), (600, False, "grid"),
@@ -315,13 +317,13 @@ def test_distinct_plans_on_distinct_threads(jb, monkeypatch):
 
 
 def test_dynamic_tile_plans_concurrently(jb, monkeypatch):
-    """Dynamic tile assignment (variant 26; DESIGN.md §6 tail paragraph): each plan owns its tile
+    """Dynamic tile assignment (variant 10; DESIGN.md §6 tail paragraph): each plan owns its tile
     counters, so two plans claiming tiles at once on different streams give the bits each gives
     alone, and the counters reset themselves between launches (many sweeps, several solves)."""
     import threading
     monkeypatch.delenv("JACOBI_PERSIST", raising=False)
     monkeypatch.setenv("JACOBI_PERSIST", "0")
-    monkeypatch.setenv("JACOBI_SWEEP_VARIANT", "26")
+    monkeypatch.setenv("JACOBI_SWEEP_VARIANT", "10")
     systems = [dominant(n, 700 + n, scale=1.05) for n in (4096, 6000)]
     alone = []
     for A, b, _ in systems:
@@ -331,7 +333,7 @@ def test_dynamic_tile_plans_concurrently(jb, monkeypatch):
     monkeypatch.delenv("JACOBI_SWEEP_VARIANT")
     with jb.Plan(systems[0][0]) as p:  # the static default of this size: same bits
         assert np.array_equal(p.solve(systems[0][1], None, 45, 0.0).x, alone[0])
-    monkeypatch.setenv("JACOBI_SWEEP_VARIANT", "26")
+    monkeypatch.setenv("JACOBI_SWEEP_VARIANT", "10")
     plans = [jb.Plan(A) for A, _, _ in systems]
     out, errs = [None] * len(systems), []
 

@@ -234,6 +234,8 @@ def test_device_borrowed_A_and_device_solve(jb):
         db = torch.from_numpy(b).cuda()
         dx0 = torch.zeros(n, dtype=torch.float64, device="cuda")
         dxo = torch.empty(n, dtype=torch.float64, device="cuda")
+        with pytest.raises(ValueError):  # the kernels write d_k into hist during the solve: too short = refused
+            p.solve_device(db, dx0, dxo, 20, 0.0, hist=torch.empty(19, dtype=torch.float64, device="cuda"))
         hist = torch.empty(20, dtype=torch.float64, device="cuda")
         r = p.solve_device(db, dx0, dxo, 20, 0.0, hist=hist)
         assert r.iters == 20 and rel_linf(dxo.cpu().numpy(), x_o) <= TOL64
@@ -420,14 +422,14 @@ def test_all_sweep_variants_bitwise_identical(jb, n, f32, monkeypatch):
     ref = None
     with jb.Plan(A) as p:
         nvar = p.info.num_variants  # the fused-exchange instance is never selected by JACOBI_SWEEP_VARIANT
-    assert nvar >= 12
+    assert nvar >= 11
     for v in range(nvar):
         monkeypatch.setenv("JACOBI_SWEEP_VARIANT", str(v))
         with jb.Plan(A) as p:
             assert p.info.num_variants == nvar
             r = p.solve(b, None, 12, 0.0, history=True)
             c = p.solve(b, None, 500, 1e-11)
-            if n == 8190 and v in (6, 7, 9, 10, 24, 26):
+            if n == 8190 and v in (2, 3, 7, 8, 9, 10):
                 for nb in (2, 3, 5):  # P12a through the CTA kernel, ragged rows per CTA
                     p.set_row_blocks(nb)
                     rb = p.solve(b, None, 12, 0.0, history=True)
