@@ -249,6 +249,19 @@ __device__ __forceinline__ bool sweep_prologue(const SweepArgs& a, int j, bool l
 // are not loaded (their sums are unused).
 // XSM: x^(k-1) of this chunk comes from shared memory, xs[col - c0] (else from global, xo[col]).
 // PIN: see the step loop below.
+// Row count nv in [1, R] as a compile-time constant: f(std::integral_constant<int, nv>).
+template <int N>
+struct NvConst { static constexpr int value = N; };
+template <int R, typename F>
+__device__ __forceinline__ void with_nv(const int nv, F&& f) {
+  if constexpr (R <= 1) {
+    f(NvConst<1>{});
+  } else {
+    if (nv >= R) f(NvConst<R>{});
+    else with_nv<R - 1>(nv, f);
+  }
+}
+
 template <typename T, int R, int U, int XL = 0, bool POL = false, bool XSM = false, bool PIN = false>
 __device__ __forceinline__ void accumulate_chunk(const T* const (&rowp)[R], const int nv,
                                                  const double* __restrict__ xo, const int64_t c0,
@@ -582,13 +595,13 @@ __device__ __forceinline__ unsigned long long cta_sweep(const SweepArgs& a, cons
       // Full units take the constant-row-count instance: with a run-time row count nvcc wraps each
       // row's load (and, for fp32, its converts) in a branch and keeps one A load in flight per warp
       // (c5 fell to 3.97 TB/s); with nv = R the loads are unconditional and software-pipelined.
+      // Partial units (a CTA's last tile: c2 has 27-28 rows per CTA, a c3 P = 8 shard 13-14) dispatch
+      // their row count to a compile-time constant too, so they keep every load in flight.
       check_tile<T, RG>(a, rp, c0, c1);
-      if (nvg == RG)
-        accumulate_chunk<T, RG, U, XL, POL, false, PIN>(rp, RG, xo, c0, c1, a.chunk, a.cend, g0 + rg * RG, lane, acc,
-                                                        pol);
-      else
-        accumulate_chunk<T, RG, U, XL, POL, false, PIN>(rp, nvg, xo, c0, c1, a.chunk, a.cend, g0 + rg * RG, lane, acc,
-                                                        pol);
+      with_nv<RG>(nvg, [&](auto nvc) {
+        accumulate_chunk<T, RG, U, XL, POL, false, PIN>(rp, decltype(nvc)::value, xo, c0, c1, a.chunk, a.cend,
+                                                        g0 + rg * RG, lane, acc, pol);
+      });
 #pragma unroll
       for (int r = 0; r < RG; ++r)
 #pragma unroll
@@ -626,34 +639,6 @@ __device__ __forceinline__ unsigned long long cta_sweep(const SweepArgs& a, cons
   return dmax;
 }
 
-// Start of a sweep kernel with static rows: while thread 0 runs the prologue (one L2 round trip for
-// the stop state), every warp asks L2 for the first a.pf_steps column steps of its first unit (A does
-// not depend on the previous sweep), so the unit's first loads find their lines in L2 or in flight
-// instead of paying the full HBM latency after the barrier.  pf_steps = 0 turns it off.
-template <typename T, int R, int NW, int GR>
-__device__ __forceinline__ void prefetch_first_unit(const SweepArgs& a, int cta, int ncta) {
-  if (a.pf_steps <= 0) return;
-  constexpr int E = VecOf<T>::E;
-  constexpr int RG = R / GR;
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (w >= a.nchunks * GR) return;
-  const int64_t rb = (int64_t)cta * a.m / ncta, re = (int64_t)(cta + 1) * a.m / ncta;
-  const int c = w / GR, rg = w % GR;
-  const int64_t c0 = a.col0 + (int64_t)c * a.chunk;
-  const int steps = min(a.pf_steps, a.chunk / (32 * E));
-  const T* A = static_cast<const T*>(a.A);
-  for (int r = 0; r < RG; ++r) {
-    const int64_t row = rb + rg * RG + r;
-    if (row >= re) break;
-    const T* rp = A + row * a.lda - a.col0;
-    for (int s = 0; s < steps; ++s) {
-      const int64_t col = c0 + (int64_t)(s * 32 + lane) * E;
-      if (col < a.cend && (lane & (128 / (E * sizeof(T)) - 1)) == 0)  // one request per 128-byte line
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + col));
-    }
-  }
-}
-
 template <typename T, int R, int NW, int U = 1, int XL = 0, bool PUSH = false, bool POL = false, int GR = 1,
           bool DYN = false>
 __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, const int j) {
@@ -663,7 +648,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_cta(const SweepArgs a, con
   __shared__ int s_go;
   __shared__ int s_tile[8];  // DYN: tile of sequence t at [t & 7]
   __shared__ long long s_k;
-  if constexpr (!DYN) prefetch_first_unit<T, R, NW, GR>(a, blockIdx.x, gridDim.x);
   if (threadIdx.x == 0) {
     s_go = sweep_prologue(a, j, blockIdx.x == 0, &s_k);
     if (DYN && s_go) {  // the tiles of sequences 0 .. kSlots-1
