@@ -687,3 +687,30 @@ def test_dynamic_tile_default_sizes_vs_oracle(jb, n, seed, max_iter, tol):
         r = p.solve(b, x0, max_iter, tol)
     assert (r.status, r.iters) == (st_o, it_o)
     assert rel_linf(r.x, x_o) <= TOL64
+
+
+def test_time_shard_hook(jb):
+    """jacobi_plan_time_shard (per-GPU shard measurement): runs the three modes on a rank's row block,
+    reports the variant its plan would pick, rejects bad arguments, and leaves the plan usable (the
+    next solve still matches the oracle)."""
+    import torch
+    n = 8192
+    A, b, _ = dominant(n, 404, scale=1.05)
+    dA = torch.from_numpy(A).cuda()
+    db = torch.from_numpy(b).cuda()
+    dx0 = torch.zeros(n, dtype=torch.float64, device="cuda")
+    with jb.Plan(dA, n=n) as p:
+        for P, r in ((1, 0), (4, 3), (8, 5)):
+            for mode in ("graph", "persistent", "persistent-push"):
+                ms, v = p.time_shard(db, dx0, P, r, 8, mode)
+                assert 0 < ms < 50, (P, r, mode, ms)
+                if mode == "graph":
+                    assert jb.variant_name(v).startswith("k_sweep")
+        for bad in ((3, 0), (4, 4), (0, 0)):  # 3 does not divide 8192; rank out of range; no ranks
+            with pytest.raises(jb.JacobiError) as e:
+                p.time_shard(db, dx0, bad[0], bad[1], 8, "graph")
+            assert e.value.status == jb.EINVAL
+        with pytest.raises(jb.JacobiError):
+            p.time_shard(db, dx0, 2, 0, 5000, "graph")  # more than 4096 sweeps
+        orc = oracle.jacobi(A, b, None, 30, 1e-11, nthreads=16, history=True)
+        match_oracle(p.solve(b, None, 30, 1e-11, history=True), orc)
