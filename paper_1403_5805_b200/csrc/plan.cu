@@ -104,8 +104,9 @@ static int check_last(const char* what) {
   } while (0)
 
 // L2-resident share of A (sweep variants with POL), per mille of the stored block's work units: a
-// budget of 50 % of the L2 (per-unit keep, µs per sweep at budget 0.5 / 0.65 / 0.78 / 0.9: c2 19.7 /
-// 19.6 / 22.6 / 26.4, c3 P = 8 shard 40.3 / 40.8 / 44.3 / 46.5, profiles/keep_budget_r02.txt) is kept across sweeps
+// budget of 55 % of the L2 (per-unit Weyl keep walked per warp, µs per sweep at budget 0.45 / 0.55 /
+// 0.6 / 0.65: c2 17.4 / 16.7 / 17.0 / 16.5, c3 P = 8 shard graph 35.5 / 34.6 / 34.8 / 36.1, P = 4 72.0 /
+// 72.5 / 73.8 / 74.6, profiles/keep_budget*_r02.txt) is kept across sweeps
 // with evict_last loads and the rest streams with evict_first, whenever that budget is at least 2 % of
 // the block (a smaller share is not worth giving up the dynamic-tile kernel of large blocks).  Each CTA
 // keeps that share of its own (tile, chunk) units (keep_unit in sweep.cu), so the kept bytes stay within
@@ -115,7 +116,7 @@ static int check_last(const char* what) {
 static int l2_keep_for(int l2, int64_t a_rows, int64_t a_cols, int dtype, int num_sms) {
   (void)num_sms;
   const double a_bytes = (double)a_rows * (double)a_cols * (dtype == JACOBI_F32 ? 4.0 : 8.0);
-  double budget = 0.5;
+  double budget = 0.55;
   if (const char* e = getenv("JACOBI_L2_BUDGET")) budget = atof(e);
   int keep = (l2 > 0 && a_bytes > 0) ? (int)std::min(1000.0, std::floor(1000.0 * budget * l2 / a_bytes)) : 0;
   if (keep < 20) keep = 0;
@@ -196,7 +197,6 @@ int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dty
   }
   choose_variant(p, a_cols, &p->variant, &p->grid);
   JLAST("sweep kernel occupancy query");
-  if (const char* e = getenv("JACOBI_GRID_PREFETCH")) p->pf_steps = std::max(0, atoi(e));
   p->x_len = round_up(n, 256) + 256;
   const int64_t nchunks = (a_cols + p->chunk - 1) / p->chunk;
   JCUDA(cudaMalloc(&p->diag, (size_t)m * 8));
@@ -517,7 +517,6 @@ static jacobi::SweepArgs sweep_args(const jacobi_plan* p, int blk) {
   const int R = jacobi::variant_rows_dt(p->variant, p->dtype);
   a.tiles = (int)((mb + R - 1) / R);
   a.l2_keep_pm = p->l2_keep_pm;
-  a.pf_steps = p->pf_steps;
   a.a_base = p->dA;
   a.a_elems = p->a_rows * p->lda;
   a.x_len = p->x_len;

@@ -722,7 +722,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync(const SweepArgs a
   const int64_t rb = (int64_t)blockIdx.x * a.m / gridDim.x;
   const int64_t re = (int64_t)(blockIdx.x + 1) * a.m / gridDim.x;
   const int64_t ntile = (re - rb + R - 1) / R;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nch = a.nchunks;
+  const int lane = threadIdx.x & 31;
   const bool l2 = a.norm == JACOBI_NORM_L2;
   for (int64_t k = k0;; ++k) {
     if (threadIdx.x == 0) {
@@ -803,24 +803,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync(const SweepArgs a
     if (threadIdx.x == 0) {
       __threadfence();
       atomicAdd(gbar, 1ull);
-    }
-    // While the grid barrier completes, ask L2 for this warp's first unit of the next sweep (A does
-    // not change between sweeps): its first loads then hit L2 instead of paying HBM latency (kept units
-    // are already resident; the request is a no-op for them).
-    if (a.pf_steps > 0 && w < nch * GR && rb < re) {
-      constexpr int E = VecOf<T>::E;
-      constexpr int RG = R / GR;
-      const int c = w / GR, rg = w % GR;
-      const int64_t cols = min((int64_t)a.chunk, a.cend - (a.col0 + (int64_t)c * a.chunk));
-      const T* base = static_cast<const T*>(a.A) + (int64_t)c * a.chunk;
-      constexpr int PER_LINE = 128 / (int)sizeof(T);
-      for (int r = 0; r < RG; ++r) {
-        const int64_t row = rb + rg * RG + r;
-        if (row >= re) break;
-        for (int64_t col = (int64_t)lane * PER_LINE; col < cols; col += 32 * PER_LINE)
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(base + row * a.lda + col));
-      }
-      (void)E;
     }
   }
 }

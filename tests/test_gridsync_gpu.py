@@ -151,7 +151,7 @@ def test_gridsync_device_borrowed(jb, monkeypatch):
 def test_l2_keep_share_rule(jb, n, f32, monkeypatch):
     """L2-resident share of A: per mille of the block's work units kept with evict_last =
     floor(1000 x budget x L2 / A bytes), capped at 1000 (A within the budget is kept whole) and 0 below
-    20 (less than 2 % is not worth it); budget = 0.5 of the L2, JACOBI_L2_BUDGET / JACOBI_L2_KEEP override.
+    20 (less than 2 % is not worth it); budget = 0.55 of the L2, JACOBI_L2_BUDGET / JACOBI_L2_KEEP override.
     The same rule gives a rank's share from its m x n block (jacobi_plan_time_shard)."""
     import torch
     monkeypatch.delenv("JACOBI_L2_KEEP", raising=False)
@@ -159,7 +159,7 @@ def test_l2_keep_share_rule(jb, n, f32, monkeypatch):
     L2 = torch.cuda.get_device_properties(0).L2_cache_size
     dA = torch.eye(n, dtype=torch.float32 if f32 else torch.float64, device="cuda") * 2.0
     a_bytes = n * n * (4 if f32 else 8)
-    want = min(1000, int(1000 * 0.5 * L2 / a_bytes))
+    want = min(1000, int(1000 * 0.55 * L2 / a_bytes))
     want = 0 if want < 20 else want
     with jb.Plan(dA, n=n) as p:
         assert p.info.l2_keep_permille == want, (n, p.info.l2_keep_permille, want)
