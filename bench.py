@@ -68,6 +68,8 @@ def parse():
     ap.add_argument("--no-fused", action="store_true", help="N > 1: skip the fused-exchange side measurement")
     ap.add_argument("--fused-timeout", type=float, default=180.0,
                     help="watchdog (s) of the fused-exchange side measurement")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="test hook: take the N > 1 code path (distributed plans, fused-exchange leg) even at N = 1")
     ap.add_argument("--launcher-dry-run", action="store_true",
                     help="spawn the ranks (gloo, no GPU work) and report what was spawned: tests the launcher")
     ap.add_argument("--out", default=None, help="also append the JSON line to this file")
@@ -467,7 +469,10 @@ def main():
         print(f"bench.py: rank {rank} needs CUDA device {local}; {torch.cuda.device_count()} visible", file=sys.stderr)
         return 2
     torch.cuda.set_device(local)
-    if world > 1:
+    dist_on = world > 1 or args.force_dist
+    if dist_on:
+        if world == 1 and "MASTER_PORT" not in os.environ:
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()), RANK="0", WORLD_SIZE="1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = g.CONFIGS[gname]
     n = cfg.n
@@ -480,7 +485,7 @@ def main():
     row0, m = jb.partition(n, world, rank)
 
     # ---- resident inputs (device twin of the generator; identical bits to the host generator)
-    cols = world > 1 and args.exchange == "cols"
+    cols = dist_on and args.exchange == "cols"
     db = torch.empty(m, dtype=torch.float64, device="cuda")
     if cols:  # column slab [row0, row0 + m) of all n rows: generate all rows, keep the slab
         dA = torch.empty((n, m), dtype=dt, device="cuda")
@@ -510,11 +515,11 @@ def main():
 
     def planted_error():  # max over ranks
         e = torch.tensor([local_planted_error()], dtype=torch.float64, device="cuda")
-        if world > 1:
+        if dist_on:
             dist.all_reduce(e, op=dist.ReduceOp.MAX)
         return float(e.item())
 
-    if world > 1:
+    if dist_on:
         from paper_1403_5805_b200.dist import dist_plan
         plan = dist_plan(dA, n, stream=sh, layout="cols" if cols else "rows", p2p=args.exchange == "p2p")
     else:
@@ -531,7 +536,7 @@ def main():
     info = plan.info
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
-        if world > 1:
+        if dist_on:
             dist.barrier()
         torch.cuda.synchronize()
         e0.record(stream)
@@ -542,10 +547,10 @@ def main():
             launches += li.sweeps_launched + li.sweeps_launched // K + 1  # sweeps + k_advance + k_prepare
         e1.record(stream)
         torch.cuda.synchronize()
-        if world > 1:
+        if dist_on:
             dist.barrier()
     ms = e0.elapsed_time(e1)
-    if world > 1:
+    if dist_on:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -558,7 +563,7 @@ def main():
     # per-kernel timing (untimed cross-check: events around each sweep kernel alone)
     kms = plan.time_sweeps(db, dx0, min(sweeps, 20))
     kernel_ms = float(np.median(kms[1:])) if len(kms) > 1 else float(kms[0])
-    if world > 1:
+    if dist_on:
         t = torch.tensor([kernel_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         kernel_ms = float(t.item())
@@ -579,7 +584,7 @@ def main():
         "config": {"workload": desc, "n": n, "sweeps_per_step": sweeps, "tol": tol,
                    "parallelism": (f"row-block x{world}" if not cols else f"column-slab x{world}") + (
                        {"nccl": " + NCCL allgather/allreduce", "p2p": " + fused NVLink push exchange (NEXT-1)",
-                        "cols": " + NCCL reduce-scatter/allreduce (NEXT-4)"}[args.exchange] if world > 1 else ""),
+                        "cols": " + NCCL reduce-scatter/allreduce (NEXT-4)"}[args.exchange] if dist_on else ""),
                    "l2": "A per GPU >> 126 MB L2; each sweep streams A from HBM (no flush needed)",
                    "graph_batch": K, "chunk_cols": info.chunk_cols, "rows_per_warp": info.rows_per_warp,
                    "grid": f"{info.grid_ctas}x{info.threads_per_cta}"},
@@ -603,7 +608,7 @@ def main():
     }
 
     # ---- N > 1: the fused NVLink exchange as a side measurement, under a watchdog
-    if world > 1 and args.exchange == "nccl" and not args.no_fused and not cols:
+    if dist_on and args.exchange == "nccl" and not args.no_fused and not cols:
         done = threading.Event()
 
         def watchdog():
@@ -640,7 +645,7 @@ def main():
         it = ctypes.c_int64()
 
         def e2e_step():
-            if world == 1:
+            if not dist_on:
                 st = solve_fn(n, hA.data_ptr(), hb.data_ptr(), hx0.data_ptr(), sweeps, tol, hx.data_ptr(),
                               ctypes.byref(it))
                 assert st == jb.MAX_ITER and it.value == sweeps, (st, jb.last_error())
@@ -652,14 +657,14 @@ def main():
 
         e2e_step()  # warm-up
         torch.cuda.synchronize()
-        if world > 1:
+        if dist_on:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             e2e_step()
         torch.cuda.synchronize()
         el = time.perf_counter() - t0
-        if world > 1:
+        if dist_on:
             t = torch.tensor([el], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
@@ -667,11 +672,11 @@ def main():
                        "h2d_bytes_per_step": int(world * (hA.numel() * hA.element_size() + 8 * m + 8 * n)),
                        "d2h_bytes_per_step": int(world * (8 * n + 48)), "steps": args.e2e_steps,
                        "api": ("jacobi_solve (C-ABI one-shot, host pinned buffers: plan setup + H2D + sweeps + D2H "
-                               "per step)" if world == 1 else
+                               "per step)" if not dist_on else
                                "jacobi_dist_plan_create + jacobi_plan_solve per step on every rank (host row block, "
                                "H2D, NCCL comm init, sweeps, D2H); wall time, max over ranks")}
 
-    if world == 1 and not args.no_configs:
+    if not dist_on and not args.no_configs:
         line["other_configs"] = other_configs(jb, g, torch, stream)
 
     # ---- CPU oracle on rank 0's host cores (every N); reuses the e2e host A when it is the whole system
@@ -690,7 +695,7 @@ def main():
         if args.out:
             with open(args.out, "a") as f:
                 f.write(s + "\n")
-    if world > 1:
+    if dist_on:
         dist.barrier()
         dist.destroy_process_group()
     return 0

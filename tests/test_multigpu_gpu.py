@@ -34,11 +34,14 @@ def _rel(x, ref):
     return np.max(np.abs(x - ref)) / np.max(np.abs(ref))
 
 
-@pytest.mark.parametrize("P", [2, 3, 4, 8])
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 8])
 def test_multi_gpu_exchanges_vs_one_gpu_and_oracle(P, tmp_path):
+    """P = 1 runs the same harness as one torchrun process on one GPU (NCCL communicator of one rank,
+    IPC handles of its own buffers): it checks the launcher, the worker and the comparisons wherever
+    the multi-GPU cases skip."""
     ng = _gpus()
-    if ng < 2:
-        pytest.skip(f"needs >= 2 GPUs ({ng} visible)")
+    if ng < 1:
+        pytest.skip("needs a GPU")
     if P > min(8, ng):
         pytest.skip(f"P = {P} needs {P} GPUs ({ng} visible)")
     import socket
@@ -78,3 +81,24 @@ def test_multi_gpu_exchanges_vs_one_gpu_and_oracle(P, tmp_path):
                     o = one[(mi, tol)]
                     assert (st, it) == (o.status, o.iters) and np.array_equal(x, o.x) and np.array_equal(h, o.hist), \
                         (P, key)
+
+
+def test_bench_distributed_path_on_one_rank():
+    """bench.py's N > 1 code path (distributed plan with the NCCL exchange as the headline, then the
+    fused-exchange side leg behind its votes and watchdog) taken at N = 1 with --force-dist, on the
+    small c2 workload: one JSON line, planted solution reached, a fused-exchange value."""
+    import json
+    if _gpus() < 1:
+        pytest.skip("needs a GPU")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--workload", "c2", "--force-dist", "--steps", "2",
+                        "--warmup", "3", "--no-e2e", "--no-cpu-baseline"], capture_output=True, text=True,
+                       timeout=600, cwd=ROOT, env={k: v for k, v in os.environ.items()
+                                                    if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_PORT")})
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 1 and "NCCL" in d["config"]["parallelism"] and d["value"] > 0
+    assert d["check"]["planted_max_abs_err"] <= 1e-12
+    fx = d["fused_exchange"]
+    assert "error" not in fx and fx["value"] > 0, fx
