@@ -107,7 +107,7 @@ const char* variant_name(int variant);
 int default_variant(int dtype, int nchunks, int chunk, bool l2_keep, int64_t rows, int num_sms);
 bool variant_is_cta(int variant);
 bool variant_is_push(int variant);
-int push_variant();
+int push_variant(int dtype, int64_t rows, int num_sms);
 bool variant_fits(int variant, int nchunks, int dtype, int chunk);
 int variant_rows_dt(int variant, int dtype);
 int variant_rows(int variant);

@@ -323,9 +323,10 @@ static unsigned long long peer_wait_ns() {
   return (unsigned long long)std::max(1ll, ms) * 1000000ull;
 }
 
-static int p2p_pick_variant(jacobi_plan* p) {
+static int p2p_pick_variant(jacobi_plan* p, int64_t rows_per_rank) {
   const int nch = (int)((p->n + p->chunk - 1) / p->chunk);
-  const int v = jacobi::push_variant();
+  int v = jacobi::push_variant(p->dtype, rows_per_rank, p->num_sms);
+  if (!jacobi::variant_fits(v, nch, p->dtype, p->chunk)) v = jacobi::push_variant(p->dtype, 0, p->num_sms);
   if (!jacobi::variant_fits(v, nch, p->dtype, p->chunk))
     return jacobi_set_error(JACOBI_EINVAL, "fused exchange needs the CTA sweep kernel (n with >= 16 chunks)");
   p->variant = v;
@@ -337,7 +338,7 @@ extern "C" int jacobi_plan_set_p2p_emulation(jacobi_plan* p, int P) {
   if (!p || P < 1 || P > jacobi::kMaxPeers || p->comm || p->colwise || p->colblocks > 1 || p->m % P != 0 ||
       p->norm != JACOBI_NORM_MAX || p->p2p)
     return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_set_p2p_emulation: 1-GPU max-norm plan, P in [1, 8] dividing n, once");
-  JRC(p2p_pick_variant(p));
+  JRC(p2p_pick_variant(p, p->m / P));
   if (P > 1) {
     JCUDA(cudaMalloc(&p->ex_x, (size_t)(P - 1) * 2 * p->x_len * 8));
     JCUDA(cudaMemsetAsync(p->ex_x, 0, (size_t)(P - 1) * 2 * p->x_len * 8, p->stream));
@@ -386,7 +387,7 @@ extern "C" int jacobi_plan_ipc_attach(jacobi_plan* p, const void* all_handles) {
   if (!p || !all_handles || !p->comm || p->colwise || p->nranks > jacobi::kMaxPeers || p->norm != JACOBI_NORM_MAX ||
       p->p2p)
     return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_ipc_attach: row-wise max-norm distributed plan, <= 8 ranks, once");
-  JRC(p2p_pick_variant(p));
+  JRC(p2p_pick_variant(p, p->m));
   jacobi::PeerArgs a;
   std::memset(&a, 0, sizeof(a));
   a.P = p->nranks;

@@ -1288,6 +1288,8 @@ const Variant kVariants[] = {
     // ... with dynamic tile assignment (a launch-wide counter) instead of static row ranges
     {"k_sweep_cta R8 U1 L2-policy dynamic", 8, 512, 1, 4, 1, 1, k_sweep_cta<double, 8, 16, 1, 0, false, true, 1, true>, k_sweep_cta<float, 4, 16, 1, 0, false, true, 1, true>},
     {"k_sweep_cta R4 U2 L2-policy dynamic", 4, 512, 1, 4, 2, 2, k_sweep_cta<double, 4, 16, 2, 0, false, true, 1, true>, k_sweep_cta<float, 4, 16, 2, 0, false, true, 1, true>},
+    // fused-exchange instance of 10 (large row blocks per rank, e.g. c4 at P <= 2)
+    {"k_sweep_cta R4 U2 dynamic fused-exchange", 4, 512, 2, 4, 2, 2, k_sweep_cta<double, 4, 16, 2, 3, true, true, 1, true>, k_sweep_cta<float, 4, 16, 2, 3, true, true, 1, true>},
 };
 // Round 1 also compiled item kernels R2 U4 / R4 U1 / 256 and 1024 threads, CTA kernels R8 256t / R4 U2 /
 // R2 U4 / R4 fused-exchange / R4 L2-keep / rows/4 / R4 U1 dynamic, and panel kernels x-evict_last / R8 /
@@ -1315,7 +1317,11 @@ unsigned long long bounds_violations(bool reset) {
 int num_variants() { return kNumVariants; }
 const char* variant_name(int v) { return v >= 0 && v < kNumVariants ? kVariants[v].name : nullptr; }
 bool variant_is_cta(int v) { return kVariants[v].cta != 0; }
-int push_variant() { return 4; }
+// Fused-exchange kernel for a rank's row block: the dynamic-tile instance under the same rule as
+// default_variant (>= 32 four-row tiles per CTA), else the static R8 instance.
+int push_variant(int dtype, int64_t rows, int num_sms) {
+  return (dtype == JACOBI_F64 && num_sms > 0 && rows >= (int64_t)32 * 4 * num_sms) ? 11 : 4;
+}
 // Shared memory of a variant: the CTA kernel's partial slots.
 size_t variant_smem(int v, int nchunks, int dtype, int chunk) {
   const Variant& V = kVariants[v];

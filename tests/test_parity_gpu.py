@@ -714,3 +714,33 @@ def test_time_shard_hook(jb):
             p.time_shard(db, dx0, 2, 0, 5000, "graph")  # more than 4096 sweeps
         orc = oracle.jacobi(A, b, None, 30, 1e-11, nthreads=16, history=True)
         match_oracle(p.solve(b, None, 30, 1e-11, history=True), orc)
+
+
+def test_fused_exchange_dynamic_tiles(jb):
+    """A rank with >= 32 four-row tiles per CTA runs the dynamic-tile fused-exchange kernel (variant 11):
+    bitwise equal to the plain plan and matching the oracle, as one emulated rank and as the real IPC
+    path with one rank; two emulated ranks of the same system take the static fused kernel (4)."""
+    import torch
+    n = 20480
+    rng = np.random.default_rng(2048)
+    A = rng.uniform(-1, 1, (n, n))
+    np.fill_diagonal(A, 0.0)
+    np.fill_diagonal(A, np.abs(A).sum(1) * 1.05)
+    b = rng.uniform(-1, 1, n)
+    orc = oracle.jacobi(A, b, None, 200, 1e-11, nthreads=16, history=True)
+    with jb.Plan(A) as p0:
+        ref = p0.solve(b, None, 200, 1e-11, history=True)
+    for P, want in ((1, 11), (2, 4)):
+        with jb.Plan(A) as p:
+            p.set_p2p_emulation(P)
+            assert p.info.variant == want, (P, p.info.variant)
+            r = p.solve(b, None, 200, 1e-11, history=True)
+            match_oracle(r, orc)
+            assert np.array_equal(r.x, ref.x) and np.array_equal(r.hist, ref.hist)
+    dA = torch.from_numpy(A).cuda()
+    with jb.Plan(dA, n=n, dist=(jb.nccl_unique_id(), 0, 1)) as p:
+        p.ipc_attach(p.ipc_export())
+        assert p.info.variant == 11
+        r = p.solve(b, None, 200, 1e-11, history=True)
+        match_oracle(r, orc)
+        assert np.array_equal(r.x, ref.x)
