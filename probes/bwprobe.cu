@@ -24,7 +24,7 @@ __device__ __forceinline__ void ld256(const void* p, double& a, double& b, doubl
 
 // mode 0: 128-bit nc no_allocate; 1: + L2 evict_first policy; 2: 256-bit
 template <int U, int MODE>
-__global__ void k_read(const double* __restrict__ buf, size_t nelem, double* out) {
+__global__ void k_read(const double* __restrict__ buf, size_t nelem, double* out, int reps = 1) {
   uint64_t pol = 0;
   if (MODE == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   const int V = (MODE == 2) ? 4 : 2;
@@ -32,6 +32,7 @@ __global__ void k_read(const double* __restrict__ buf, size_t nelem, double* out
   size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   size_t stride = (size_t)gridDim.x * blockDim.x;
   double acc = 0.0;
+  for (int rep = 0; rep < reps; ++rep) {  // several passes in one launch (L2-resident buffers)
   size_t i = tid;
   for (; i + (U - 1) * stride < nvec; i += U * stride) {
     double v[U][V];
@@ -51,6 +52,7 @@ __global__ void k_read(const double* __restrict__ buf, size_t nelem, double* out
     double a, b;
     ld128(buf + i * V, a, b);
     acc += a + b;
+  }
   }
   if (acc == 12345.678) out[0] = acc;  // keep loads alive
 }
@@ -139,7 +141,10 @@ static double time_best(F f, int reps) {
 
 int main(int argc, char** argv) {
   size_t gib = argc > 1 ? atoll(argv[1]) : 32;
-  size_t nbytes = gib << 30, n = nbytes / 8;
+  // "probes/bwprobe N mib": an N MiB buffer — L2-resident after the first pass when N is below ~100,
+  // i.e. the L2-hit streaming rate of the same load flavours
+  const bool mib = argc > 2 && argv[2][0] == 'm';
+  size_t nbytes = mib ? gib << 20 : gib << 30, n = nbytes / 8;
   int nsm; CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
   int bus, memclk, l2;
   CK(cudaDeviceGetAttribute(&bus, cudaDevAttrGlobalMemoryBusWidth, 0));
@@ -154,8 +159,9 @@ int main(int argc, char** argv) {
     printf("{\"probe\":\"%s\",\"tpb\":%d,\"blocks_per_sm\":%d,\"ms\":%.3f,\"gbs\":%.1f}\n", name, tpb, bps, ms, bytes / ms / 1e6);
     fflush(stdout);
   };
-#define RUN(U, MODE, TPB, BPS) { double ms = time_best([&]{ k_read<U, MODE><<<nsm * BPS, TPB>>>(buf, n, out); }, 5); \
-    char nm[64]; snprintf(nm, 64, "read_m%d_u%d", MODE, U); rep(nm, TPB, BPS, ms, (double)nbytes); }
+  const int passes = mib ? 20 : 1;  // small buffers: 20 passes per launch so the launch does not dominate
+#define RUN(U, MODE, TPB, BPS) { double ms = time_best([&]{ k_read<U, MODE><<<nsm * BPS, TPB>>>(buf, n, out, passes); }, 5); \
+    char nm[64]; snprintf(nm, 64, "read_m%d_u%d", MODE, U); rep(nm, TPB, BPS, ms, (double)nbytes * passes); }
   RUN(4, 0, 256, 8); RUN(8, 0, 256, 8); RUN(16, 0, 256, 4); RUN(8, 0, 512, 4); RUN(8, 0, 1024, 2);
   RUN(4, 0, 512, 4); RUN(2, 0, 1024, 2);
   RUN(8, 1, 256, 8); RUN(16, 1, 256, 4);
