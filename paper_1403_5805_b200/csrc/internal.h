@@ -78,7 +78,6 @@ struct SweepArgs {
   int nchunks;              // ceil(n / chunk)
   int tiles;                // ceil(m / R)
   int l2_keep_pm;           // per-mille of the work units loaded with L2 evict_last (variants with POL)
-  int pf_steps;             // persistent solver experiment: L1 prefetch of the next sweep's first steps
   const void* a_base;       // the stored block's allocation and its extent in elements, and the
   int64_t a_elems, x_len;   // x buffers' length: checked by the JACOBI_BOUNDS_CHECK build only
 };
@@ -177,7 +176,6 @@ struct jacobi_plan {
   int variant = 0;               // sweep kernel variant (R, U, threads); default per dtype, JACOBI_SWEEP_VARIANT overrides
   int batch = 32;                // sweeps per graph batch
   int l2_keep_pm = 0;            // per-mille of A's work units kept L2-resident (evict_last) by the POL variants
-  int pf_steps = 0;              // persistent solver experiment (JACOBI_GRID_PREFETCH)
   int grid_G = 0;                // persistent grid solver: CTAs (0 = not used)
   size_t grid_smem = 0;
   unsigned long long* gbar = nullptr;  // its grid-barrier counter (zeroed per solve)

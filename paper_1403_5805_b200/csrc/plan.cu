@@ -197,7 +197,6 @@ int plan_init_common(jacobi_plan* p, int64_t n, int64_t m, int64_t row0, int dty
   }
   choose_variant(p, a_cols, &p->variant, &p->grid);
   JLAST("sweep kernel occupancy query");
-  if (const char* e = getenv("JACOBI_GRID_PREFETCH")) p->pf_steps = std::max(0, atoi(e));
   p->x_len = round_up(n, 256) + 256;
   const int64_t nchunks = (a_cols + p->chunk - 1) / p->chunk;
   JCUDA(cudaMalloc(&p->diag, (size_t)m * 8));
@@ -519,7 +518,6 @@ static jacobi::SweepArgs sweep_args(const jacobi_plan* p, int blk) {
   const int R = jacobi::variant_rows_dt(p->variant, p->dtype);
   a.tiles = (int)((mb + R - 1) / R);
   a.l2_keep_pm = p->l2_keep_pm;
-  a.pf_steps = p->pf_steps;
   a.a_base = p->dA;
   a.a_elems = p->a_rows * p->lda;
   a.x_len = p->x_len;

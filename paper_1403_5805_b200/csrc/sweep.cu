@@ -722,7 +722,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync(const SweepArgs a
   const int64_t rb = (int64_t)blockIdx.x * a.m / gridDim.x;
   const int64_t re = (int64_t)(blockIdx.x + 1) * a.m / gridDim.x;
   const int64_t ntile = (re - rb + R - 1) / R;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nch = a.nchunks;
+  const int lane = threadIdx.x & 31;
   const bool l2 = a.norm == JACOBI_NORM_L2;
   for (int64_t k = k0;; ++k) {
     if (threadIdx.x == 0) {
@@ -803,25 +803,6 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync(const SweepArgs a
     if (threadIdx.x == 0) {
       __threadfence();
       atomicAdd(gbar, 1ull);
-    }
-    // Experiment (JACOBI_GRID_PREFETCH = 1 | 2): while the grid barrier completes, pull this warp's
-    // first unit of the next sweep (first column step, or the whole unit) into L1, so the loads after
-    // the barrier do not start with a full memory round trip.
-    if (a.pf_steps > 0 && w < nch * GR && rb < re) {
-      constexpr int E = VecOf<T>::E;
-      constexpr int RG = R / GR;
-      const int c = w / GR, rg = w % GR;
-      const int64_t c0 = a.col0 + (int64_t)c * a.chunk;
-      const int64_t cols = min((int64_t)a.chunk, a.cend - c0);
-      const int64_t ncols = min(cols, (int64_t)a.pf_steps * 32 * E);
-      const T* Ab = static_cast<const T*>(a.A) - a.col0;
-      constexpr int PER_LINE = 128 / (int)sizeof(T);
-      for (int r = 0; r < RG; ++r) {
-        const int64_t row = rb + rg * RG + r;
-        if (row >= re) break;
-        for (int64_t col = (int64_t)lane * PER_LINE; col < ncols; col += 32 * PER_LINE)
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(Ab + row * a.lda + c0 + col));
-      }
     }
   }
 }
