@@ -111,8 +111,8 @@ static int check_last(const char* what) {
 // the block (a smaller share is not worth giving up the dynamic-tile kernel of large blocks).  Each CTA
 // keeps that share of its own (tile, chunk) units (keep_unit in sweep.cu), so the kept bytes stay within
 // the budget at any row length.  A function of the block's shape only: a P-rank plan's rank applies it
-// to its m x n block (c3: P = 1/2/4/8 keep 4.5 / 9 / 18 / 36 % of the block).  JACOBI_L2_KEEP (per
-// mille) and JACOBI_L2_BUDGET (fraction of the L2) override.
+// to its m x n block (c2 keeps 54 %; c3 at P = 1/2/4/8 keeps 3.3 / 6.7 / 13.5 / 27 % of the block; c4 and
+// c5 blocks are too large).  JACOBI_L2_KEEP (per mille) and JACOBI_L2_BUDGET (fraction of the L2) override.
 static int l2_keep_for(int l2, int64_t a_rows, int64_t a_cols, int dtype, int num_sms) {
   (void)num_sms;
   const double a_bytes = (double)a_rows * (double)a_cols * (dtype == JACOBI_F32 ? 4.0 : 8.0);
