@@ -16,8 +16,11 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# JACOBI_LIB=check loads the bounds-checked build (make lib-check) — same API, checks in the kernels.
-LIB_PATH = os.path.join(_HERE, "libjacobi_check.so" if os.environ.get("JACOBI_LIB") == "check" else "libjacobi.so")
+# JACOBI_LIB=check loads the bounds-checked build (make lib-check) — same API, checks in the kernels;
+# JACOBI_LIB=<path>.so loads a probe build of the same sources (e.g. -DJACOBI_SM_TIMING).
+_LIBSEL = os.environ.get("JACOBI_LIB", "")
+LIB_PATH = (os.path.join(_HERE, "libjacobi_check.so") if _LIBSEL == "check" else
+            os.path.abspath(_LIBSEL) if _LIBSEL.endswith(".so") else os.path.join(_HERE, "libjacobi.so"))
 
 CONVERGED, MAX_ITER = 0, 1
 EINVAL, EZERODIAG, ENONFINITE, ENOMEM, ECUDA, ENCCL, EINDIVISIBLE = -1, -2, -3, -4, -5, -6, -7

@@ -166,6 +166,7 @@ __device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long
 // finishes across SMs and dies.
 #ifdef JACOBI_SM_TIMING
 __device__ unsigned long long g_smt[3 * 4096];
+__device__ int g_rot = 0;  // row-panel kernel: CTA b takes the rows of block (b + g_rot) mod G
 #define SMT_BEGIN()                              \
   unsigned long long smt0_ = 0;                  \
   if (threadIdx.x == 0) smt0_ = global_ns()
@@ -1017,8 +1018,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_panel(const SweepArgs a, c
   double* __restrict__ xn = (k & 1) ? a.x1buf : a.x0buf;        // x^(k)
   const T* __restrict__ A = static_cast<const T*>(a.A);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t rb = (int64_t)blockIdx.x * a.m / gridDim.x;
-  const int64_t re = (int64_t)(blockIdx.x + 1) * a.m / gridDim.x;
+#ifdef JACOBI_SM_TIMING
+  const int64_t cb = (blockIdx.x + g_rot) % gridDim.x;  // probe build: rotate the CTA -> row-block map
+#else
+  const int64_t cb = blockIdx.x;
+#endif
+  const int64_t rb = cb * a.m / gridDim.x;
+  const int64_t re = (cb + 1) * a.m / gridDim.x;
   const int64_t wb = rb + (re - rb) * w / NW, we = rb + (re - rb) * (w + 1) / NW;
   // x ring schedule: round t = every warp's t-th tile; arrivals of round t = warps with > t tiles.
   XRing ring{};
@@ -1375,6 +1381,9 @@ int variant_threads(int v) { return kVariants[v].threads; }
 #ifdef JACOBI_SM_TIMING
 extern "C" int jacobi_debug_sm_times(unsigned long long* out, int nctas) {
   return cudaMemcpyFromSymbol(out, g_smt, sizeof(unsigned long long) * 3 * (size_t)nctas) == cudaSuccess ? 0 : -5;
+}
+extern "C" int jacobi_debug_set_rotation(int rot) {
+  return cudaMemcpyToSymbol(g_rot, &rot, sizeof(rot)) == cudaSuccess ? 0 : -5;
 }
 #endif
 
