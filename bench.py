@@ -316,6 +316,10 @@ def reference_arm(args, rank):
 # ----------------------------------------------------------------------------- other configs (N = 1)
 OTHER_RUNS = (("c1", 200, 0.0), ("c1", 200, 1e-12), ("c2", 500, 0.0), ("c3", 5000, 1e-10), ("c3", 1000, 0.0),
               ("c5", 2000, 1e-6), ("c5", 100, 0.0))
+# The NEXT rows measured on c3 (informational): the paper's Euclidean stop rule (NEXT-2: per-sweep dx^2
+# block tree + final sum) and the column-wise scheme's slab kernels as 8 slabs on one GPU (NEXT-4: 8
+# slab GEMVs writing row sums + the column-sum epilogue), each over 1000 fixed sweeps.
+NEXT_RUNS = (("c3", 1000, 0.0, "l2", 1), ("c3", 1000, 0.0, "max", 8))
 
 
 def other_configs(jb, g, torch, stream):
@@ -334,8 +338,12 @@ def other_configs(jb, g, torch, stream):
         dxo = torch.empty(n, dtype=torch.float64, device="cuda")
         with jb.Plan(dA, n=n, stream=sh) as p:
             inf = p.info
-            for _, max_iter, tol in (r for r in OTHER_RUNS if r[0] == name):
+            runs = [(mi, tol, "max", 1) for nm, mi, tol in OTHER_RUNS if nm == name]
+            runs += [(mi, tol, norm, cb) for nm, mi, tol, norm, cb in NEXT_RUNS if nm == name]
+            for max_iter, tol, norm, colblocks in runs:
                 p.set_batch(20 if max_iter % 20 == 0 else 32)
+                p.set_norm(norm)
+                p.set_col_blocks(colblocks)
                 r = p.solve_device(db, dx0, dxo, max_iter, tol)
                 best = None
                 for _ in range(3):
@@ -353,7 +361,12 @@ def other_configs(jb, g, torch, stream):
                             "effective_gbs": round(inf.bytes_per_sweep * its / 1e9, 1),
                             "path": (f"cluster x{inf.cluster_ctas}" if inf.cluster_ctas else
                                      f"persistent x{inf.persistent_ctas}: cta_sweep" if inf.persistent_ctas else
-                                     f"graph: {jb.variant_name(inf.variant)}")})
+                                     f"graph: {jb.variant_name(inf.variant)}")
+                            + ("" if norm == "max" else " + Euclidean rule (NEXT-2)")
+                            + ("" if colblocks == 1 else f"; as {colblocks} column slabs of {n // colblocks} columns on "
+                                                          "one GPU (NEXT-4 emulation: slab GEMVs + column-sum epilogue)")})
+            p.set_norm("max")
+            p.set_col_blocks(1)
         del dA, db
         torch.cuda.empty_cache()
     return out
