@@ -341,7 +341,9 @@ def other_configs(jb, g, torch, stream):
             runs = [(mi, tol, "max", 1) for nm, mi, tol in OTHER_RUNS if nm == name]
             runs += [(mi, tol, norm, cb) for nm, mi, tol, norm, cb in NEXT_RUNS if nm == name]
             for max_iter, tol, norm, colblocks in runs:
-                p.set_batch(20 if max_iter % 20 == 0 else 32)
+                # fixed runs: batches that divide the sweep count; tol runs: short loop bodies (a stop
+                # inside a batch leaves its remaining sweeps as no-ops)
+                p.set_batch(8 if tol > 0 else (20 if max_iter % 20 == 0 else 32))
                 p.set_norm(norm)
                 p.set_col_blocks(colblocks)
                 r = p.solve_device(db, dx0, dxo, max_iter, tol)

@@ -90,6 +90,8 @@ unsigned long long bounds_violations(bool reset);
 // Launchers (sweep.cu).  Return cudaGetLastError() of the launch.
 cudaError_t launch_sweep(int dtype, int variant, const SweepArgs& a, int j, int grid, cudaStream_t s);
 cudaError_t launch_advance(State* st, unsigned long long* dslot, int K, cudaStream_t s);
+cudaError_t launch_advance_while(State* st, unsigned long long* dslot, int K, cudaGraphConditionalHandle h,
+                                 cudaStream_t s);
 cudaError_t launch_setup_diag(int dtype, const void* A, int64_t lda, int64_t m, int64_t row0,
                               double* diag, unsigned long long* zero_min, cudaStream_t s);
 cudaError_t launch_scan_nonfinite_A(int dtype, const void* A, int64_t lda, int64_t m, int64_t n,
@@ -209,6 +211,7 @@ struct jacobi_plan {
   ncclComm_t comm = nullptr;     // distributed plans only
   cudaGraphExec_t graph = nullptr;
   int graph_batch = 0, graph_nblocks = 0, graph_norm = -1, graph_colblocks = 0;
+  bool graph_while = false;      // the graph is one device-side while loop over batches (no host polling)
   int64_t sweeps_launched = 0;
   int chunk = 0;
 };

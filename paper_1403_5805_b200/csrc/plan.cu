@@ -615,14 +615,74 @@ static int enqueue_sweep(jacobi_plan* p, int j) {
   return 0;
 }
 
+// Device-side loop (plans without NCCL): one graph whose only node is a conditional WHILE node; its
+// body is a batch of K sweeps followed by k_advance_while, which settles the stop decision for the
+// batch's last sweep and sets the loop condition, so a solve is one graph launch and one wait — no
+// host polling and no look-ahead batches of no-op sweeps after the stop.  JACOBI_GRAPH_WHILE=0 falls
+// back to host-polled batches (also used by distributed plans: NCCL is not captured into a
+// conditional body).
+static bool want_while_graph(const jacobi_plan* p) {
+  const char* e = getenv("JACOBI_GRAPH_WHILE");
+  return !p->comm && !(e && e[0] == '0');
+}
+
+static int build_while_graph(jacobi_plan* p) {
+  cudaGraph_t g = nullptr;
+  JCUDA(cudaGraphCreate(&g, 0));
+  int rc = 0;
+  cudaGraphConditionalHandle h;
+  cudaError_t e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault);
+  cudaGraphNode_t node;
+  cudaGraphNodeParams cp = {};
+  if (e == cudaSuccess) {
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    e = cudaGraphAddNode(&node, g, nullptr, 0, &cp);
+  }
+  if (e == cudaSuccess) e = cudaStreamBeginCaptureToGraph(p->stream, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                                          cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) {
+    cudaGraphDestroy(g);
+    cudaGetLastError();
+    return jacobi_set_error(JACOBI_ECUDA, std::string("while graph: ") + cudaGetErrorString(e));
+  }
+  for (int j = 0; j < p->batch && rc == 0; ++j) rc = enqueue_sweep(p, j);
+  if (rc == 0) {
+    cudaError_t ae = jacobi::launch_advance_while(p->st, p->dslot, p->batch, h, p->stream);
+    if (ae != cudaSuccess) rc = jacobi_set_error(JACOBI_ECUDA, std::string("k_advance_while: ") + cudaGetErrorString(ae));
+  }
+  cudaGraph_t body = nullptr;
+  cudaError_t ee = cudaStreamEndCapture(p->stream, &body);
+  if (rc == 0 && ee != cudaSuccess) rc = jacobi_set_error(JACOBI_ECUDA, std::string("while body capture: ") + cudaGetErrorString(ee));
+  if (rc == 0) {
+    cudaError_t ie = cudaGraphInstantiate(&p->graph, g, 0);
+    if (ie != cudaSuccess) rc = jacobi_set_error(JACOBI_ECUDA, std::string("while graph instantiate: ") + cudaGetErrorString(ie));
+  }
+  cudaGraphDestroy(g);
+  cudaGetLastError();
+  return rc;
+}
+
 static int ensure_graph(jacobi_plan* p) {
+  const bool wg = want_while_graph(p);
   if (p->graph && p->graph_batch == p->batch && p->graph_nblocks == p->nblocks && p->graph_norm == p->norm &&
-      p->graph_colblocks == p->colblocks)
+      p->graph_colblocks == p->colblocks && p->graph_while == wg)
     return 0;
   if (p->graph) {
     cudaGraphExecDestroy(p->graph);
     p->graph = nullptr;
   }
+  if (wg && build_while_graph(p) == 0) {
+    p->graph_batch = p->batch;
+    p->graph_nblocks = p->nblocks;
+    p->graph_norm = p->norm;
+    p->graph_colblocks = p->colblocks;
+    p->graph_while = true;
+    return 0;
+  }
+  p->graph_while = false;
   cudaGraph_t g = nullptr;
   JCUDA(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
   int rc = 0;
@@ -644,6 +704,7 @@ static int ensure_graph(jacobi_plan* p) {
   p->graph_nblocks = p->nblocks;
   p->graph_norm = p->norm;
   p->graph_colblocks = p->colblocks;
+  p->graph_while = false;
   return 0;
 }
 
@@ -680,6 +741,19 @@ static int solve_run(jacobi_plan* p, int64_t max_iter, jacobi::State* fin) {
   int rc = ensure_graph(p);
   if (rc) return rc;
   const int64_t K = p->batch;
+  if (p->graph_while) {  // the whole solve: one launch of the device-side loop, one wait
+    JCUDA(cudaGraphLaunch(p->graph, p->stream));
+    JCUDA(cudaMemcpyAsync(&p->st_host[0], p->st, sizeof(jacobi::State), cudaMemcpyDeviceToHost, p->stream));
+    cudaError_t se = cudaStreamSynchronize(p->stream);
+    if (se != cudaSuccess) return jacobi_set_error(JACOBI_ECUDA, std::string("sweep loop: ") + cudaGetErrorString(se));
+    const jacobi::State& s = p->st_host[0];
+    if (s.nonfinite) return nonfinite_error();
+    if (s.fault) return jacobi_set_error(JACOBI_ECUDA, "fused exchange: a peer's sweep signal did not arrive within the wait bound");
+    if (!s.done) return jacobi_set_error(JACOBI_ECUDA, "internal: device loop ended without a stop decision");
+    p->sweeps_launched = ((std::max<int64_t>(s.iters, 1) + K - 1) / K) * K * p->nblocks;  // batches run x K
+    *fin = s;
+    return 0;
+  }
   const int64_t max_batches = (max_iter + K - 1) / K;  // the stop is decided within these
   cudaEvent_t ev[kLookahead];
   for (int i = 0; i < kLookahead; ++i) JCUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));

@@ -1142,14 +1142,21 @@ __global__ void k_colsum_epilogue(const double* __restrict__ rsum, int nb, int64
 
 // After a graph batch of K sweeps: settle the stop decision for the batch's last sweep (same rule
 // as the prologue) and advance the sweep counter.
-__global__ void k_advance(State* st, const unsigned long long* dslot, int K) {
-  if (st->done || st->nonfinite || st->fault) return;
+__device__ __forceinline__ bool advance(State* st, const unsigned long long* dslot, int K) {
+  if (st->done || st->nonfinite || st->fault) return false;
   const int64_t k = st->kbase + K + 1;  // the sweep that would come next
   const double d = __longlong_as_double((long long)dslot[(k - 1) & 3]);
   if (st->hist) st->hist[k - 2] = d;
-  if (d < st->tol) { st->status = JACOBI_CONVERGED; st->iters = k - 1; st->done = 1; return; }
-  if (k > st->max_iter) { st->status = JACOBI_MAX_ITER; st->iters = st->max_iter; st->done = 1; return; }
+  if (d < st->tol) { st->status = JACOBI_CONVERGED; st->iters = k - 1; st->done = 1; return false; }
+  if (k > st->max_iter) { st->status = JACOBI_MAX_ITER; st->iters = st->max_iter; st->done = 1; return false; }
   st->kbase += K;
+  return true;
+}
+__global__ void k_advance(State* st, const unsigned long long* dslot, int K) { advance(st, dslot, K); }
+// ... and, as the last node of the body of a device-side while loop (conditional graph node), decide
+// whether the loop runs another batch: the solve needs one graph launch and no host polling.
+__global__ void k_advance_while(State* st, const unsigned long long* dslot, int K, cudaGraphConditionalHandle h) {
+  cudaGraphSetConditional(h, advance(st, dslot, K) ? 1u : 0u);
 }
 
 template <typename T>
@@ -1520,6 +1527,12 @@ cudaError_t launch_colsum_epilogue(const double* rsum, int nb, int64_t stride, i
 
 cudaError_t launch_advance(State* st, unsigned long long* dslot, int K, cudaStream_t s) {
   k_advance<<<1, 1, 0, s>>>(st, dslot, K);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_advance_while(State* st, unsigned long long* dslot, int K, cudaGraphConditionalHandle h,
+                                 cudaStream_t s) {
+  k_advance_while<<<1, 1, 0, s>>>(st, dslot, K, h);
   return cudaGetLastError();
 }
 

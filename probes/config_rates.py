@@ -32,7 +32,7 @@ for name in names:
     with jb.Plan(dA, n=n, stream=stream.cuda_stream) as p:
         inf = p.info
         for max_iter, tol in RUNS[name]:
-            p.set_batch(20 if max_iter % 20 == 0 else 32)
+            p.set_batch(8 if tol > 0 else (20 if max_iter % 20 == 0 else 32))
             r = p.solve_device(db, dx0, xo, max_iter, tol)  # warm-up (graph capture)
             best = None
             for _ in range(3):
