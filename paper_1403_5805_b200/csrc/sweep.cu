@@ -725,6 +725,11 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync(const SweepArgs a
   const int64_t ntile = (re - rb + R - 1) / R;
   const int lane = threadIdx.x & 31;
   const bool l2 = a.norm == JACOBI_NORM_L2;
+  // The stop test's parameters do not change during a launch: read once, so thread 0's per-sweep chain
+  // is barrier spin -> distance slot -> decision (each extra dependent L2 read cost ~0.3 µs per sweep).
+  const double tol = st->tol;
+  const int64_t max_iter = st->max_iter;
+  double* const hist = st->hist;
   for (int64_t k = k0;; ++k) {
     if (threadIdx.x == 0) {
       int go = 1;
@@ -745,7 +750,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync(const SweepArgs a
       }
       s_go = go;
     }
-    __syncthreads();
+    if (l2) __syncthreads();  // max norm: thread 0 goes straight on to the stop test below
     if (l2 && s_go && k >= 2) {
       // The Euclidean distance of PAPER.md:94 over all rows, computed redundantly by every CTA in the
       // order of k_l2_partials / k_l2_final (256-row shared-memory trees, then a strided ascending
@@ -778,14 +783,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync(const SweepArgs a
       int go = s_go;
       if (go && k >= 2) {  // stop test for sweep k-1, identical in every CTA
         const double d = l2 ? s_d2 : ld_x1<2>(reinterpret_cast<const double*>(a.dslot + ((k - 1) & 3)));
-        if (blockIdx.x == 0 && st->hist) st->hist[k - 2] = d;
-        if (d < st->tol) {
+        if (blockIdx.x == 0 && hist) hist[k - 2] = d;
+        if (d < tol) {
           if (blockIdx.x == 0) { st->status = JACOBI_CONVERGED; st->iters = k - 1; st->done = 1; }
           go = 0;
         }
       }
-      if (go && k > st->max_iter) {
-        if (blockIdx.x == 0) { st->status = JACOBI_MAX_ITER; st->iters = st->max_iter; st->done = 1; }
+      if (go && k > max_iter) {
+        if (blockIdx.x == 0) { st->status = JACOBI_MAX_ITER; st->iters = max_iter; st->done = 1; }
         go = 0;
       }
       if (go && k > k1) go = 0;  // end of this launch's segment; the next launch resumes at k
@@ -849,6 +854,9 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync_push(const SweepA
   const int64_t re = (int64_t)(blockIdx.x - c0 + 1) * a.m / (c1 - c0);
   const int64_t ntile = (re - rb + R - 1) / R;
   const bool leader = blockIdx.x == c0;  // writes this rank's state, history and slot clears
+  const double tol = st->tol;            // fixed during the launch (see k_solve_gridsync)
+  const int64_t max_iter = st->max_iter;
+  double* const hist = st->hist;
   for (int64_t k = k0;; ++k) {
     if (threadIdx.x == 0) {
       int go = 1;
@@ -871,14 +879,14 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync_push(const SweepA
       }
       if (go && k >= 2) {  // stop test for sweep k-1, identical on every rank
         const double d = ld_x1<2>(reinterpret_cast<const double*>(a.dslot + ((k - 1) & 3)));
-        if (leader && st->hist) st->hist[k - 2] = d;
-        if (d < st->tol) {
+        if (leader && hist) hist[k - 2] = d;
+        if (d < tol) {
           if (leader) { st->status = JACOBI_CONVERGED; st->iters = k - 1; st->done = 1; }
           go = 0;
         }
       }
-      if (go && k > st->max_iter) {
-        if (leader) { st->status = JACOBI_MAX_ITER; st->iters = st->max_iter; st->done = 1; }
+      if (go && k > max_iter) {
+        if (leader) { st->status = JACOBI_MAX_ITER; st->iters = max_iter; st->done = 1; }
         go = 0;
       }
       if (go && k > k1) go = 0;  // end of this launch's segment; the next launch resumes at k
