@@ -744,3 +744,30 @@ def test_fused_exchange_dynamic_tiles(jb):
         r = p.solve(b, None, 200, 1e-11, history=True)
         match_oracle(r, orc)
         assert np.array_equal(r.x, ref.x)
+
+
+def test_device_while_loop_matches_host_polled_batches(jb, monkeypatch):
+    """The device-side while loop over graph batches (conditional graph node) and the
+    host-polled batches give the same bits, statuses and iteration counts for fixed runs, tol stops
+    inside and at the end of a batch, max_iter not a multiple of the batch, and both norms."""
+    n = 6000
+    A, b, _ = dominant(n, 909, scale=1.05)
+    x0 = np.random.default_rng(9).uniform(-1, 1, n)
+    runs = [(37, 0.0, "max"), (5000, 1e-10, "max"), (5000, 1e-10, "l2"), (8, 0.0, "max"), (1, 0.0, "max")]
+    out = {}
+    for w in ("1", "0"):
+        monkeypatch.setenv("JACOBI_GRAPH_WHILE", w)
+        monkeypatch.setenv("JACOBI_PERSIST", "0")
+        with jb.Plan(A) as p:
+            for K in (4, 8):
+                p.set_batch(K)
+                for mi, tol, norm in runs:
+                    p.set_norm(norm)
+                    out[(w, K, mi, tol, norm)] = p.solve(b, x0, mi, tol, history=True)
+    for K in (4, 8):
+        for mi, tol, norm in runs:
+            r, q = out[("1", K, mi, tol, norm)], out[("0", K, mi, tol, norm)]
+            assert (r.status, r.iters) == (q.status, q.iters), (K, mi, tol, norm)
+            assert np.array_equal(r.x, q.x) and np.array_equal(r.hist, q.hist), (K, mi, tol, norm)
+    orc = oracle.jacobi(A, b, x0, 5000, 1e-10, nthreads=16, history=True)
+    match_oracle(out[("1", 8, 5000, 1e-10, "max")], orc)
