@@ -114,11 +114,12 @@ void jacobi_plan_destroy(jacobi_plan* plan);
 int jacobi_plan_set_row_blocks(jacobi_plan* plan, int nblocks);
 /* Select the stop-test norm (JACOBI_NORM_MAX or JACOBI_NORM_L2) for subsequent solves. */
 int jacobi_plan_set_norm(jacobi_plan* plan, int norm);
-/* Sweeps per captured CUDA graph batch (multiple of 4, 4..1024; default 32).  Plans without NCCL run
- * the batches as the body of a device-side while loop (a conditional graph node: one graph launch
- * per solve, the loop condition set by the device's stop decision after each batch; JACOBI_GRAPH_WHILE=0
- * falls back to host polling); distributed plans poll the stop state on the host once per batch.
- * Sweeps of the batch after the stop decision are no-op launches, so tol runs favour short batches. */
+/* Sweeps per captured CUDA graph batch (multiple of 4, 4..1024; default 32).  A tol > 0 solve on a
+ * plan without NCCL runs the batches as the body of a device-side while loop (a conditional graph
+ * node: one graph launch per solve, the loop condition set by the device's stop decision after each
+ * batch; JACOBI_GRAPH_WHILE=0 disables it); fixed-iteration solves and distributed plans launch
+ * batches from the host and poll the stop state once per batch.  Sweeps of the batch after the stop
+ * decision are no-op launches, so tol runs favour short batches. */
 int jacobi_plan_set_batch(jacobi_plan* plan, int sweeps_per_batch);
 
 typedef struct {

@@ -209,9 +209,10 @@ struct jacobi_plan {
   int* flag_dev = nullptr;       // scratch: non-finite flag / zero-diag min index
   unsigned long long* zmin_dev = nullptr;
   ncclComm_t comm = nullptr;     // distributed plans only
-  cudaGraphExec_t graph = nullptr;
-  int graph_batch = 0, graph_nblocks = 0, graph_norm = -1, graph_colblocks = 0;
-  bool graph_while = false;      // the graph is one device-side while loop over batches (no host polling)
+  // [0]: a batch of sweeps launched and polled from the host; [1]: a device-side while loop over
+  // batches (conditional graph node) used for tol runs; each with the configuration it was built for
+  cudaGraphExec_t graphs[2] = {nullptr, nullptr};
+  int gkey[2][4] = {{0, 0, -1, 0}, {0, 0, -1, 0}};  // batch, nblocks, norm, colblocks
   int64_t sweeps_launched = 0;
   int chunk = 0;
 };

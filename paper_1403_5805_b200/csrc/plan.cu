@@ -70,7 +70,8 @@ static int plan_free(jacobi_plan* p) {
   auto chk = [&](cudaError_t e, const char* what) {
     if (e != cudaSuccess && first.empty()) first = std::string(what) + ": " + cudaGetErrorString(e);
   };
-  if (p->graph) chk(cudaGraphExecDestroy(p->graph), "cudaGraphExecDestroy");
+  for (cudaGraphExec_t g : p->graphs)
+    if (g) chk(cudaGraphExecDestroy(g), "cudaGraphExecDestroy");
   if (p->comm) ncclCommDestroy(p->comm);
   void* dev[] = {p->dA_owned, p->diag, p->b, p->x[0], p->x[1], p->part, p->cnt, p->dslot, p->st,
                  p->hist_dev, p->flag_dev, p->zmin_dev, p->sq, p->blk, p->blk_all, p->rsum, p->rs_own,
@@ -657,7 +658,7 @@ static int build_while_graph(jacobi_plan* p) {
   cudaError_t ee = cudaStreamEndCapture(p->stream, &body);
   if (rc == 0 && ee != cudaSuccess) rc = jacobi_set_error(JACOBI_ECUDA, std::string("while body capture: ") + cudaGetErrorString(ee));
   if (rc == 0) {
-    cudaError_t ie = cudaGraphInstantiate(&p->graph, g, 0);
+    cudaError_t ie = cudaGraphInstantiate(&p->graphs[1], g, 0);
     if (ie != cudaSuccess) rc = jacobi_set_error(JACOBI_ECUDA, std::string("while graph instantiate: ") + cudaGetErrorString(ie));
   }
   cudaGraphDestroy(g);
@@ -665,24 +666,22 @@ static int build_while_graph(jacobi_plan* p) {
   return rc;
 }
 
-static int ensure_graph(jacobi_plan* p) {
-  const bool wg = want_while_graph(p);
-  if (p->graph && p->graph_batch == p->batch && p->graph_nblocks == p->nblocks && p->graph_norm == p->norm &&
-      p->graph_colblocks == p->colblocks && p->graph_while == wg)
-    return 0;
-  if (p->graph) {
-    cudaGraphExecDestroy(p->graph);
-    p->graph = nullptr;
+// The graph for a solve: the device-side while loop (wg) or a host-polled batch, built on first use
+// for the plan's current configuration and cached.  Returns the slot used (0 or 1).
+static int ensure_graph(jacobi_plan* p, bool wg, int* slot) {
+  const int key[4] = {p->batch, p->nblocks, p->norm, p->colblocks};
+  const int w = wg ? 1 : 0;
+  *slot = w;
+  if (p->graphs[w] && std::memcmp(p->gkey[w], key, sizeof(key)) == 0) return 0;
+  if (p->graphs[w]) {
+    cudaGraphExecDestroy(p->graphs[w]);
+    p->graphs[w] = nullptr;
   }
-  if (wg && build_while_graph(p) == 0) {
-    p->graph_batch = p->batch;
-    p->graph_nblocks = p->nblocks;
-    p->graph_norm = p->norm;
-    p->graph_colblocks = p->colblocks;
-    p->graph_while = true;
+  if (wg) {
+    JRC(build_while_graph(p));
+    std::memcpy(p->gkey[1], key, sizeof(key));
     return 0;
   }
-  p->graph_while = false;
   cudaGraph_t g = nullptr;
   JCUDA(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
   int rc = 0;
@@ -697,14 +696,10 @@ static int ensure_graph(jacobi_plan* p) {
     return rc;
   }
   if (ee != cudaSuccess) return jacobi_set_error(JACOBI_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ee));
-  cudaError_t ie = cudaGraphInstantiate(&p->graph, g, 0);
+  cudaError_t ie = cudaGraphInstantiate(&p->graphs[0], g, 0);
   cudaGraphDestroy(g);
   if (ie != cudaSuccess) return jacobi_set_error(JACOBI_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ie));
-  p->graph_batch = p->batch;
-  p->graph_nblocks = p->nblocks;
-  p->graph_norm = p->norm;
-  p->graph_colblocks = p->colblocks;
-  p->graph_while = false;
+  std::memcpy(p->gkey[0], key, sizeof(key));
   return 0;
 }
 
@@ -736,13 +731,19 @@ static int solve_prepare(jacobi_plan* p, const double* b, const double* x0, bool
 static int nonfinite_error() { return jacobi_set_error(JACOBI_ENONFINITE, "b or x0 contains NaN or Inf"); }
 
 // Runs graph batches until the device decides to stop.  Fills *fin with the final state.
-static int solve_run(jacobi_plan* p, int64_t max_iter, jacobi::State* fin) {
+static int solve_run(jacobi_plan* p, int64_t max_iter, double tol, jacobi::State* fin) {
   Range nvtx_range("jacobi: sweeps (CUDA graph batches)");
-  int rc = ensure_graph(p);
+  // tol runs stop where the device decides: loop on the device (no polling, no look-ahead batches of
+  // no-op sweeps).  Fixed runs know their batch count: host-launched batches cost nothing extra there,
+  // and keep every sweep kernel visible to launch-level profilers.
+  int w = 0;
+  int rc = ensure_graph(p, tol > 0 && want_while_graph(p), &w);
+  if (rc && w == 1) rc = ensure_graph(p, false, &w);  // no conditional nodes here: host-polled batches
   if (rc) return rc;
   const int64_t K = p->batch;
-  if (p->graph_while) {  // the whole solve: one launch of the device-side loop, one wait
-    JCUDA(cudaGraphLaunch(p->graph, p->stream));
+  cudaGraphExec_t graph = p->graphs[w];
+  if (w == 1) {  // the whole solve: one launch of the device-side loop, one wait
+    JCUDA(cudaGraphLaunch(graph, p->stream));
     JCUDA(cudaMemcpyAsync(&p->st_host[0], p->st, sizeof(jacobi::State), cudaMemcpyDeviceToHost, p->stream));
     cudaError_t se = cudaStreamSynchronize(p->stream);
     if (se != cudaSuccess) return jacobi_set_error(JACOBI_ECUDA, std::string("sweep loop: ") + cudaGetErrorString(se));
@@ -762,7 +763,7 @@ static int solve_run(jacobi_plan* p, int64_t max_iter, jacobi::State* fin) {
   p->sweeps_launched = 0;
   auto issue = [&]() -> int {
     const int slot = (int)(issued % kLookahead);
-    JCUDA(cudaGraphLaunch(p->graph, p->stream));
+    JCUDA(cudaGraphLaunch(graph, p->stream));
     JCUDA(cudaMemcpyAsync(&p->st_host[slot], p->st, sizeof(jacobi::State), cudaMemcpyDeviceToHost, p->stream));
     JCUDA(cudaEventRecord(ev[slot], p->stream));
     ++issued;
@@ -994,7 +995,7 @@ static int solve_impl(jacobi_plan* p, const double* b, const double* x0, bool de
     if (rc) return rc;
     finalized = dev;
   } else {
-    rc = solve_run(p, max_iter, &fin);
+    rc = solve_run(p, max_iter, tol, &fin);
     if (rc) return rc;
   }
   if (p->colwise && fin.iters > 0) {  // column-wise ranks hold only their slice: assemble x^(iters)
