@@ -462,11 +462,20 @@ __device__ __forceinline__ bool keep_unit(unsigned i, unsigned thr) { return i *
 // x stores): fold the CTA's max|dx| bits into every rank's distance slot, then — behind one system-scope
 // fence, cumulative over the stores the barrier ordered before it — add one arrival to every rank's
 // counter for the parity of k.
+// The reductions are system-scoped (red.global.sys): the counters and slots live in other GPUs' memory
+// and are read there with ld.acquire.sys, so both sides of the synchronisation are morally strong at
+// the same scope (global-space PTX, so no generic-address fallback is generated).
+__device__ __forceinline__ void red_max_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.global.sys.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.global.sys.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ void push_signal(const PeerArgs* pe, int64_t k, unsigned long long m) {
   const int P = pe->P;
-  for (int p = 0; p < P; ++p) atomicMax(pe->dslot[p] + (k & 3), m);
+  for (int p = 0; p < P; ++p) red_max_sys(pe->dslot[p] + (k & 3), m);
   __threadfence_system();
-  for (int p = 0; p < P; ++p) atomicAdd(pe->flags[p] + (k & 1), 1ull);
+  for (int p = 0; p < P; ++p) red_add_sys(pe->flags[p] + (k & 1), 1ull);
 }
 
 // CTA-wide max of the warps' max|dx| bits (every thread must call it; returns the max in thread 0).
