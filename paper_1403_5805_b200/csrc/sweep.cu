@@ -474,7 +474,7 @@ __device__ __forceinline__ void red_add_sys(unsigned long long* p, unsigned long
 __device__ __forceinline__ void push_signal(const PeerArgs* pe, int64_t k, unsigned long long m) {
   const int P = pe->P;
   for (int p = 0; p < P; ++p) red_max_sys(pe->dslot[p] + (k & 3), m);
-  __threadfence_system();
+  asm volatile("fence.acq_rel.sys;" ::: "memory");  // release: the pushes and maxima before the arrivals
   for (int p = 0; p < P; ++p) red_add_sys(pe->flags[p] + (k & 1), 1ull);
 }
 
@@ -816,7 +816,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync(const SweepArgs a
     if (lane == 0 && dmax) atomicMax(&a.dslot[k & 3], dmax);
     __syncthreads();  // every x_i^(k) store and max|dx| atomic of this CTA has been issued
     if (threadIdx.x == 0) {
-      __threadfence();
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");  // release, cumulative over the CTA's stores
       atomicAdd(gbar, 1ull);
     }
   }
