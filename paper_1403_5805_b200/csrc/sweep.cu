@@ -739,6 +739,10 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync(const SweepArgs a
   const double tol = st->tol;
   const int64_t max_iter = st->max_iter;
   double* const hist = st->hist;
+  // A fixed-count run (tol <= 0: d_k < tol never holds) needs d_{k-1} only for the
+  // history, i.e. in CTA 0 when one is recorded: the other CTAs skip its L2 round trip (max norm) or
+  // its all-rows reduction (Euclidean) on the way from the barrier to the next sweep.
+  const bool need_d = tol > 0.0 || (blockIdx.x == 0 && hist);
   for (int64_t k = k0;; ++k) {
     if (threadIdx.x == 0) {
       int go = 1;
@@ -760,7 +764,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync(const SweepArgs a
       s_go = go;
     }
     if (l2) __syncthreads();  // max norm: thread 0 goes straight on to the stop test below
-    if (l2 && s_go && k >= 2) {
+    if (l2 && need_d && s_go && k >= 2) {
       // The Euclidean distance of PAPER.md:94 over all rows, computed redundantly by every CTA in the
       // order of k_l2_partials / k_l2_final (256-row shared-memory trees, then a strided ascending
       // warp sum and a butterfly), so the bits equal the graph path's.  dx^2 of sweep k-1 lives in
@@ -790,7 +794,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync(const SweepArgs a
     }
     if (threadIdx.x == 0) {
       int go = s_go;
-      if (go && k >= 2) {  // stop test for sweep k-1, identical in every CTA
+      if (go && need_d && k >= 2) {  // stop test for sweep k-1, identical in every CTA
         const double d = l2 ? s_d2 : ld_x1<2>(reinterpret_cast<const double*>(a.dslot + ((k - 1) & 3)));
         if (blockIdx.x == 0 && hist) hist[k - 2] = d;
         if (d < tol) {
@@ -808,6 +812,13 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync(const SweepArgs a
     }
     __syncthreads();
     if (!s_go) break;
+#ifdef JACOBI_SM_TIMING
+    // probe build: sweeps k0+20 .. k0+23 of the launch, per CTA: SM id, start of the sweep's work (after
+    // the barrier and stop test), end of it (before the barrier arrival)
+    const int64_t smt_i = k - k0 - 20;
+    unsigned long long smt_go = 0;
+    if (threadIdx.x == 0 && smt_i >= 0 && smt_i < 4) smt_go = global_ns();
+#endif
     SweepArgs ak = a;
     ak.sq = a.sq + (k & 1) * a.m;  // double-buffered dx^2 (Euclidean rule)
     const unsigned long long dmax =
@@ -816,6 +827,16 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync(const SweepArgs a
     if (lane == 0 && dmax) atomicMax(&a.dslot[k & 3], dmax);
     __syncthreads();  // every x_i^(k) store and max|dx| atomic of this CTA has been issued
     if (threadIdx.x == 0) {
+#ifdef JACOBI_SM_TIMING
+      if (smt_i >= 0 && smt_i < 4 && blockIdx.x < 1024) {
+        unsigned sm_;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_));
+        const size_t o = 3 * ((size_t)smt_i * 1024 + blockIdx.x);
+        g_smt[o] = sm_;
+        g_smt[o + 1] = smt_go;
+        g_smt[o + 2] = global_ns();
+      }
+#endif
       asm volatile("fence.acq_rel.gpu;" ::: "memory");  // release, cumulative over the CTA's stores
       atomicAdd(gbar, 1ull);
     }
@@ -866,6 +887,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync_push(const SweepA
   const double tol = st->tol;            // fixed during the launch (see k_solve_gridsync)
   const int64_t max_iter = st->max_iter;
   double* const hist = st->hist;
+  const bool need_d = tol > 0.0 || (leader && hist);  // as in k_solve_gridsync
   for (int64_t k = k0;; ++k) {
     if (threadIdx.x == 0) {
       int go = 1;
@@ -886,7 +908,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync_push(const SweepA
           }
         }
       }
-      if (go && k >= 2) {  // stop test for sweep k-1, identical on every rank
+      if (go && need_d && k >= 2) {  // stop test for sweep k-1, identical on every rank
         const double d = ld_x1<2>(reinterpret_cast<const double*>(a.dslot + ((k - 1) & 3)));
         if (leader && hist) hist[k - 2] = d;
         if (d < tol) {
