@@ -55,5 +55,8 @@ with jb.Plan(dA, n=n, stream=torch.cuda.current_stream().cuda_stream) as p:
                 line["release_after_last_end_us"] = float(go[s + 1].min() - end[s].max())
                 line["cycle_us"] = float(np.median(go[s + 1] - go[s]))
             print(json.dumps(line), flush=True)
-        print(json.dumps({"n": n, "rep": rep, "slowest_ctas": np.argsort(-work.mean(0))[:8].tolist(),
+        rows = [(b + 1) * n // G - b * n // G for b in range(G)]
+        print(json.dumps({"n": n, "rep": rep, "cta_rows": rows, "cta_smid": a[0, :, 0].tolist(),
+                          "cta_work_us": [round(float(v), 3) for v in work.mean(0)],
+                          "slowest_ctas": np.argsort(-work.mean(0))[:8].tolist(),
                           "slowest_sms": [int(a[0, i, 0]) for i in np.argsort(-work.mean(0))[:8]]}), flush=True)
