@@ -739,7 +739,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_solve_gridsync(const SweepArgs a
   const double tol = st->tol;
   const int64_t max_iter = st->max_iter;
   double* const hist = st->hist;
-  // A fixed-count run (tol <= 0: d_k < tol never holds) needs d_{k-1} only for the
+  // A fixed-count run (tol = 0: d_k < tol never holds) needs d_{k-1} only for the
   // history, i.e. in CTA 0 when one is recorded: the other CTAs skip its L2 round trip (max norm) or
   // its all-rows reduction (Euclidean) on the way from the barrier to the next sweep.
   const bool need_d = tol > 0.0 || (blockIdx.x == 0 && hist);

@@ -80,6 +80,24 @@ def test_gridsync_bitwise_vs_graph_and_oracle(jb, monkeypatch, n, f32):
     np.testing.assert_allclose(r.hist, h_o, rtol=1e-9, atol=1e-14)
 
 
+@pytest.mark.parametrize("n", [1000, 4096, 6000])
+def test_gridsync_fixed_count_without_history(jb, monkeypatch, n):
+    """Fixed-count runs without a history skip the distance read between sweeps in every CTA (tol = 0
+    never satisfies d_k < tol): the iterates must not change — bitwise equal to the graph
+    path, and to the same run with a history (which CTA 0 records)."""
+    A, b, _ = dominant(n, 17 + n, scale=1.05)
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("JACOBI_PERSIST", mode)
+        with jb.Plan(A) as p:
+            assert (p.info.persistent_ctas > 0) == (mode == "1")
+            out[mode] = (p.solve(b, None, 60, 0.0), p.solve(b, None, 60, 0.0, history=True))
+    for r in out["1"] + out["0"]:
+        assert (r.status, r.iters) == (jb.MAX_ITER, 60)
+        assert np.array_equal(r.x, out["0"][0].x)
+    assert np.array_equal(out["1"][1].hist, out["0"][1].hist)
+
+
 def test_gridsync_c2_config(jb, monkeypatch):
     """BASELINE.json configs[1]: n = 4096, fixed 500 iterations (the default path for c2)."""
     A, b, xs = g.host_system(g.CONFIGS["c2"])
