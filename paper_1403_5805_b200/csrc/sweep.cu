@@ -1118,6 +1118,121 @@ __global__ void __launch_bounds__(NW * 32, 1) k_sweep_panel(const SweepArgs a, c
   SMT_END();
 }
 
+// k_sweep_group: the row-panel kernel with G warps per tile.  The CTA's NW warps form NW/G groups;
+// group p owns an equal share of the CTA's rows and walks them in tiles of R rows; warp q of the group
+// takes the tile's chunks q, q + G, ... (each chunk's lane chains and butterfly exactly as in the panel
+// kernel), writes the chunk sums to the group's shared-memory partials (double-buffered by tile
+// parity), and after a group barrier warp 0 folds them in ascending chunk order — the canonical order
+// again — and applies the fused epilogue.  Why: a group streams G chunks of each of its rows at once,
+// so the chip keeps 1/G as many DRAM rows open as the panel kernel (probes/tma_warp_probe.cu, c5's
+// pattern: 7.10 TB/s for one warp per 4-row tile, 7.21-7.28 for 2-16), while x^(k-1) still comes from
+// the CTA's shared-memory ring (each chunk read by one warp of every group).
+template <typename T, int R, int NW, int G, int XSN>
+__global__ void __launch_bounds__(NW * 32, 1) k_sweep_group(const SweepArgs a, const int j) {
+  SMT_BEGIN();
+  static_assert(XSN > 0 && XSN <= kMaxXSN && NW % G == 0 && NW / G <= 15, "group kernel shape");
+  constexpr int NG = NW / G;
+  extern __shared__ __align__(128) double s_xring[];  // [XSN][chunk] x ring, then [NG][2][R][nchunks] partials
+  __shared__ __align__(8) uint64_t s_xfull[XSN];
+  __shared__ unsigned s_xcnt[XSN];
+  __shared__ int s_go;
+  __shared__ long long s_k;
+  if (threadIdx.x == 0) {
+    s_go = sweep_prologue(a, j, blockIdx.x == 0, &s_k);
+    for (int q = 0; q < XSN; ++q) {
+      mbar_init(&s_xfull[q], 1);
+      s_xcnt[q] = 0u;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (!s_go) return;
+
+  const int64_t k = s_k;
+  const double* __restrict__ xo = (k & 1) ? a.x0buf : a.x1buf;  // x^(k-1)
+  double* __restrict__ xn = (k & 1) ? a.x1buf : a.x0buf;        // x^(k)
+  const T* __restrict__ A = static_cast<const T*>(a.A);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, grp = w / G, q = w % G;
+  const int64_t rb = blockIdx.x * a.m / gridDim.x, re = (blockIdx.x + 1) * a.m / gridDim.x;
+  auto tiles_of = [&](int gg) {
+    const int64_t b0 = rb + (re - rb) * gg / NG, b1 = rb + (re - rb) * (gg + 1) / NG;
+    return (int)((b1 - b0 + R - 1) / R);
+  };
+  const int64_t gb = rb + (re - rb) * grp / NG, ge = rb + (re - rb) * (grp + 1) / NG;
+  int rounds = 0;
+  for (int gg = 0; gg < NG; ++gg) rounds = max(rounds, tiles_of(gg));
+  const int nch = a.nchunks;
+  const XRing ring{s_xring, s_xfull, s_xcnt, (int64_t)rounds * nch, XSN};
+  if (threadIdx.x == 0)
+    for (int64_t i = 0; i < XSN; ++i) xring_issue(ring, a, xo, i);
+  double* const part0 = s_xring + (size_t)XSN * a.chunk + (size_t)grp * 2 * R * nch;
+  unsigned long long dmax = 0ull;
+  int t = 0;
+  for (int64_t r0 = gb; r0 < ge; r0 += R, ++t) {
+    const int nv = (int)min((int64_t)R, ge - r0);
+    unsigned arrivals = 0;  // groups with a t-th tile: one warp of each reads every item of round t
+    for (int gg = 0; gg < NG; ++gg) arrivals += tiles_of(gg) > t ? 1u : 0u;
+    double* const part = part0 + (size_t)(t & 1) * R * nch;
+    const int64_t g0 = a.row0 + r0;
+    with_nv<R>(nv, [&](auto NVc) {
+      constexpr int NV = decltype(NVc)::value;
+      const T* rowp[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) rowp[r] = A + (r0 + (r < NV ? r : NV - 1)) * a.lda - a.col0;
+      for (int c = q; c < nch; c += G) {
+        double acc[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = 0.0;
+        const int64_t c0 = a.col0 + (int64_t)c * a.chunk;
+        const int64_t c1 = min(c0 + (int64_t)a.chunk, a.cend);
+        check_tile<T, R>(a, rowp, c0, c1);
+        const int64_t i = (int64_t)t * nch + c;
+        const int slot = (int)(i % XSN);
+        mbar_wait(&ring.full[slot], (unsigned)((i / XSN) & 1));
+        accumulate_chunk<T, R, 1, 0, false, true>(rowp, NV, xo, c0, c1, a.chunk, a.cend, g0, lane, acc, 0,
+                                                  ring.xs + (size_t)slot * a.chunk);
+        __syncwarp();
+        if (lane == 0 && atomicAdd(&ring.cnt[slot], 1u) + 1u == arrivals) {  // last reader of item i
+          ring.cnt[slot] = 0u;
+          xring_issue(ring, a, xo, i + XSN);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) acc[r] += __shfl_xor_sync(kFull, acc[r], off);
+          if (lane == r) part[r * nch + c] = acc[r];
+        }
+      }
+    });
+    // the group's chunk sums of this tile are in `part`; the barrier of tile t + 1 orders warp 0's
+    // fold of tile t before any write of tile t + 2 into the same buffer
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(G * 32) : "memory");
+    if (q == 0 && lane < nv) {
+      double mine = part[lane * nch];
+      for (int c = 1; c < nch; ++c) mine += part[lane * nch + c];  // ascending chunk order
+      const int64_t row = r0 + lane;
+      JB_CHECK(row >= 0 && row < a.m && a.row0 + row < a.x_len, 5);
+      if (a.rsum) {  // column-wise partial product of this slab (epilogue after the reduction)
+        a.rsum[row] = mine;
+      } else {
+        const double xnew = __ddiv_rn(__dsub_rn(a.b[row], mine), a.diag[row]);
+        const int64_t gi = a.row0 + row;
+        const double dx = __dsub_rn(xnew, xo[gi]);
+        xn[gi] = xnew;
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(dx) & 0x7fffffffffffffffull;
+        dmax = bits > dmax ? bits : dmax;
+        if (a.norm == JACOBI_NORM_L2) a.sq[row] = __dmul_rn(dx, dx);
+      }
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const unsigned long long o = __shfl_xor_sync(kFull, dmax, off);
+    dmax = o > dmax ? o : dmax;
+  }
+  if (lane == 0 && dmax) atomicMax(&a.dslot[k & 3], dmax);
+  SMT_END();
+}
 
 // Euclidean distance (NEXT-2 row), deterministic: k_l2_partials sums each block of
 // kL2Block rows' squared changes with a fixed smem tree; k_l2_final (one warp) sums the block partials
@@ -1342,6 +1457,9 @@ const Variant kVariants[] = {
     {"k_sweep_cta R4 U2 L2-policy dynamic", 4, 512, 1, 4, 2, 2, k_sweep_cta<double, 4, 16, 2, 0, false, true, 1, true>, k_sweep_cta<float, 4, 16, 2, 0, false, true, 1, true>},
     // fused-exchange instance of 10 (large row blocks per rank, e.g. c4 at P <= 2)
     {"k_sweep_cta R4 U2 dynamic fused-exchange", 4, 512, 2, 4, 2, 2, k_sweep_cta<double, 4, 16, 2, 3, true, true, 1, true>, k_sweep_cta<float, 4, 16, 2, 3, true, true, 1, true>},
+    // row-panel kernel with 4 warps per 8-row tile (cta = 6: G = 4 warps per group), x ring as 6: fp32
+    // default with few rows per SM (c5 shards at P >= 2)
+    {"k_sweep_group R8 G4 x-smem", 8, 512, 6, 8, 1, 1, k_sweep_group<double, 8, 16, 4, 8>, k_sweep_group<float, 8, 16, 4, 8>},
 };
 // Round 1 also compiled item kernels R2 U4 / R4 U1 / 256 and 1024 threads, CTA kernels R8 256t / R4 U2 /
 // R2 U4 / R4 fused-exchange / R4 L2-keep / rows/4 / R4 U1 dynamic, and panel kernels x-evict_last / R8 /
@@ -1378,6 +1496,10 @@ int push_variant(int dtype, int64_t rows, int num_sms) {
 size_t variant_smem(int v, int nchunks, int dtype, int chunk) {
   const Variant& V = kVariants[v];
   if (V.cta == 4) return (size_t)8 * chunk * 8;  // x ring: 8 slots of one chunk of fp64 x
+  if (V.cta >= 5) {  // x ring + per group two tiles' chunk sums (cta 5 / 6 / 7: 2 / 4 / 8 warps per group)
+    const int R = dtype == JACOBI_F32 ? V.R32 : V.R, groups = V.threads / (32 << (V.cta - 4));
+    return (size_t)8 * chunk * 8 + (size_t)groups * 2 * R * nchunks * 8;
+  }
   const int R = dtype == JACOBI_F32 ? V.R32 : V.R;
   return (V.cta == 1 || V.cta == 2) ? (size_t)kSlots * nchunks * R * 8 : 0;  // 2: fused exchange
 }
@@ -1385,7 +1507,7 @@ bool variant_fits(int v, int nchunks, int dtype, int chunk) {
   const Variant& V = kVariants[v];
   const int step_cols = 32 * (dtype == JACOBI_F32 ? 8 : 4) * (dtype == JACOBI_F32 ? V.u32 : V.u64);
   if (chunk % step_cols != 0) return false;
-  if (V.cta == 4) return variant_smem(v, nchunks, dtype, chunk) <= 200 * 1024;
+  if (V.cta >= 4) return variant_smem(v, nchunks, dtype, chunk) <= 200 * 1024;
   return !V.cta || V.cta == 3 || (nchunks >= V.threads / 32 && variant_smem(v, nchunks, dtype, chunk) <= 48 * 1024);
 }
 bool variant_is_push(int v) { return kVariants[v].cta == 2; }
@@ -1405,6 +1527,13 @@ int variant_rows_dt(int v, int dtype) { return dtype == JACOBI_F32 ? kVariants[v
 // - fewer chunks: the item kernel R=8,U=1 (fp64) or R=4,U=1 (fp32).
 int default_variant(int dtype, int nchunks, int chunk, bool l2_keep, int64_t rows, int num_sms) {
   (void)l2_keep;  // every default instance with an L2 policy handles any kept share (0 included)
+  // fp32 A with fewer than 512 rows per SM (c5 shards at P >= 2): the group kernel, whose 4 warps per
+  // 8-row tile stream 4 chunks of each row at once (sustained 100-sweep shard times, panel / group:
+  // P = 2 4909-4927 / 4866-4873 µs, P = 4 2582-2586 / 2459-2464, P = 8 1300-1302 / 1242-1244; at
+  // P = 1, 885 rows per SM, 7055-7066 / 7041 GB/s, so the panel kernel stays).
+  if (dtype == JACOBI_F32 && nchunks >= 16 && num_sms > 0 && rows < (int64_t)512 * num_sms &&
+      variant_fits(12, nchunks, dtype, chunk))
+    return 12;
   if (dtype == JACOBI_F32 && nchunks >= 16) return variant_fits(6, nchunks, dtype, chunk) ? 6 : 5;
   // Dynamic tiles of 4 rows, two column steps in flight (10) once a CTA has >= 32 such tiles: the
   // expected idle of dynamic assignment, about half a tile, then undercuts the static partition's

@@ -28,9 +28,9 @@ QUICK = "--quick" in sys.argv  # one graph-path case (checker self-test)
 # falls back to the default, and the line printed says which ran.
 CASES = ((1, False, [None], ["0"]), (37, False, [None], ["0"]), (300, True, [None], ["0"]),
          (700, False, [None], ["1", "0"]), (3001, False, [None, "0", "3", "5", "6"], ["1", "0"]),
-         (2049, True, [None, "5", "6"], ["1", "0"]),
-         (8190, False, [None, "0", "1", "2", "3", "5", "6", "7", "8", "9", "10"], ["0"]),
-         (8190, True, [None, "0", "5", "6"], ["0"]))
+         (2049, True, [None, "5", "6", "12"], ["1", "0"]),
+         (8190, False, [None, "0", "1", "2", "3", "5", "6", "7", "8", "9", "10", "12"], ["0"]),
+         (8190, True, [None, "0", "5", "6", "12"], ["0"]), (20000, True, ["12"], ["0"]))
 for n, f32, variants, modes in (((3001, False, [None], ["0"]),) if QUICK else CASES):
     A, b = dominant(n, n, f32)
     for v, mode in [(v, m) for v in variants for m in modes]:

@@ -377,7 +377,7 @@ def test_c4_full_parity_all_rows(jb):
     torch.cuda.empty_cache()
 
 
-def test_c5_full_parity_tol_run(jb):
+def test_c5_full_parity_tol_run(jb, monkeypatch):
     """BASELINE.json configs[4] at full size (n = 131072, A stored fp32, 68.7 GB; diagonal = 1.2 x
     row abs-sum; tol 1e-6 or 2000): the whole-system oracle on the same fp32 values (widened exactly)
     must stop at the SAME iteration with the same status, x within the fp32-storage
@@ -408,6 +408,19 @@ def test_c5_full_parity_tol_run(jb):
         r = p.solve_device(db, dx0, dxo, 100, 0.0)  # the fixed-100 companion the rates are quoted on
         assert (r.status, r.iters) == (jb.MAX_ITER, 100)
         assert np.max(np.abs(dxo.cpu().numpy() - g.host_xstar(cfg))) <= 1e-12
+    # the P = 2/4/8 shards' kernel (the group kernel a rank with 65536 / 32768 / 16384 rows picks):
+    # forced on the same borrowed A, as one launch and as 2/4/8 row blocks of exactly the shard shapes,
+    # bitwise equal to the P = 1 default run above (P12) — same stop iteration, x and d_k history
+    monkeypatch.setenv("JACOBI_SWEEP_VARIANT", "12")
+    with jb.Plan(dA) as p:
+        assert jb.variant_name(p.info.variant) == "k_sweep_group R8 G4 x-smem"
+        for nb in (1, 2, 4, 8):
+            p.set_row_blocks(nb)
+            dxq = torch.empty(n, dtype=torch.float64, device="cuda")
+            hq = torch.empty(2000, dtype=torch.float64, device="cuda")
+            q = p.solve_device(db, dx0, dxq, 2000, 1e-6, hist=hq)
+            assert (q.status, q.iters) == (jb.CONVERGED, it_o), nb
+            assert np.array_equal(dxq.cpu().numpy(), x) and np.array_equal(hq.cpu().numpy()[:it_o], h), nb
     del dA
     torch.cuda.empty_cache()
 
@@ -429,7 +442,7 @@ def test_all_sweep_variants_bitwise_identical(jb, n, f32, monkeypatch):
             assert p.info.num_variants == nvar
             r = p.solve(b, None, 12, 0.0, history=True)
             c = p.solve(b, None, 500, 1e-11)
-            if n == 8190 and v in (2, 3, 7, 8, 9, 10):
+            if n == 8190 and v in (2, 3, 7, 8, 9, 10, 12):
                 for nb in (2, 3, 5):  # P12a through the CTA kernel, ragged rows per CTA
                     p.set_row_blocks(nb)
                     rb = p.solve(b, None, 12, 0.0, history=True)
@@ -684,6 +697,28 @@ def test_dynamic_tile_default_sizes_vs_oracle(jb, n, seed, max_iter, tol):
     st_o, x_o, it_o = oracle.jacobi(A, b, x0, max_iter, tol, nthreads=16)
     with jb.Plan(A) as p:
         assert jb.variant_name(p.info.variant) == "k_sweep_cta R4 U2 L2-policy dynamic"
+        r = p.solve(b, x0, max_iter, tol)
+    assert (r.status, r.iters) == (st_o, it_o)
+    assert rel_linf(r.x, x_o) <= TOL64
+
+
+@pytest.mark.parametrize("n,seed,max_iter,tol", [(33001, 4, 5, 0.0), (40000, 5, 60, 1e-9)])
+def test_group_kernel_default_sizes_vs_oracle(jb, n, seed, max_iter, tol):
+    """fp32 A with >= 16 column chunks and fewer than 512 rows per SM: the default is the group kernel
+    (4 warps per 8-row tile, chunk sums folded in ascending order).  Ragged n (a partial
+    last chunk and tile): same status and iteration count as the oracle on the same fp32 values
+    (PAPER.md:59-66), relative L-inf error <= 1e-10 (both sides accumulate in fp64)."""
+    rng = np.random.default_rng(seed)
+    A = rng.random((n, n), dtype=np.float32)
+    A *= 2
+    A -= 1
+    np.fill_diagonal(A, 0.0)
+    np.fill_diagonal(A, (np.abs(A).sum(1, dtype=np.float64) * 1.05).astype(np.float32))
+    b = rng.uniform(-1, 1, n)
+    x0 = rng.uniform(-1, 1, n)
+    st_o, x_o, it_o = oracle.jacobi(A, b, x0, max_iter, tol, nthreads=16)
+    with jb.Plan(A) as p:
+        assert jb.variant_name(p.info.variant) == "k_sweep_group R8 G4 x-smem"
         r = p.solve(b, x0, max_iter, tol)
     assert (r.status, r.iters) == (st_o, it_o)
     assert rel_linf(r.x, x_o) <= TOL64
