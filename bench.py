@@ -324,10 +324,12 @@ NEXT_RUNS = (("c3", 1000, 0.0, "l2", 1), ("c3", 1000, 0.0, "max", 8))
 
 def other_configs(jb, g, torch, stream):
     """Rates of the other BASELINE.json configs on this GPU (informational; the headline is c4):
-    device-resident inputs, best of 3 solves after a warm-up, CUDA events on the plan's stream.
+    device-resident inputs, best of 3 solves (10 for c1/c2) after a warm-up, CUDA events on the plan's
+    stream; a 1 s pause first lets the SM clock recover from the headline's power-capped run.
     it/s = sweeps / time; GB/s = algorithmic bytes per sweep x it/s (c1/c2 sit in or near L2)."""
     out = []
     sh = stream.cuda_stream
+    time.sleep(1.0)
     for name in dict.fromkeys(r[0] for r in OTHER_RUNS):
         cfg = g.CONFIGS[name]
         n = cfg.n
@@ -348,7 +350,8 @@ def other_configs(jb, g, torch, stream):
                 p.set_col_blocks(colblocks)
                 r = p.solve_device(db, dx0, dxo, max_iter, tol)
                 best = None
-                for _ in range(3):
+                # latency-bound small configs (c1, c2: µs per solve, clock-sensitive): best of 10
+                for _ in range(10 if n <= 4096 else 3):
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record(stream)
                     r = p.solve_device(db, dx0, dxo, max_iter, tol)
