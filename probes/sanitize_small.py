@@ -30,7 +30,8 @@ CASES = ((1, False, [None], ["0"]), (37, False, [None], ["0"]), (300, True, [Non
          (700, False, [None], ["1", "0"]), (3001, False, [None, "0", "3", "5", "6"], ["1", "0"]),
          (2049, True, [None, "5", "6", "12"], ["1", "0"]),
          (8190, False, [None, "0", "1", "2", "3", "5", "6", "7", "8", "9", "10", "12"], ["0"]),
-         (8190, True, [None, "0", "5", "6", "12"], ["0"]), (20000, True, ["12"], ["0"]))
+         (8190, True, [None, "0", "5", "6", "12"], ["0"]), (20000, True, ["12"], ["0"]),
+         (300, True, ["12"], ["0"]), (149, False, ["12"], ["0"]))
 for n, f32, variants, modes in (((3001, False, [None], ["0"]),) if QUICK else CASES):
     A, b = dominant(n, n, f32)
     for v, mode in [(v, m) for v in variants for m in modes]:
@@ -39,6 +40,10 @@ for n, f32, variants, modes in (((3001, False, [None], ["0"]),) if QUICK else CA
             os.environ.pop("JACOBI_SWEEP_VARIANT", None)
         else:
             os.environ["JACOBI_SWEEP_VARIANT"] = v
+        if v is not None and n < 1000:  # a forced sweep variant on a small n: graph path, not the cluster solver
+            os.environ["JACOBI_SMALL_N"] = "0"
+        else:
+            os.environ.pop("JACOBI_SMALL_N", None)
         with jb.Plan(A) as p:
             ran = jb.variant_name(p.info.variant)
             r = p.solve(b, None, 6, 0.0, history=True)

@@ -724,6 +724,26 @@ def test_group_kernel_default_sizes_vs_oracle(jb, n, seed, max_iter, tol):
     assert rel_linf(r.x, x_o) <= TOL64
 
 
+@pytest.mark.parametrize("n,f32", [(300, True), (149, False), (600, True)])
+def test_group_kernel_few_rows_per_cta(jb, n, f32, monkeypatch):
+    """The group kernel (variant 12) on the graph path with fewer rows per CTA than groups (n = 149 / 300:
+    1-2 rows per CTA, so some of a CTA's 4 groups own no tile and the x ring counts only the others):
+    bitwise equal to the row-panel kernel (variant 6) and to the item kernel, within 1e-10 of the oracle."""
+    A, b, _ = dominant(n, 900 + n, scale=1.05, f32=f32)
+    orc = oracle.jacobi(A, b, None, 30, 1e-11, nthreads=16, history=True)
+    monkeypatch.setenv("JACOBI_SMALL_N", "0")
+    monkeypatch.setenv("JACOBI_PERSIST", "0")
+    out = {}
+    for v in ("12", "6", "0"):
+        monkeypatch.setenv("JACOBI_SWEEP_VARIANT", v)
+        with jb.Plan(A) as p:
+            assert p.info.variant == int(v), (v, p.info.variant)
+            out[v] = p.solve(b, None, 30, 1e-11, history=True)
+    match_oracle(out["12"], orc)
+    for v in ("6", "0"):
+        assert np.array_equal(out[v].x, out["12"].x) and np.array_equal(out[v].hist, out["12"].hist), v
+
+
 def test_time_shard_hook(jb):
     """jacobi_plan_time_shard (per-GPU shard measurement): runs the three modes on a rank's row block,
     reports the variant its plan would pick, rejects bad arguments, and leaves the plan usable (the
