@@ -330,7 +330,7 @@ def _tie_margin_ok(h_gpu, h_orc, it, tol):
     return ok_last and ok_prev, delta
 
 
-def test_c4_full_parity_all_rows(jb):
+def test_c4_full_parity_all_rows(jb, monkeypatch):
     """BASELINE.json configs[3] at full size in the bench's launch configuration (n = 65536, 34.4 GB,
     the dynamic-tile default kernel): against the oracle over the WHOLE system (PAPER.md:55 component
     equation, PAPER.md:59-66 loop) — every one of the 65536 entries after each of sweeps 1-8 (sweep 1
@@ -373,6 +373,21 @@ def test_c4_full_parity_all_rows(jb):
         assert rel_linf(x100, x100_orc) <= TOL64
         np.testing.assert_allclose(hist.cpu().numpy(), h_orc, rtol=1e-9, atol=1e-14)
         assert np.max(np.abs(x100 - g.host_xstar(cfg))) <= 1e-12  # P8 planted solution
+        r = p.solve_device(db, dx0, dxo, 3, 0.0)
+        x3 = dxo.cpu().numpy()
+    # the kernels the P = 2 / 4 / 8 ranks pick for their 32768 / 16384 / 8192-row blocks (the dynamic-tile
+    # kernel at P = 2, the static L2-policy CTA kernel at P = 4 and 8), forced on the same borrowed A as
+    # 2 / 4 / 8 row blocks of exactly those shapes: sweeps 1-3 bitwise equal to the P = 1 run (P12)
+    for v, nbs in (("10", (2,)), ("7", (4, 8))):
+        monkeypatch.setenv("JACOBI_SWEEP_VARIANT", v)
+        with jb.Plan(dA) as p:
+            assert p.info.variant == int(v)
+            for nb in nbs:
+                p.set_row_blocks(nb)
+                q = p.solve_device(db, dx0, dxo, 3, 0.0)
+                assert (q.status, q.iters) == (jb.MAX_ITER, 3)
+                assert np.array_equal(dxo.cpu().numpy(), x3), (v, nb)
+    monkeypatch.delenv("JACOBI_SWEEP_VARIANT")
     del dA
     torch.cuda.empty_cache()
 
