@@ -199,6 +199,25 @@ def test_p9_contraction_bounds():
             assert h[k] <= tn * h[k - 1] + 1e-14
 
 
+def test_p9b_slow_companion_rate_is_exactly_one_over_1_05():
+    """SURVEY.md Q21's slow companion (off-diagonals U[0,1); a_ii = 1.05 x row sum):
+    T = -D^-1(L+U) is entrywise non-positive with every row of |T| summing to 1/1.05, so T 1 = -(1/1.05) 1
+    and rho(T) = ||T||inf = 1/1.05 (Perron).  Once that mode dominates, d_{k+1} / d_k equals 1/1.05 to
+    rounding; a dropped or doubled term, a wrong diagonal or an off-by-one row index changes the rate."""
+    rng = np.random.default_rng(5)
+    for n in (50, 200):
+        A = rng.uniform(0, 1, (n, n))
+        np.fill_diagonal(A, 0.0)
+        np.fill_diagonal(A, 1.05 * A.sum(1))
+        b = A @ rng.uniform(-1, 1, n)
+        st, x, it, h = oracle.jacobi(A, b, None, 300, 0.0, history=True)
+        assert (st, it) == (oracle.MAX_ITER, 300)
+        h = np.asarray(h)
+        assert np.all(h[1:] <= h[:-1] / 1.05 + 1e-14)  # ||T||inf bound (P9) from the first sweep on
+        ratio = h[1:] / h[:-1]
+        assert np.max(np.abs(ratio[100:250] - 1 / 1.05)) <= 1e-8
+
+
 # ---------------------------------------------------------------- P10: exact rational brute force
 def test_p10_exact_rational_brute_force():
     rng = np.random.default_rng(10)

@@ -290,6 +290,36 @@ def test_c3_full_parity_and_shards(jb):
         assert np.max(np.abs(f.x - xs)) <= 1e-12  # P8 planted solution
 
 
+def slow_companion(n, seed):
+    """SURVEY.md Q21 / DESIGN.md R21: the truly slow companion of c3 — off-diagonals U[0,1) (the
+    paper's own distribution) and a_ii = 1.05 x row sum, so T = -D^-1(L+U) is entrywise
+    non-positive with every row of |T| summing to 1/1.05: rho(T) = 1/1.05 and ~360-380 sweeps to 1e-10."""
+    rng = np.random.default_rng(seed)
+    A = rng.uniform(0, 1, (n, n))
+    np.fill_diagonal(A, 0.0)
+    np.fill_diagonal(A, 1.05 * A.sum(1))
+    xs = rng.uniform(-1, 1, n)
+    return A, A @ xs, xs
+
+
+@pytest.mark.parametrize("n", [1500, 4096, 10007])
+def test_slow_companion_iteration_count(jb, n):
+    """A long tol run on the slow companion, on the persistent path (n = 1500, 4096)
+    and the graph path (n = 10007, ragged): same status and iteration count as the oracle over
+    ~370 sweeps of different summation orders (R20 margin checked), x within 1e-10, every d_k."""
+    A, b, xs = slow_companion(n, 100 + n)
+    st_o, x_o, it_o, h_o = oracle.jacobi(A, b, None, 5000, 1e-10, nthreads=16, history=True)
+    assert st_o == oracle.CONVERGED and it_o > 300
+    with jb.Plan(A) as p:
+        r = p.solve(b, None, 5000, 1e-10, history=True)
+    assert (r.status, r.iters) == (jb.CONVERGED, it_o), (r.iters, it_o)
+    ok, delta = _tie_margin_ok(r.hist, h_o, it_o, 1e-10)
+    assert ok, (delta, h_o[it_o - 2], h_o[it_o - 1])
+    assert rel_linf(r.x, x_o) <= TOL64
+    np.testing.assert_allclose(r.hist, h_o, rtol=1e-9, atol=1e-14)
+    assert np.max(np.abs(r.x - xs)) <= 1e-9  # converged to the planted solution (|x - x*| ~ d / (1 - rho))
+
+
 def _twin_rows_check(cfg, dA, db, b_all, rows):
     """Device twin of the generator == host generator on sampled rows of A and on all of b (the two
     sides of every full-size parity test start from the same bits)."""
