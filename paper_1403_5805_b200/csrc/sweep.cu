@@ -291,12 +291,30 @@ __device__ __forceinline__ void accumulate_chunk(const T* const (&rowp)[R], cons
           }
         }
       }
+#ifdef JACOBI_PROBE_NOFMA
+      // Probe build only (wrong results): the same loads, each A element folded into the sum's bits
+      // with one integer XOR instead of convert + DFMA, x^(k-1) once per step — separates the load
+      // pattern's rate from the arithmetic's (profiles/nofma_probe_r02.txt).
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          long long bits = __double_as_longlong(acc[r]) ^ __double_as_longlong(xv[u][r % E]);
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            if constexpr (sizeof(T) == 4) bits ^= (long long)__float_as_int((float)av[u][r][e]) << (e & 1) * 32;
+            else bits ^= __double_as_longlong((double)av[u][r][e]);
+          }
+          acc[r] = __longlong_as_double(bits);
+        }
+#else
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int r = 0; r < R; ++r)
 #pragma unroll
           for (int e = 0; e < E; ++e) acc[r] = __fma_rn((double)av[u][r][e], xv[u][e], acc[r]);
+#endif
     };
     // PIN: one step per loop trip (no compiler unrolling).  In the persistent solver's register
     // budget an unrolled pair of steps is interleaved so that the first FMA waits on the first loads
