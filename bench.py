@@ -326,7 +326,8 @@ def other_configs(jb, g, torch, stream):
     """Rates of the other BASELINE.json configs on this GPU (informational; the headline is c4):
     device-resident inputs, best of 3 solves (10 for c1/c2) after a warm-up, CUDA events on the plan's
     stream; a 1 s pause first lets the SM clock recover from the headline's power-capped run.
-    it/s = sweeps / time; GB/s = algorithmic bytes per sweep x it/s (c1/c2 sit in or near L2)."""
+    it/s = sweeps / time; GB/s = algorithmic bytes per sweep x it/s (c1/c2 sit in or near L2); for the
+    footprint above 32 GiB (c5) the read-only ceiling over min(A, 64 GiB) is measured beside it."""
     out = []
     sh = stream.cuda_stream
     time.sleep(1.0)
@@ -372,6 +373,14 @@ def other_configs(jb, g, torch, stream):
                                                           "one GPU (NEXT-4 emulation: slab GEMVs + column-sum epilogue)")})
             p.set_norm("max")
             p.set_col_blocks(1)
+            if inf.bytes_per_sweep > (32 << 30):  # c5: the read ceiling over its own footprint (capped at
+                # 64 GiB), measured here beside its rates (the headline's ceiling covers 32 GiB; a probe
+                # over c3's 2.1 GB is one 0.3 ms launch per pass, ramp-bound, so it is not reported)
+                ceil = jb.bwprobe(int(min(inf.bytes_per_sweep, 64 << 30)), 3)
+                for e in out:
+                    if e["config"] == name:
+                        e["read_ceiling_gbs"] = round(ceil, 1)
+                        e["frac_of_read_ceiling"] = round(e["effective_gbs"] / ceil, 3)
         del dA, db
         torch.cuda.empty_cache()
     return out
