@@ -57,6 +57,37 @@ __global__ void k_read(const double* __restrict__ buf, size_t nelem, double* out
   if (acc == 12345.678) out[0] = acc;  // keep loads alive
 }
 
+// Mixed L2 policy (the persistent solver's traffic without its arithmetic, barriers or stop test):
+// 8 KB unit u is loaded with L2 evict_last iff frac(u * phi) < keep / 1000 (the solver's Weyl keep
+// rule), else evict_first; 256-bit no-L1 loads, U in flight per thread, `reps` passes per launch.
+__device__ __forceinline__ void ld256p(const void* p, double& a, double& b, double& c, double& d, uint64_t pol) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+               : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p), "l"(pol));
+}
+template <int U>
+__global__ void k_read_keep(const double* __restrict__ buf, size_t nelem, double* out, int reps, unsigned thr) {
+  uint64_t pk, ps;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pk));
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(ps));
+  const size_t nvec = nelem / 4;
+  const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x, stride = (size_t)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  for (int rep = 0; rep < reps; ++rep) {
+    for (size_t i = tid; i + (U - 1) * stride < nvec; i += U * stride) {
+      double v[U][4];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const size_t j = i + u * stride;
+        const unsigned unit = (unsigned)(j >> 8);  // 256 vectors of 32 B = 8 KB
+        ld256p(buf + j * 4, v[u][0], v[u][1], v[u][2], v[u][3], unit * 2654435769u < thr ? pk : ps);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc += (v[u][0] + v[u][1]) + (v[u][2] + v[u][3]);
+    }
+  }
+  if (acc == 12345.678) out[0] = acc;
+}
+
 __global__ void k_fill(double* buf, size_t n) {
   size_t stride = (size_t)gridDim.x * blockDim.x;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += stride) buf[i] = (double)(i & 1023) * 1e-3;
@@ -161,6 +192,14 @@ int main(int argc, char** argv) {
     fflush(stdout);
   };
   const int passes = mib ? 20 : 1;  // small buffers: 20 passes per launch so the launch does not dominate
+  if (argc > 4 && argv[3][0] == 'k') {  // "probes/bwprobe N mib keep P": mixed-policy streaming only
+    const int keep = atoi(argv[4]);
+    const unsigned thr = keep >= 1000 ? 0xffffffffu : (unsigned)(((unsigned long long)keep << 32) / 1000ull);
+#define RUNK(U, TPB, BPS) { double ms = time_best([&]{ k_read_keep<U><<<nsm * BPS, TPB>>>(buf, n, out, passes, thr); }, 5); \
+    char nm[64]; snprintf(nm, 64, "keep%d_u%d", keep, U); rep(nm, TPB, BPS, ms, (double)nbytes * passes); }
+    RUNK(8, 512, 1); RUNK(4, 1024, 1); RUNK(16, 512, 1); RUNK(8, 256, 4); RUNK(4, 512, 4);  // 128/128/256/256/256 KB in flight per SM
+    return 0;
+  }
 #define RUN(U, MODE, TPB, BPS) { double ms = time_best([&]{ k_read<U, MODE><<<nsm * BPS, TPB>>>(buf, n, out, passes); }, 5); \
     char nm[64]; snprintf(nm, 64, "read_m%d_u%d", MODE, U); rep(nm, TPB, BPS, ms, (double)nbytes * passes); }
   RUN(4, 0, 256, 8); RUN(8, 0, 256, 8); RUN(16, 0, 256, 4); RUN(8, 0, 512, 4); RUN(8, 0, 1024, 2);
