@@ -376,11 +376,17 @@ def other_configs(jb, g, torch, stream):
             if inf.bytes_per_sweep > (32 << 30):  # c5: the read ceiling over its own footprint (capped at
                 # 64 GiB), measured here beside its rates (the headline's ceiling covers 32 GiB; a probe
                 # over c3's 2.1 GB is one 0.3 ms launch per pass, ramp-bound, so it is not reported)
-                ceil = jb.bwprobe(int(min(inf.bytes_per_sweep, 64 << 30)), 3)
+                try:  # informational: a failed probe (e.g. no room beside A) must not cost the line
+                    ceil = jb.bwprobe(int(min(inf.bytes_per_sweep, 64 << 30)), 3)
+                except jb.JacobiError as ex:
+                    ceil, err = None, str(ex)
                 for e in out:
                     if e["config"] == name:
-                        e["read_ceiling_gbs"] = round(ceil, 1)
-                        e["frac_of_read_ceiling"] = round(e["effective_gbs"] / ceil, 3)
+                        if ceil:
+                            e["read_ceiling_gbs"] = round(ceil, 1)
+                            e["frac_of_read_ceiling"] = round(e["effective_gbs"] / ceil, 3)
+                        else:
+                            e["read_ceiling_error"] = err
         del dA, db
         torch.cuda.empty_cache()
     return out
