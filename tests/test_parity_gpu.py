@@ -221,6 +221,33 @@ def test_errors_and_edges_on_gpu(jb):
     assert (r.status, r.iters) == (jb.CONVERGED, 1) and np.array_equal(r.x, [1.0, 2.0, 3.0])  # P5
 
 
+@pytest.mark.parametrize("n,f32", [(256, False), (2000, False), (5000, False), (3001, True), (9001, True)])
+def test_p6_row_scaling_and_p4_diagonal_on_every_path(jb, n, f32):
+    """Pins P6 and P4 on the CUDA path, at sizes that take the cluster (256),
+    persistent (2000, fp32 3001) and graph (5000, fp32 9001) paths.
+    P6: scaling row i of A and b_i by 2^e_i (PAPER.md:55 is homogeneous per row: every product, partial
+    sum and the division scale exactly) leaves every iterate and every d_k bitwise unchanged — a row
+    index off by one anywhere (b_i, a_ii, the diagonal mask, x_i^(k-1) of the epilogue) breaks it.
+    P4: a diagonal system gives x = b / diag after sweep 1 and d_2 = 0, i.e. CONVERGED at k = 2."""
+    A, b, _ = dominant(n, 600 + n, scale=1.1, f32=f32)
+    rng = np.random.default_rng(n)
+    s = np.ldexp(1.0, rng.integers(-20, 21, n))
+    As = (A.astype(np.float64) * s[:, None]).astype(A.dtype)  # exact: powers of two, no over/underflow
+    x0 = rng.uniform(-1, 1, n)
+    with jb.Plan(A) as p, jb.Plan(As) as q:
+        assert (p.info.persistent_ctas > 0) == (q.info.persistent_ctas > 0)
+        r = p.solve(b, x0, 12, 0.0, history=True)
+        rs = q.solve(b * s, x0, 12, 0.0, history=True)
+    assert np.array_equal(r.x, rs.x) and np.array_equal(r.hist, rs.hist)
+    st_o, x_o, it_o, h_o = oracle.jacobi(A, b, x0, 12, 0.0, nthreads=16, history=True)
+    assert rel_linf(r.x, x_o) <= (TOL64 if not f32 else 1e-10)
+    D = np.diag(np.diag(A)).astype(A.dtype)
+    with jb.Plan(D) as p:
+        r = p.solve(b, None, 50, 1e-300, history=True)
+    assert (r.status, r.iters) == (jb.CONVERGED, 2)
+    assert np.array_equal(r.x, b / np.diag(A).astype(np.float64)) and r.hist[1] == 0.0
+
+
 def test_device_borrowed_A_and_device_solve(jb):
     import torch
     n = 3000
