@@ -175,13 +175,13 @@ def test_p13_p11_determinism_split_and_batch(jb):
 
 
 # ------------------------------------------------------------------ P14: divergent paper regime
-@pytest.mark.parametrize("n", [8, 64, 512])
+@pytest.mark.parametrize("n", [8, 64, 512, 2000, 5000])  # cluster, persistent (2000), graph (5000) paths
 def test_p14_divergence_nan_semantics(jb, n):
     rng = np.random.default_rng(14)
     A = rng.uniform(0, 1, (n, n))
     b = rng.uniform(0, 1, n)
     x0 = rng.uniform(0, 1, n)
-    st_o, x_o, it_o, h_o = oracle.jacobi(A, b, x0, 1000, 1e-8, history=True)
+    st_o, x_o, it_o, h_o = oracle.jacobi(A, b, x0, 1000, 1e-8, nthreads=16, history=True)
     with jb.Plan(A) as p:
         r = p.solve(b, x0, 1000, 1e-8, history=True)
     assert (r.status, r.iters) == (st_o, it_o) == (jb.MAX_ITER, 1000)
