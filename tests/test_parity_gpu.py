@@ -774,6 +774,42 @@ def test_dynamic_tile_default_sizes_vs_oracle(jb, n, seed, max_iter, tol):
     assert rel_linf(r.x, x_o) <= TOL64
 
 
+def test_dynamic_tile_every_sweep_on_slow_companion(jb):
+    """The dynamic-tile kernel (tiles claimed from a launch-wide counter, reset once per launch) over
+    150 sweeps of a system that does not converge within them (R21's slow companion, rho(T) = 1/1.05):
+    a tile dropped or done twice in any sweep leaves an error of order d_k that decays only by 1/1.05 per
+    sweep, so every d_k and the final x against the oracle pin every sweep — unlike
+    a fast-converging system, where Jacobi heals such an error before the last iterate."""
+    n = 20001
+    A, b, _ = slow_companion(n, 20001)
+    x0 = np.random.default_rng(3).uniform(-1, 1, n)
+    st_o, x_o, it_o, h_o = oracle.jacobi(A, b, x0, 150, 0.0, nthreads=16, history=True)
+    with jb.Plan(A) as p:
+        assert jb.variant_name(p.info.variant) == "k_sweep_cta R4 U2 L2-policy dynamic"
+        r = p.solve(b, x0, 150, 0.0, history=True)
+    assert (r.status, r.iters) == (st_o, it_o) == (jb.MAX_ITER, 150)
+    assert h_o[-1] > 1e-6  # still far from converged: no healing
+    assert rel_linf(r.x, x_o) <= TOL64
+    np.testing.assert_allclose(r.hist, h_o, rtol=1e-9, atol=1e-14)
+
+
+def test_group_kernel_every_sweep_on_slow_companion(jb):
+    """The same every-sweep pin for the fp32 group kernel (the c5-shard default below 512 rows per SM):
+    60 sweeps of the slow companion stored in fp32, n = 33001 (ragged), still far from converged."""
+    n = 33001
+    A, b, _ = slow_companion(n, 33001)
+    A = A.astype(np.float32)
+    x0 = np.random.default_rng(4).uniform(-1, 1, n)
+    st_o, x_o, it_o, h_o = oracle.jacobi(A, b, x0, 60, 0.0, nthreads=16, history=True)
+    with jb.Plan(A) as p:
+        assert jb.variant_name(p.info.variant) == "k_sweep_group R8 G4 x-smem"
+        r = p.solve(b, x0, 60, 0.0, history=True)
+    assert (r.status, r.iters) == (st_o, it_o) == (jb.MAX_ITER, 60)
+    assert h_o[-1] > 1e-4
+    assert rel_linf(r.x, x_o) <= 1e-10  # fp32 storage, fp64 arithmetic on both sides: self-check bar
+    np.testing.assert_allclose(r.hist, h_o, rtol=1e-9, atol=1e-14)
+
+
 @pytest.mark.parametrize("n,seed,max_iter,tol", [(33001, 4, 5, 0.0), (40000, 5, 60, 1e-9)])
 def test_group_kernel_default_sizes_vs_oracle(jb, n, seed, max_iter, tol):
     """fp32 A with >= 16 column chunks and fewer than 512 rows per SM: the default is the group kernel
