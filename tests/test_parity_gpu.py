@@ -701,6 +701,26 @@ def test_fused_exchange_emulated_ranks_bitwise(jb):
         assert np.array_equal(r.hist, ref.hist)
 
 
+@pytest.mark.parametrize("persist", ["0", "1"])
+def test_fused_exchange_every_sweep_on_slow_companion(jb, monkeypatch, persist):
+    """NEXT-1's protocol pinned per sweep: P = 2/4/8 emulated ranks pushing
+    x_i^(k) into every rank's copy (graph kernels, and the persistent push solver) over 120 sweeps of the
+    slow companion, far from convergence — a missed or late push leaves stale x_j^(k-1) in a rank's copy,
+    an error of order d_k that decays only by 1/1.05 per sweep — every d_k and x against the oracle."""
+    monkeypatch.setenv("JACOBI_PERSIST", persist)
+    n = 8192
+    A, b, _ = slow_companion(n, 8192)
+    x0 = np.random.default_rng(5).uniform(-1, 1, n)
+    orc = oracle.jacobi(A, b, x0, 120, 0.0, nthreads=16, history=True)
+    assert orc[3][-1] > 1e-6  # still far from converged (d_120 ~ 1e-5)
+    for P in (2, 4, 8):
+        with jb.Plan(A) as p:
+            p.set_p2p_emulation(P)
+            assert (p.info.persistent_ctas > 0) == (persist == "1")
+            r = p.solve(b, x0, 120, 0.0, history=True)
+        match_oracle(r, orc)
+
+
 def test_fused_exchange_silent_peer_faults_instead_of_hanging(jb, monkeypatch):
     """A rank whose kernels never signal (fault injection: virtual rank 1 of 2 is never launched)
     must not hang its peers: the next sweep's wait for the signals is bounded (JACOBI_PEER_WAIT_MS),
