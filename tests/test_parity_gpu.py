@@ -701,6 +701,27 @@ def test_fused_exchange_emulated_ranks_bitwise(jb):
         assert np.array_equal(r.hist, ref.hist)
 
 
+def test_slabs_and_row_blocks_every_sweep_on_slow_companion(jb):
+    """NEXT-4's column slabs (P = 2/4/8 slabs emulated on one GPU) and the row-block
+    split (P12a) over 120 sweeps of the slow companion, far from convergence: every d_k and
+    x against the oracle (slabs re-associate the chunk sums: tolerance), row blocks bitwise = P = 1."""
+    n = 8192
+    A, b, _ = slow_companion(n, 8193)
+    x0 = np.random.default_rng(6).uniform(-1, 1, n)
+    orc = oracle.jacobi(A, b, x0, 120, 0.0, nthreads=16, history=True)
+    with jb.Plan(A) as p:
+        ref = p.solve(b, x0, 120, 0.0, history=True)
+        match_oracle(ref, orc)
+        for P in (2, 4, 8):
+            p.set_col_blocks(P)
+            match_oracle(p.solve(b, x0, 120, 0.0, history=True), orc)
+        p.set_col_blocks(1)
+        for P in (2, 4, 8):
+            p.set_row_blocks(P)
+            r = p.solve(b, x0, 120, 0.0, history=True)
+            assert np.array_equal(r.x, ref.x) and np.array_equal(r.hist, ref.hist), P
+
+
 @pytest.mark.parametrize("persist", ["0", "1"])
 def test_fused_exchange_every_sweep_on_slow_companion(jb, monkeypatch, persist):
     """NEXT-1's protocol pinned per sweep: P = 2/4/8 emulated ranks pushing
