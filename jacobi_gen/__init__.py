@@ -136,3 +136,18 @@ def device_xstar(cfg: GenConfig, ptr: int, stream: int = 0):
     c = cfg.c()
     if _load().jgen_device_xstar(ctypes.byref(c), ctypes.c_void_p(ptr), ctypes.c_void_p(stream)) != 0:
         raise RuntimeError("jgen_device_xstar failed")
+
+
+def slow_companion(n: int, seed: int, f32: bool = False):
+    """(A, b, x*) of c3's truly slow companion (R21; a parity case, not a
+    BASELINE.json config): off-diagonals U[0,1) — the paper's own distribution, PAPER.md:154 — and
+    a_ii = 1.05 x the row sum, so T = -D^-1(L+U) has rho(T) = 1/1.05 (~360-380 sweeps to 1e-10).
+    numpy's seeded generator on the host (sizes that fit host RAM); b = A x* over the stored values."""
+    rng = np.random.default_rng(seed)
+    A = rng.uniform(0, 1, (n, n))
+    np.fill_diagonal(A, 0.0)
+    np.fill_diagonal(A, 1.05 * A.sum(1))
+    if f32:
+        A = A.astype(np.float32)
+    xs = rng.uniform(-1, 1, n)
+    return A, A.astype(np.float64) @ xs, xs

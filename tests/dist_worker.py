@@ -9,7 +9,8 @@ C-ABI with every distributed exchange the library has:
   cols        column slabs + NCCL reduce-scatter (NEXT-4)
 Rank 0 writes every result (x, iters, status, d_k history, or the error) to an .npz file.
 
-python -m torch.distributed.run --nproc-per-node P tests/dist_worker.py OUT.npz name:n:mode:scale ...
+python -m torch.distributed.run --nproc-per-node P tests/dist_worker.py OUT.npz name:n:scale ...
+(name "slow": the slow companion of jacobi_gen, scale unused)
 """
 import os
 import sys
@@ -28,10 +29,18 @@ RUNS = ((30, 0.0), (3000, 1e-10))
 MODES = ("nccl", "p2p", "p2p_persist", "cols")
 
 
-def block(cfg, rank, world, layout, stream):
+SLOW_SEED = 7  # the "slow" system: jacobi_gen.slow_companion(n, SLOW_SEED)
+
+
+def block(cfg, rank, world, layout, stream, host=None):
     n = cfg.n
     row0, m = jb.partition(n, world, rank)
     db = torch.empty(m, dtype=torch.float64, device="cuda")
+    if host is not None:  # a host-built system (A, b): this rank's rows or column slab
+        A, b = host
+        dA = torch.from_numpy(np.ascontiguousarray(A[row0:row0 + m] if layout == "rows" else A[:, row0:row0 + m]))
+        db.copy_(torch.from_numpy(b[row0:row0 + m]))
+        return dA.cuda(), db
     if layout == "rows":
         dA = torch.empty((m, n), dtype=torch.float64, device="cuda")
         g.device_rows(cfg, row0, row0 + m, dA.data_ptr(), n, db.data_ptr(), stream)
@@ -58,12 +67,13 @@ def main():
     for spec in specs:
         name, n, scale = spec.split(":")
         cfg = g.GenConfig(int(n), seed=3, diag_mode=g.DIAG_SCALE, diag_scale=float(scale))
+        host = g.slow_companion(int(n), SLOW_SEED)[:2] if name == "slow" else None
         for mode in MODES:
             os.environ["JACOBI_PERSIST"] = "1" if mode == "p2p_persist" else "0"
             layout = "cols" if mode == "cols" else "rows"
             if mode == "cols" and (cfg.n // world) % 8 != 0:
                 continue  # column slabs must be a multiple of 8 columns (jacobi.h)
-            dA, db = block(cfg, rank, world, layout, stream)
+            dA, db = block(cfg, rank, world, layout, stream, host)
             try:
                 with dist_plan(dA, cfg.n, stream=stream, layout=layout, p2p=mode.startswith("p2p")) as p:
                     info = p.info

@@ -4,8 +4,9 @@ plan and the oracle (skipped when fewer than 2 GPUs are visible).
 Row blocks (§3) with the NCCL allgather + max allreduce, the fused
 NVLink push exchange (NEXT-1) in the graph path and in the persistent solver,
 and column slabs with a reduce-scatter (NEXT-4), for P = 2 .. min(8, #GPUs), on the
-c3 recipe (n = 16384, diagonal 1.05 x row abs-sum) and a ragged n = 13440 (26.25 column chunks,
-divisible by 2..8).  Row-block results must be bitwise equal to the 1-GPU plan (pin P12(b): the
+c3 recipe (n = 16384, diagonal 1.05 x row abs-sum), a ragged n = 13440 (26.25 column chunks,
+divisible by 2..8) and the slow companion (n = 8400, rho(T) = 1/1.05: no self-healing of a missed
+exchange within the 30-sweep run, ~370 sweeps for the tol run).  Row-block results must be bitwise equal to the 1-GPU plan (pin P12(b): the
 per-row summation order depends only on column indices) and match the oracle (status, iteration count,
 x at relative L-inf <= 1e-10, d_k history); column slabs match the oracle within the same tolerance.
 """
@@ -21,7 +22,7 @@ import oracle
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SYSTEMS = (("c3", 16384, 1.05), ("ragged", 13440, 1.05))
+SYSTEMS = (("c3", 16384, 1.05), ("ragged", 13440, 1.05), ("slow", 8400, 0.0))  # slow: SURVEY.md Q21
 RUNS = ((30, 0.0), (3000, 1e-10))
 
 
@@ -59,8 +60,11 @@ def test_multi_gpu_exchanges_vs_one_gpu_and_oracle(P, tmp_path):
     res = dict(np.load(out))
     import paper_1403_5805_b200 as jb
     for name, n, scale in systems:
-        cfg = g.GenConfig(n, seed=3, diag_mode=g.DIAG_SCALE, diag_scale=scale)
-        A, b, _ = g.host_system(cfg)
+        if name == "slow":  # far from convergence after 30 sweeps: a missed exchange cannot self-heal
+            A, b, _ = g.slow_companion(n, 7)  # tests/dist_worker.py SLOW_SEED
+        else:
+            cfg = g.GenConfig(n, seed=3, diag_mode=g.DIAG_SCALE, diag_scale=scale)
+            A, b, _ = g.host_system(cfg)
         with jb.Plan(A) as p1:
             one = {(mi, tol): p1.solve(b, None, mi, tol, history=True) for mi, tol in RUNS}
         orc = {(mi, tol): oracle.jacobi(A, b, None, mi, tol, nthreads=16, history=True) for mi, tol in RUNS}

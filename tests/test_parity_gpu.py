@@ -317,16 +317,8 @@ def test_c3_full_parity_and_shards(jb):
         assert np.max(np.abs(f.x - xs)) <= 1e-12  # P8 planted solution
 
 
-def slow_companion(n, seed):
-    """SURVEY.md Q21 / DESIGN.md R21: the truly slow companion of c3 — off-diagonals U[0,1) (the
-    paper's own distribution) and a_ii = 1.05 x row sum, so T = -D^-1(L+U) is entrywise
-    non-positive with every row of |T| summing to 1/1.05: rho(T) = 1/1.05 and ~360-380 sweeps to 1e-10."""
-    rng = np.random.default_rng(seed)
-    A = rng.uniform(0, 1, (n, n))
-    np.fill_diagonal(A, 0.0)
-    np.fill_diagonal(A, 1.05 * A.sum(1))
-    xs = rng.uniform(-1, 1, n)
-    return A, A @ xs, xs
+def slow_companion(n, seed, f32=False):
+    return g.slow_companion(n, seed, f32)  # SURVEY.md Q21 / DESIGN.md R21 (jacobi_gen: input construction)
 
 
 @pytest.mark.parametrize("n", [1500, 4096, 10007])
@@ -838,8 +830,7 @@ def test_group_kernel_every_sweep_on_slow_companion(jb):
     """The same every-sweep pin for the fp32 group kernel (the c5-shard default below 512 rows per SM):
     60 sweeps of the slow companion stored in fp32, n = 33001 (ragged), still far from converged."""
     n = 33001
-    A, b, _ = slow_companion(n, 33001)
-    A = A.astype(np.float32)
+    A, b, _ = slow_companion(n, 33001, f32=True)
     x0 = np.random.default_rng(4).uniform(-1, 1, n)
     st_o, x_o, it_o, h_o = oracle.jacobi(A, b, x0, 60, 0.0, nthreads=16, history=True)
     with jb.Plan(A) as p:
