@@ -158,9 +158,11 @@ int jacobi_plan_time_sweeps(jacobi_plan* plan, const double* d_b, const double* 
  * on the m x n block's shape only), and no exchange.  mode 0: a CUDA graph of sweep kernels (the
  * graph path); 1: the persistent grid solver on the shard; 2: the persistent fused-exchange kernel
  * (k_solve_gridsync_push) with its peer set reduced to this GPU (pushes, remote atomics and arrival
- * counters all local).  d_b (n) and d_x0 (n) are device vectors.  Writes the average ms per sweep
+ * counters all local); 3: rank `rank`'s column slab of an nranks-rank column-wise plan (NEXT-4,
+ * the n x m slab of columns [rank*m, (rank+1)*m) writing all n row sums, then the
+ * epilogue on the rank's m rows; m must be a multiple of 8).  d_b (n) and d_x0 (n) are device vectors.  Writes the average ms per sweep
  * (CUDA events around one warm launch of all sweeps) and, if variant_out is non-NULL, the sweep
- * variant (-1 / -2 for modes 1 / 2).  Rows outside the shard keep x0, so the iterates are not the
+ * variant (-1 / -2 for modes 1 / 2; the slab kernel's variant for mode 3).  Rows outside the shard keep x0, so the iterates are not the
  * system's: a measurement hook, not a solver.  Errors: EINVAL (distributed / emulating plan,
  * nranks does not divide n, bad arguments, persistent mode unsupported for this shape), ECUDA. */
 int jacobi_plan_time_shard(jacobi_plan* plan, int nranks, int rank, const double* d_b, const double* d_x0,

@@ -294,10 +294,11 @@ class Plan:
 
     def time_shard(self, b, x0, nranks, rank=0, sweeps=20, mode="graph"):
         """jacobi_plan_time_shard: ms per sweep of rank `rank`'s row block of an nranks-rank plan, on this
-        GPU, exchange excluded.  mode: "graph", "persistent" or "persistent-push".  Returns (ms, variant)."""
+        GPU, exchange excluded.  mode: "graph", "persistent", "persistent-push" or "colslab" (rank `rank`'s
+        column slab of a column-wise plan, NEXT-4).  Returns (ms, variant)."""
         ms = ctypes.c_float()
         v = ctypes.c_int()
-        m = {"graph": 0, "persistent": 1, "persistent-push": 2}[mode]
+        m = {"graph": 0, "persistent": 1, "persistent-push": 2, "colslab": 3}[mode]
         _check(_lib.jacobi_plan_time_shard(self._h, int(nranks), int(rank), _dev_ptr(b, self.n, "b"),
                                            _dev_ptr(x0, self.n, "x0"), int(sweeps), m, ctypes.byref(ms),
                                            ctypes.byref(v)))

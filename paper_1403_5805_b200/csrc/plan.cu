@@ -1074,10 +1074,12 @@ extern "C" int jacobi_plan_time_sweeps(jacobi_plan* p, const double* d_b, const 
 extern "C" int jacobi_plan_time_shard(jacobi_plan* p, int nranks, int rank, const double* d_b, const double* d_x0,
                                       int sweeps, int mode, float* ms_per_sweep, int* variant_out) {
   if (!p || nranks < 1 || rank < 0 || rank >= nranks || !d_b || !d_x0 || sweeps < 1 ||
-      sweeps > jacobi::kMaxSweepsPerLaunch || mode < 0 || mode > 2 || !ms_per_sweep || p->comm || p->colwise ||
+      sweeps > jacobi::kMaxSweepsPerLaunch || mode < 0 || mode > 3 || !ms_per_sweep || p->comm || p->colwise ||
       p->p2p || p->nblocks != 1 || p->colblocks != 1 || p->n % nranks != 0)
     return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_time_shard: 1-GPU row-wise plan, nranks | n, 0 <= rank < "
-                                           "nranks, 1 <= sweeps <= 4096, mode 0/1/2");
+                                           "nranks, 1 <= sweeps <= 4096, mode 0/1/2/3");
+  if (mode == 3 && (p->n / nranks) % 8 != 0)
+    return jacobi_set_error(JACOBI_EINVAL, "jacobi_plan_time_shard: column slabs need n / nranks a multiple of 8");
   JCUDA(cudaSetDevice(p->device));
   const int64_t ms = p->n / nranks, r0 = (int64_t)rank * ms;
   int l2 = 0;
@@ -1096,6 +1098,31 @@ extern "C" int jacobi_plan_time_shard(jacobi_plan* p, int nranks, int rank, cons
   a.sq = p->sq + r0;
   a.tiles = (int)((ms + jacobi::variant_rows_dt(v, p->dtype) - 1) / jacobi::variant_rows_dt(v, p->dtype));
   a.l2_keep_pm = keep;
+  double* slab_rsum = nullptr;
+  void* slab_A = nullptr;
+  if (mode == 3) {  // NEXT-4: rank `rank`'s n x m column slab (columns [r0, r0 + m)) writing all n row sums,
+    // stored as that rank stores it: a compact n x m block (lda = m), copied out of this plan's A
+    const int keep3 = l2_keep_for(l2, p->n, ms, p->dtype, p->num_sms);
+    choose_variant_for(p, ms, p->n, keep3, &v, &grid);
+    JLAST("slab variant");
+    a = sweep_args(p, 0);
+    a.col0 = r0;
+    a.cend = r0 + ms;
+    JCUDA(cudaMalloc(&slab_A, (size_t)(p->n * ms * esz)));
+    JCUDA(cudaMemcpy2DAsync(slab_A, (size_t)(ms * esz), (const char*)p->dA + (size_t)(r0 * esz), (size_t)(p->lda * esz),
+                            (size_t)(ms * esz), (size_t)p->n, cudaMemcpyDeviceToDevice, p->stream));
+    a.A = slab_A;  // kernels index A by global column: row i, column c at A[i * lda + c - col0]
+    a.lda = ms;
+    a.a_base = slab_A;
+    a.a_elems = p->n * ms;
+    a.m = p->n;
+    a.row0 = 0;
+    a.nchunks = (int)((ms + p->chunk - 1) / p->chunk);
+    a.tiles = (int)((p->n + jacobi::variant_rows_dt(v, p->dtype) - 1) / jacobi::variant_rows_dt(v, p->dtype));
+    a.l2_keep_pm = keep3;
+    JCUDA(cudaMalloc(&slab_rsum, (size_t)p->n * 8));
+    a.rsum = slab_rsum;
+  }
   int rc = 0;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   cudaGraphExec_t gx = nullptr;
@@ -1109,7 +1136,7 @@ extern "C" int jacobi_plan_time_shard(jacobi_plan* p, int nranks, int rank, cons
     return 0;
   };
   auto launch = [&]() -> int {
-    if (mode == 0) {
+    if (mode == 0 || mode == 3) {
       JCUDA(cudaGraphLaunch(gx, p->stream));
     } else if (mode == 1) {
       JCUDA(jacobi::launch_solve_gridsync(p->dtype, a, p->gbar, 1, sweeps, G, smem, p->stream));
@@ -1120,12 +1147,15 @@ extern "C" int jacobi_plan_time_shard(jacobi_plan* p, int nranks, int rank, cons
   };
   rc = [&]() -> int {
     const int nch = (int)((p->n + p->chunk - 1) / p->chunk);
-    if (mode == 0) {  // a graph of `sweeps` sweep kernels, like the rank's graph minus the collectives
+    if (mode == 0 || mode == 3) {  // a graph of `sweeps` sweep kernels, like the rank's graph minus the collectives
       cudaGraph_t g = nullptr;
       JCUDA(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
       int lrc = 0;
       for (int j = 0; j < sweeps && lrc == 0; ++j) {
         cudaError_t e = jacobi::launch_sweep(p->dtype, v, a, j, grid, p->stream);
+        if (e == cudaSuccess && mode == 3)  // the rank's epilogue on its own m rows (after the reduce-scatter)
+          e = jacobi::launch_colsum_epilogue(slab_rsum + r0, 1, ms, ms, r0, p->b + r0, p->diag + r0, p->x[0], p->x[1],
+                                             p->dslot, p->sq, JACOBI_NORM_MAX, p->st, j, p->stream);
         if (e != cudaSuccess) lrc = jacobi_set_error(JACOBI_ECUDA, std::string("shard sweep: ") + cudaGetErrorString(e));
       }
       cudaError_t ee = cudaStreamEndCapture(p->stream, &g);
@@ -1183,6 +1213,8 @@ extern "C" int jacobi_plan_time_shard(jacobi_plan* p, int nranks, int rank, cons
   if (e1) cudaEventDestroy(e1);
   if (ra) cudaFree(ra);
   if (pa) cudaFree(pa);
+  if (slab_rsum) cudaFree(slab_rsum);
+  if (slab_A) cudaFree(slab_A);
   cudaGetLastError();
   return rc;
 }

@@ -885,7 +885,8 @@ def test_group_kernel_few_rows_per_cta(jb, n, f32, monkeypatch):
 
 
 def test_time_shard_hook(jb):
-    """jacobi_plan_time_shard (per-GPU shard measurement): runs the three modes on a rank's row block,
+    """jacobi_plan_time_shard (per-GPU shard measurement): runs the three row-block modes and the column
+    slab mode (NEXT-4) of a rank,
     reports the variant its plan would pick, rejects bad arguments, and leaves the plan usable (the
     next solve still matches the oracle)."""
     import torch
@@ -896,11 +897,14 @@ def test_time_shard_hook(jb):
     dx0 = torch.zeros(n, dtype=torch.float64, device="cuda")
     with jb.Plan(dA, n=n) as p:
         for P, r in ((1, 0), (4, 3), (8, 5)):
-            for mode in ("graph", "persistent", "persistent-push"):
+            for mode in ("graph", "persistent", "persistent-push", "colslab"):
                 ms, v = p.time_shard(db, dx0, P, r, 8, mode)
                 assert 0 < ms < 50, (P, r, mode, ms)
-                if mode == "graph":
+                if mode in ("graph", "colslab"):
                     assert jb.variant_name(v).startswith("k_sweep")
+        with pytest.raises(jb.JacobiError) as e:
+            p.time_shard(db, dx0, 2048, 0, 8, "colslab")  # slabs of 4 columns: not a multiple of 8
+        assert e.value.status == jb.EINVAL
         for bad in ((3, 0), (4, 4), (0, 0)):  # 3 does not divide 8192; rank out of range; no ranks
             with pytest.raises(jb.JacobiError) as e:
                 p.time_shard(db, dx0, bad[0], bad[1], 8, "graph")
