@@ -107,6 +107,7 @@ cudaError_t launch_copy_pitched(int dtype, const void* src, int64_t src_ld, void
 int num_variants();
 const char* variant_name(int variant);
 int default_variant(int dtype, int nchunks, int chunk, bool l2_keep, int64_t rows, int num_sms);
+int slab_variant(int dtype, int nchunks, int chunk, int fallback);  // column slabs (ncols < n)
 bool variant_is_cta(int variant);
 bool variant_is_push(int variant);
 int push_variant(int dtype, int64_t rows, int num_sms);

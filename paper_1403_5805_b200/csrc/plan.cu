@@ -131,6 +131,7 @@ static void choose_variant_for(const jacobi_plan* p, int64_t ncols, int64_t rows
                                int* grid) {
   const int nch = (int)((ncols + p->chunk - 1) / p->chunk);
   int v = jacobi::default_variant(p->dtype, nch, p->chunk, l2_keep_pm > 0, rows, p->num_sms);
+  if (ncols < p->n) v = jacobi::slab_variant(p->dtype, nch, p->chunk, v);  // a column slab (NEXT-4)
   if (const char* e = getenv("JACOBI_SWEEP_VARIANT")) {  // tuning override (all variants: same bits)
     const int vi = atoi(e);
     if (vi >= 0 && vi < jacobi::num_variants() && !jacobi::variant_is_push(vi) &&

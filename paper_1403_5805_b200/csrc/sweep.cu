@@ -1568,6 +1568,18 @@ int default_variant(int dtype, int nchunks, int chunk, bool l2_keep, int64_t row
   if (variant_fits(big, nchunks, dtype, chunk)) return big;
   return dtype == JACOBI_F32 ? 0 : 1;  // item kernel: fits every chunk
 }
+// Column slabs (NEXT-4: all n rows, m < n columns) with fewer than 16 column chunks, where
+// default_variant falls back to the item kernel: per-rank slab rates (jacobi_plan_time_shard mode 3,
+// profiles/colslab_rates_r02.txt), item R8 U1 / R4 U2 / panel / group GB/s: c3 P = 2 (8 chunks) 6374 /
+// 6357 / 6220 / 6683, P = 4 (4) 5989 / 6148 / 6228 / 6345, P = 8 (2) 5152 / 5594 / 5536 / 4631; c4 P = 8 (8)
+// 6833 / 6674 / 6998 / 7072; c5 P = 8 (8, fp32) 6233 / 6605 / 6942 / 7052.  The group kernel from 4
+// chunks up, the item kernel R4 U2 below.
+int slab_variant(int dtype, int nchunks, int chunk, int fallback) {
+  if (nchunks >= 16) return fallback;
+  if (nchunks >= 4 && variant_fits(12, nchunks, dtype, chunk)) return 12;
+  if (variant_fits(0, nchunks, dtype, chunk)) return 0;
+  return fallback;
+}
 int variant_rows(int v) { return kVariants[v].R; }
 int variant_threads(int v) { return kVariants[v].threads; }
 
