@@ -128,10 +128,12 @@ static int l2_keep_for(int l2, int64_t a_rows, int64_t a_cols, int dtype, int nu
 // Sweep-kernel variant for a GEMV over `ncols` columns and `rows` rows per launch (default from
 // measurements; the JACOBI_SWEEP_VARIANT override is honoured when the variant can tile the chunking).
 static void choose_variant_for(const jacobi_plan* p, int64_t ncols, int64_t rows, int l2_keep_pm, int* variant,
-                               int* grid) {
+                               int* grid, bool compact_slab = false) {
   const int nch = (int)((ncols + p->chunk - 1) / p->chunk);
   int v = jacobi::default_variant(p->dtype, nch, p->chunk, l2_keep_pm > 0, rows, p->num_sms);
-  if (ncols < p->n) v = jacobi::slab_variant(p->dtype, nch, p->chunk, v);  // a column slab (NEXT-4)
+  // a rank's compact column slab (NEXT-4; the 1-GPU P-slab emulation reads strided slabs of the whole A
+  // and keeps the default: 380 vs 390 µs per c3 sweep as 8 slabs)
+  if (compact_slab && ncols < p->n) v = jacobi::slab_variant(p->dtype, nch, p->chunk, v);
   if (const char* e = getenv("JACOBI_SWEEP_VARIANT")) {  // tuning override (all variants: same bits)
     const int vi = atoi(e);
     if (vi >= 0 && vi < jacobi::num_variants() && !jacobi::variant_is_push(vi) &&
@@ -142,7 +144,8 @@ static void choose_variant_for(const jacobi_plan* p, int64_t ncols, int64_t rows
   *grid = jacobi::sweep_grid(p->dtype, v, p->num_sms, nch, p->chunk);
 }
 static void choose_variant(const jacobi_plan* p, int64_t ncols, int* variant, int* grid) {
-  choose_variant_for(p, ncols, p->colwise ? p->n : p->m / p->nblocks, p->l2_keep_pm, variant, grid);
+  choose_variant_for(p, ncols, p->colwise ? p->n : p->m / p->nblocks, p->l2_keep_pm, variant, grid,
+                     p->colwise && ncols == p->m);
 }
 
 // Common plan setup.  The stored block of A is a_rows x a_cols (row-major, lda): the m x n row block
@@ -1104,7 +1107,7 @@ extern "C" int jacobi_plan_time_shard(jacobi_plan* p, int nranks, int rank, cons
   if (mode == 3) {  // NEXT-4: rank `rank`'s n x m column slab (columns [r0, r0 + m)) writing all n row sums,
     // stored as that rank stores it: a compact n x m block (lda = m), copied out of this plan's A
     const int keep3 = l2_keep_for(l2, p->n, ms, p->dtype, p->num_sms);
-    choose_variant_for(p, ms, p->n, keep3, &v, &grid);
+    choose_variant_for(p, ms, p->n, keep3, &v, &grid, true);
     JLAST("slab variant");
     a = sweep_args(p, 0);
     a.col0 = r0;
