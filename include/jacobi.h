@@ -164,7 +164,8 @@ int jacobi_plan_time_sweeps(jacobi_plan* plan, const double* d_b, const double* 
  * (CUDA events around one warm launch of all sweeps) and, if variant_out is non-NULL, the sweep
  * variant (-1 / -2 for modes 1 / 2; the slab kernel's variant for mode 3).  Rows outside the shard keep x0, so the iterates are not the
  * system's: a measurement hook, not a solver.  Errors: EINVAL (distributed / emulating plan,
- * nranks does not divide n, bad arguments, persistent mode unsupported for this shape), ECUDA. */
+ * nranks does not divide n, bad arguments, persistent mode unsupported for this shape, mode 3 with
+ * n / nranks not a multiple of 8), ENOMEM (mode 3: no room for the slab copy), ECUDA. */
 int jacobi_plan_time_shard(jacobi_plan* plan, int nranks, int rank, const double* d_b, const double* d_x0,
                            int sweeps, int mode, float* ms_per_sweep, int* variant_out);
 

@@ -1112,9 +1112,18 @@ extern "C" int jacobi_plan_time_shard(jacobi_plan* p, int nranks, int rank, cons
     a = sweep_args(p, 0);
     a.col0 = r0;
     a.cend = r0 + ms;
-    JCUDA(cudaMalloc(&slab_A, (size_t)(p->n * ms * esz)));
-    JCUDA(cudaMemcpy2DAsync(slab_A, (size_t)(ms * esz), (const char*)p->dA + (size_t)(r0 * esz), (size_t)(p->lda * esz),
-                            (size_t)(ms * esz), (size_t)p->n, cudaMemcpyDeviceToDevice, p->stream));
+    cudaError_t e = cudaMalloc(&slab_A, (size_t)(p->n * ms * esz));
+    if (e == cudaSuccess) e = cudaMalloc(&slab_rsum, (size_t)p->n * 8);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(slab_A, (size_t)(ms * esz), (const char*)p->dA + (size_t)(r0 * esz), (size_t)(p->lda * esz),
+                            (size_t)(ms * esz), (size_t)p->n, cudaMemcpyDeviceToDevice, p->stream);
+    if (e != cudaSuccess) {  // nothing else is allocated yet
+      if (slab_A) cudaFree(slab_A);
+      if (slab_rsum) cudaFree(slab_rsum);
+      cudaGetLastError();
+      return jacobi_set_error(e == cudaErrorMemoryAllocation ? JACOBI_ENOMEM : JACOBI_ECUDA,
+                              std::string("jacobi_plan_time_shard (column slab): ") + cudaGetErrorString(e));
+    }
     a.A = slab_A;  // kernels index A by global column: row i, column c at A[i * lda + c - col0]
     a.lda = ms;
     a.a_base = slab_A;
@@ -1124,7 +1133,6 @@ extern "C" int jacobi_plan_time_shard(jacobi_plan* p, int nranks, int rank, cons
     a.nchunks = (int)((ms + p->chunk - 1) / p->chunk);
     a.tiles = (int)((p->n + jacobi::variant_rows_dt(v, p->dtype) - 1) / jacobi::variant_rows_dt(v, p->dtype));
     a.l2_keep_pm = keep3;
-    JCUDA(cudaMalloc(&slab_rsum, (size_t)p->n * 8));
     a.rsum = slab_rsum;
   }
   int rc = 0;
