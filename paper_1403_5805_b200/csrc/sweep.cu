@@ -355,7 +355,23 @@ __device__ __forceinline__ void accumulate_chunk(const T* const (&rowp)[R], cons
   }
 }
 
-template <typename T, int R, int U, int NT>
+// L2-resident share of A (POL instances).  The kept set is made of work units — (tile, column chunk[,
+// row group]) — not whole tiles: a unit is 16-64 KB, a tile up to 1 MB (8 rows of 16384 fp64), and an
+// L2 budget of ~60 MB is less than one tile per CTA once rows are that long (c3 shards).  Unit i of a
+// CTA's sequence (offset by a per-CTA phase) is kept iff frac(i * phi) < keep_pm / 1000 (a Weyl
+// sequence: the kept units are spread evenly along every CTA's sequence and every warp's share, and
+// the kept count is the share to within a couple of units), so at any moment some CTAs stream kept
+// units from L2 while others stream from HBM.  32-bit integer hash: two instructions per unit (an exact
+// Bresenham split needed 64-bit divisions and pushed the persistent kernels into register spills).
+// The same units are kept every sweep (static rows), so they hit in L2 from the second sweep on.
+__device__ __forceinline__ unsigned keep_threshold(int keep_pm) {
+  return keep_pm >= 1000 ? 0xffffffffu : (unsigned)(((unsigned long long)max(keep_pm, 0) << 32) / 1000ull);
+}
+__device__ __forceinline__ bool keep_unit(unsigned i, unsigned thr) { return i * 2654435769u < thr; }
+
+// POL: A loaded with an L2 policy per work item — evict_last for the kept share (keep_unit over the
+// item index, a.l2_keep_pm), evict_first for the rest (column slabs of a few chunks, NEXT-4).
+template <typename T, int R, int U, int NT, bool POL = false>
 __global__ void __launch_bounds__(NT, (NT < 512 ? 512 / NT : 1)) k_sweep(const SweepArgs a, const int j) {
   __shared__ int s_go;
   __shared__ long long s_k;
@@ -386,7 +402,9 @@ __global__ void __launch_bounds__(NT, (NT < 512 ? 512 / NT : 1)) k_sweep(const S
     for (int r = 0; r < R; ++r) acc[r] = 0.0;
 
     check_tile<T, R>(a, rowp, c0, c1);
-    accumulate_chunk<T, R, U>(rowp, R, xo, c0, c1, a.chunk, a.cend, g0, lane, acc);
+    uint64_t pol = 0;
+    if constexpr (POL) pol = l2_policy(keep_unit((unsigned)it, keep_threshold(a.l2_keep_pm)));
+    accumulate_chunk<T, R, U, 0, POL>(rowp, R, xo, c0, c1, a.chunk, a.cend, g0, lane, acc, pol);
     // Butterfly: every lane ends with the same, order-fixed row sums.
 #pragma unroll
     for (int r = 0; r < R; ++r)
@@ -462,19 +480,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
 
 constexpr int kSlots = 4;
 
-// L2-resident share of A (POL instances).  The kept set is made of work units — (tile, column chunk[,
-// row group]) — not whole tiles: a unit is 16-64 KB, a tile up to 1 MB (8 rows of 16384 fp64), and an
-// L2 budget of ~60 MB is less than one tile per CTA once rows are that long (c3 shards).  Unit i of a
-// CTA's sequence (offset by a per-CTA phase) is kept iff frac(i * phi) < keep_pm / 1000 (a Weyl
-// sequence: the kept units are spread evenly along every CTA's sequence and every warp's share, and
-// the kept count is the share to within a couple of units), so at any moment some CTAs stream kept
-// units from L2 while others stream from HBM.  32-bit integer hash: two instructions per unit (an exact
-// Bresenham split needed 64-bit divisions and pushed the persistent kernels into register spills).
-// The same units are kept every sweep (static rows), so they hit in L2 from the second sweep on.
-__device__ __forceinline__ unsigned keep_threshold(int keep_pm) {
-  return keep_pm >= 1000 ? 0xffffffffu : (unsigned)(((unsigned long long)max(keep_pm, 0) << 32) / 1000ull);
-}
-__device__ __forceinline__ bool keep_unit(unsigned i, unsigned thr) { return i * 2654435769u < thr; }
 
 // Fused exchange, end of sweep k in one CTA (thread 0, after a CTA barrier that follows every thread's
 // x stores): fold the CTA's max|dx| bits into every rank's distance slot, then — behind one system-scope
@@ -1478,6 +1483,9 @@ const Variant kVariants[] = {
     // row-panel kernel with 4 warps per 8-row tile (cta = 6: G = 4 warps per group), x ring as 6: fp32
     // default with few rows per SM (c5 shards at P >= 2)
     {"k_sweep_group R8 G4 x-smem", 8, 512, 6, 8, 1, 1, k_sweep_group<double, 8, 16, 4, 8>, k_sweep_group<float, 8, 16, 4, 8>},
+    // item kernel R4 U2 with the L2 policy on A: column slabs of fewer than 4 chunks (NEXT-4), whose
+    // L2-resident share the plain item kernel cannot keep
+    {"k_sweep R4 U2 L2-policy", 4, 512, 0, 4, 2, 1, k_sweep<double, 4, 2, 512, true>, k_sweep<float, 4, 1, 512, true>},
 };
 // Round 1 also compiled item kernels R2 U4 / R4 U1 / 256 and 1024 threads, CTA kernels R8 256t / R4 U2 /
 // R2 U4 / R4 fused-exchange / R4 L2-keep / rows/4 / R4 U1 dynamic, and panel kernels x-evict_last / R8 /
@@ -1573,11 +1581,13 @@ int default_variant(int dtype, int nchunks, int chunk, bool l2_keep, int64_t row
 // profiles/colslab_rates_r02.txt), item R8 U1 / R4 U2 / panel / group GB/s: c3 P = 2 (8 chunks) 6374 /
 // 6357 / 6220 / 6683, P = 4 (4) 5989 / 6148 / 6228 / 6345, P = 8 (2) 5152 / 5594 / 5536 / 4631; c4 P = 8 (8)
 // 6833 / 6674 / 6998 / 7072; c5 P = 8 (8, fp32) 6233 / 6605 / 6942 / 7052.  The group kernel from 4
-// chunks up, the item kernel R4 U2 below.
+// chunks up; below, the item kernel R4 U2 with the L2 policy (variant 13), which keeps the slab's
+// L2-resident share (c3 P = 8: 47.5 -> 40.0 us).  (A group instance with the L2 policy measured c3 P = 2
+// +2.3 %, P = 4 -0.2 %, c4 P = 8 -2.1 %: not kept.)
 int slab_variant(int dtype, int nchunks, int chunk, int fallback) {
   if (nchunks >= 16) return fallback;
   if (nchunks >= 4 && variant_fits(12, nchunks, dtype, chunk)) return 12;
-  if (variant_fits(0, nchunks, dtype, chunk)) return 0;
+  if (variant_fits(13, nchunks, dtype, chunk)) return 13;
   return fallback;
 }
 int variant_rows(int v) { return kVariants[v].R; }

@@ -86,7 +86,7 @@ def test_variant_names_without_gpu(jb):
     names = [jb.variant_name(v) for v in range(64)]
     assert names[0].startswith("k_sweep") and names[3] == "k_sweep_cta R4 U1"
     known = [n for n in names if not n.startswith("variant ")]
-    assert len(known) == 13 and len(set(known)) == len(known)
+    assert len(known) == 14 and len(set(known)) == len(known)
     assert jb._lib.jacobi_variant_name(-1) is None and jb._lib.jacobi_variant_name(10**6) is None
 
 
@@ -115,6 +115,7 @@ def test_default_variant_indices_keep_their_names(jb):
               4: "k_sweep_cta R8 U1 fused-exchange", 5: "k_sweep_panel R4 U1", 6: "k_sweep_panel R4 U1 x-smem",
               7: "k_sweep_cta R8 U1 L2-policy", 8: "k_sweep_cta R8 U1 L2-policy rows/2",
               9: "k_sweep_cta R8 U1 L2-policy dynamic", 10: "k_sweep_cta R4 U2 L2-policy dynamic",
-              11: "k_sweep_cta R4 U2 dynamic fused-exchange", 12: "k_sweep_group R8 G4 x-smem"}
+              11: "k_sweep_cta R4 U2 dynamic fused-exchange", 12: "k_sweep_group R8 G4 x-smem",
+              13: "k_sweep R4 U2 L2-policy"}
     for v, name in expect.items():
         assert jb.variant_name(v) == name, (v, jb.variant_name(v))
