@@ -714,6 +714,22 @@ def test_slabs_and_row_blocks_every_sweep_on_slow_companion(jb):
             assert np.array_equal(r.x, ref.x) and np.array_equal(r.hist, ref.hist), P
 
 
+@pytest.mark.parametrize("variant", [12, 13])
+def test_slab_kernels_every_sweep_on_slow_companion(jb, monkeypatch, variant):
+    """The kernels a rank's narrow column slab runs (slab_variant: the group kernel for 4-15 chunks,
+    the item kernel R4 U2 with the L2 policy for 2-3), forced onto the 1-GPU slab emulation: every d_k
+    and x against the oracle over 120 sweeps of the slow companion, P = 2/4/8 slabs."""
+    monkeypatch.setenv("JACOBI_SWEEP_VARIANT", str(variant))
+    n = 8192
+    A, b, _ = slow_companion(n, 8194)
+    x0 = np.random.default_rng(7).uniform(-1, 1, n)
+    orc = oracle.jacobi(A, b, x0, 120, 0.0, nthreads=16, history=True)
+    with jb.Plan(A) as p:
+        for P in (2, 4, 8):
+            p.set_col_blocks(P)
+            match_oracle(p.solve(b, x0, 120, 0.0, history=True), orc)
+
+
 @pytest.mark.parametrize("persist", ["0", "1"])
 def test_fused_exchange_every_sweep_on_slow_companion(jb, monkeypatch, persist):
     """NEXT-1's protocol pinned per sweep: P = 2/4/8 emulated ranks pushing
